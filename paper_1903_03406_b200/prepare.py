@@ -1,0 +1,61 @@
+"""Host-side setup shared by the GPU path and the test oracle.
+
+``refine()`` in the reference validates the PLC, closes the domain with a
+padded box and shuffles the insertion order before any meshing happens
+(/root/reference/pkg/src/tetrefine/refine.py:523-531, mesh.py:873-880).
+``prepare`` does exactly that and flattens the result into the plain arrays
+the C ABI takes.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import AllCoplanar, DuplicatePoint, InvalidPLC
+from .plc import PLC, augment_with_box, validate
+
+
+@dataclass
+class Prepared:
+    plc: PLC              # augmented PLC
+    n_input: int          # points of the caller's PLC (origin 0)
+    points: np.ndarray    # (n,3) float64, C-contiguous
+    segments: np.ndarray  # (m,2) int32
+    poly_off: np.ndarray  # (f+1,) int32
+    poly_idx: np.ndarray  # (sum,) int32
+    order: np.ndarray     # (n,) int32 insertion order
+    setup_s: float = 0.0
+
+
+def shuffle_order(n: int, seed: int) -> np.ndarray:
+    """mesh.py:878-880: list(range(n)) shuffled in place by default_rng(seed)."""
+    order = list(range(n))
+    np.random.default_rng(seed).shuffle(order)
+    return np.asarray(order, dtype=np.int32)
+
+
+def prepare(plc: PLC, seed: int = 0, check: bool = True) -> Prepared:
+    import time
+
+    t0 = time.perf_counter()
+    if check:
+        violations = validate(plc)
+        if violations:
+            raise InvalidPLC(violations)
+    aug = augment_with_box(plc)
+    pts = np.ascontiguousarray(np.asarray(aug.points, dtype=np.float64).reshape(-1, 3))
+    if len(pts) < 4:
+        raise AllCoplanar("need at least 4 points")
+    if len({tuple(p) for p in aug.points}) != len(aug.points):
+        raise DuplicatePoint("duplicate input points")
+    segs = np.ascontiguousarray(np.asarray(aug.segments, dtype=np.int32).reshape(-1, 2))
+    off = [0]
+    idx = []
+    for poly in aug.polygons:
+        idx.extend(poly)
+        off.append(len(idx))
+    return Prepared(plc=aug, n_input=len(plc.points), points=pts, segments=segs,
+                    poly_off=np.asarray(off, dtype=np.int32), poly_idx=np.asarray(idx, dtype=np.int32),
+                    order=shuffle_order(len(pts), seed), setup_s=time.perf_counter() - t0)
