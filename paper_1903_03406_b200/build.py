@@ -1,0 +1,41 @@
+"""Build libgqm3d.so in-tree for sm_100a (the only CUDA target)."""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libgqm3d.so")
+SRC = os.path.join(HERE, "csrc", "gq_main.cu")
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("gq_main.cu", "gq_dev.cuh", "gq_exact.cuh")] + \
+       [os.path.join(os.path.dirname(HERE), "include", "gqm3d.h")]
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              # no FMA contraction: float filters / constructions must round
+              # exactly like the reference's
+              "-fmad=false", "-Xcompiler", "-fPIC", "-shared"]
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(SO):
+        return False
+    t = os.path.getmtime(SO)
+    return all(os.path.getmtime(d) <= t for d in DEPS)
+
+
+def build(force: bool = False, verbose: bool = True) -> str:
+    if not force and up_to_date():
+        return SO
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-o", SO + ".tmp", SRC]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+    os.replace(SO + ".tmp", SO)
+    return SO
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)

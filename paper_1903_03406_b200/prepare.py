@@ -59,3 +59,30 @@ def prepare(plc: PLC, seed: int = 0, check: bool = True) -> Prepared:
     return Prepared(plc=aug, n_input=len(plc.points), points=pts, segments=segs,
                     poly_off=np.asarray(off, dtype=np.int32), poly_idx=np.asarray(idx, dtype=np.int32),
                     order=shuffle_order(len(pts), seed), setup_s=time.perf_counter() - t0)
+
+
+def facet_keep(plc: PLC) -> np.ndarray:
+    """Projection axes (i, j) of every polygon, ordered so the projected
+    boundary is counterclockwise (facets.py:256-273, exact)."""
+    from fractions import Fraction
+
+    from .plc import _proj_axis
+
+    out = np.zeros((len(plc.polygons), 2), dtype=np.int32)
+    cache = {}
+    for pid, poly in enumerate(plc.polygons):
+        pts = [plc.points[v] for v in poly]
+        axis = _proj_axis(pts)
+        i, j = [k for k in range(3) if k != axis]
+        # exact signed area of the projected cycle
+        tot = Fraction(0)
+        n = len(pts)
+        for k in range(n):
+            x0, y0 = Fraction(pts[k][i]), Fraction(pts[k][j])
+            x1, y1 = Fraction(pts[(k + 1) % n][i]), Fraction(pts[(k + 1) % n][j])
+            tot += x0 * y1 - x1 * y0
+        if tot < 0:
+            i, j = j, i
+        out[pid] = (i, j)
+    del cache
+    return out
