@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 namespace orc {
 
@@ -596,7 +597,27 @@ struct Driver {
     return false;
   }
 
+  // debug: compare the reference's global new-vertex query with the
+  // mesh-local shortcut (constraints on the inserted cavities' boundaries)
+  bool dbg_local = std::getenv("ORACLE_DEBUG_LOCAL") != nullptr;
+  long long dbg_missed = 0;
   void post_round() {   // refine.py:816-858
+    if (dbg_local) {
+      for (int v : round_new_verts) {
+        std::vector<uint64_t> s; std::vector<K3> fcs;
+        encroached_by_point(mesh.pt(v), &s, &fcs);
+        for (auto k : s) {
+          if (skipped_seg(k) || enc_segs.count(k)) continue;
+          bool covered = round_dirty_segs.count(k) || std::find(round_new_segs.begin(), round_new_segs.end(), k) != round_new_segs.end();
+          if (!covered) { dbg_missed++; std::fprintf(stderr, "[local] new vertex %d encroaches non-dirty subsegment (%d,%d)\n", v, k2u(k), k2v(k)); }
+        }
+        for (auto& k : fcs) {
+          if (skipped_face(k) || enc_faces.count(k)) continue;
+          bool covered = round_dirty_faces.count(k) || std::find(round_new_faces.begin(), round_new_faces.end(), k) != round_new_faces.end();
+          if (!covered) { dbg_missed++; std::fprintf(stderr, "[local] new vertex %d encroaches non-dirty subface (%d,%d,%d)\n", v, k.a, k.b, k.c); }
+        }
+      }
+    }
     for (int v : round_new_verts) {
       std::vector<uint64_t> s; std::vector<K3> fcs;
       encroached_by_point(mesh.pt(v), &s, &fcs);
@@ -609,6 +630,34 @@ struct Driver {
     std::set<K3> cf;
     for (auto& k : round_new_faces) if (mesh.subfaces.count(k)) cf.insert(k);
     for (auto& k : round_dirty_faces) if (mesh.subfaces.count(k)) cf.insert(k);
+    if (dbg_local) {
+      for (auto k : cs) {
+        if (skipped_seg(k) || enc_segs.count(k)) continue;
+        bool g = !mesh.edge_exists(k2u(k), k2v(k)) || seg_encroached_scan(k);
+        bool l = false;
+        auto ring = mesh.tets_around_edge(k2u(k), k2v(k));
+        if (ring.empty()) l = true;
+        for (int t : ring) for (int q = 0; q < 4; ++q) {
+          int w = mesh.tv[4 * (size_t)t + q];
+          if (w != GHOST && w != k2u(k) && w != k2v(k) && encroaches_segment(mesh.pt(k2u(k)), mesh.pt(k2v(k)), mesh.pt(w))) l = true;
+        }
+        if (g != l) { dbg_missed++; std::fprintf(stderr, "[local2] seg (%d,%d) global %d local %d\n", k2u(k), k2v(k), g, l); }
+      }
+      for (auto& k : cf) {
+        if (skipped_face(k) || enc_faces.count(k)) continue;
+        auto ti = mesh.find_tet_with_face(k);
+        bool g = ti.first < 0 || face_encroached_scan(k);
+        bool l = ti.first < 0;
+        if (!l) {
+          int w = mesh.tv[4 * (size_t)ti.first + ti.second];
+          int u = mesh.nbt(ti.first, ti.second), j = (int)(mesh.tn[4 * (size_t)ti.first + ti.second] & 3);
+          int w2 = mesh.tv[4 * (size_t)u + j];
+          if (w != GHOST && encroaches_face(mesh.pt(k.a), mesh.pt(k.b), mesh.pt(k.c), mesh.pt(w))) l = true;
+          if (w2 != GHOST && encroaches_face(mesh.pt(k.a), mesh.pt(k.b), mesh.pt(k.c), mesh.pt(w2))) l = true;
+        }
+        if (g != l) { dbg_missed++; std::fprintf(stderr, "[local2] face (%d,%d,%d) global %d local %d\n", k.a, k.b, k.c, g, l); }
+      }
+    }
     for (auto k : cs) {
       if (skipped_seg(k) || enc_segs.count(k)) continue;
       if (!mesh.edge_exists(k2u(k), k2v(k)) || seg_encroached_scan(k)) enc_segs.insert(k);

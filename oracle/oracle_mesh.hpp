@@ -14,6 +14,7 @@
 #include <functional>
 #include <map>
 #include <set>
+#include <cstdlib>
 
 namespace orc {
 
@@ -622,6 +623,54 @@ struct Mesh {
     compute_ratio(t0);
     int hint = t0;
     std::unordered_set<int> done(first.begin(), first.end());
+    if (std::getenv("ORACLE_PARALLEL_INIT")) {
+      std::vector<int> pend;
+      for (int k = 0; k < n; ++k) if (!done.count(order[k])) pend.push_back(order[k]);
+      std::vector<int> hints(pend.size(), t0);
+      size_t off = 0;
+      int inserted = 4;
+      while (off < pend.size()) {
+        size_t nwin = std::min(pend.size() - off, (size_t)std::max(256, 2 * inserted));
+        std::vector<Region> regs(nwin);
+        for (size_t k = 0; k < nwin; ++k) {
+          const double* p = pt(pend[off + k]);
+          double pc[3] = {p[0], p[1], p[2]};
+          int h = hints[off + k];
+          if (h < 0 || h >= nt || !alive[h]) h = t0;
+          int s0 = walk(pc, h);
+          hints[off + k] = s0;
+          regs[k] = delaunay_region(pc, {s0}, nullptr);
+        }
+        // greedy by order over claims
+        std::unordered_set<int64_t> claimed;
+        std::vector<char> acc(nwin, 0);
+        for (size_t k = 0; k < nwin; ++k) {
+          std::vector<int64_t> ks;
+          for (int t : regs[k].tets) ks.push_back(t);
+          for (auto& bf : regs[k].bfaces) {
+            int64_t a = 4 * (int64_t)bf.first + bf.second, b = tn[4 * (size_t)bf.first + bf.second];
+            ks.push_back((int64_t)1 << 40 | std::min(a, b));
+          }
+          bool clash = false;
+          for (auto x : ks) if (claimed.count(x)) { clash = true; break; }
+          for (auto x : ks) claimed.insert(x);   // pending points block later ones either way
+          acc[k] = !clash;
+        }
+        std::vector<int> np, nh;
+        for (size_t k = 0; k < nwin; ++k) {
+          if (acc[k]) {
+            const double* p = pt(pend[off + k]);
+            double pc[3] = {p[0], p[1], p[2]};
+            insert_point(pc, regs[k], 0, nullptr, {}, {}, pend[off + k]);
+            ++inserted;
+          } else { np.push_back(pend[off + k]); nh.push_back(hints[off + k]); }
+        }
+        size_t newoff = off + nwin - np.size();
+        for (size_t k = 0; k < np.size(); ++k) { pend[newoff + k] = np[k]; hints[newoff + k] = nh[k]; }
+        off = newoff;
+      }
+      return;
+    }
     for (int k = 0; k < n; ++k) {
       int idx = order[k];
       if (done.count(idx)) continue;

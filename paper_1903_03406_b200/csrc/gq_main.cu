@@ -378,6 +378,118 @@ __global__ void k_redirect(Dev D, Cand C, int n0, int n1) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// constraint-ball grid: the reference's ConstraintIndex (refine.py:107-253)
+// on the device.  Every live subsegment / subface ball is linked into the
+// uniform cells its bounding box overlaps (balls spanning > 64 cells go to a
+// side list).  Queries enumerate candidates; decisions are the exact open-ball
+// predicates.  Records are only appended, so registration is incremental and
+// dead records are skipped at query time.
+struct CGrid {
+  double lo[3], inv[3];
+  int G;
+  int* head;          // G^3
+  int2* nodes;        // {code = 2*rec + kind, next}
+  int* nnodes;
+  int node_cap;
+  int* big;
+  int* nbig;
+  int big_cap;
+};
+__device__ __forceinline__ int cg_ci(const CGrid& g, double x, int k) {
+  double f = (x - g.lo[k]) * g.inv[k];
+  if (!(f >= 0.0)) return 0;
+  if (f >= (double)g.G) return g.G - 1;
+  return (int)f;
+}
+__device__ inline bool cons_ball(const Dev& D, int kind, int r, double* c, double& r2) {
+  if (kind == 0) {
+    int2 e = D.sg_uv[r];
+    const double *pu = PT(D, e.x), *pv = PT(D, e.y);
+    for (int k = 0; k < 3; ++k) c[k] = (pu[k] + pv[k]) / 2.0;
+    r2 = (pu[0] - c[0]) * (pu[0] - c[0]) + (pu[1] - c[1]) * (pu[1] - c[1]) + (pu[2] - c[2]) * (pu[2] - c[2]);
+    return true;
+  }
+  int4 f = D.sf_v[r];
+  Sphere s;
+  if (!circumcircle_tri(PT(D, f.x), PT(D, f.y), PT(D, f.z), s)) return false;
+  c[0] = s.c[0]; c[1] = s.c[1]; c[2] = s.c[2]; r2 = s.r2;
+  return true;
+}
+__global__ void k_grid_register(Dev D, CGrid g, int kind, int r0, int r1) {
+  for (int r = r0 + blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += gridDim.x * blockDim.x) {
+    unsigned int fl = kind == 0 ? D.sg_fl[r] : D.sf_fl[r];
+    if (!(fl & RF_LIVE)) continue;
+    double c[3], r2;
+    if (!cons_ball(D, kind, r, c, r2)) continue;
+    double rr = sqrt(r2) * (1.0 + 1e-9) + 1e-300;
+    int i0 = cg_ci(g, c[0] - rr, 0), i1 = cg_ci(g, c[0] + rr, 0);
+    int j0 = cg_ci(g, c[1] - rr, 1), j1 = cg_ci(g, c[1] + rr, 1);
+    int k0 = cg_ci(g, c[2] - rr, 2), k1 = cg_ci(g, c[2] + rr, 2);
+    long long nc = (long long)(i1 - i0 + 1) * (j1 - j0 + 1) * (k1 - k0 + 1);
+    int code = 2 * r + kind;
+    if (nc > 64) {
+      int b = atomicAdd(g.nbig, 1);
+      if (b < g.big_cap) g.big[b] = code; else raise_err(GQ_ERR_CAP);
+      continue;
+    }
+    for (int i = i0; i <= i1; ++i) for (int j = j0; j <= j1; ++j) for (int k = k0; k <= k1; ++k) {
+      int nd = atomicAdd(g.nnodes, 1);
+      if (nd >= g.node_cap) { raise_err(GQ_ERR_CAP); return; }
+      int cell = (i * g.G + j) * g.G + k;
+      g.nodes[nd].x = code;
+      g.nodes[nd].y = atomicExch(g.head + cell, nd);
+    }
+  }
+}
+// visit every live constraint whose open ball strictly contains p
+template <class F>
+__device__ inline void grid_encroached(const Dev& D, const CGrid& g, const double* p, int kinds, F f) {
+  int cell = (cg_ci(g, p[0], 0) * g.G + cg_ci(g, p[1], 1)) * g.G + cg_ci(g, p[2], 2);
+  auto test = [&](int code) {
+    int kind = code & 1, r = code >> 1;
+    if (!((kinds >> kind) & 1)) return;
+    if (kind == 0) {
+      if (!(D.sg_fl[r] & RF_LIVE)) return;
+      int2 e = D.sg_uv[r];
+      if (encroaches_segment(PT(D, e.x), PT(D, e.y), p)) f(0, r);
+    } else {
+      if (!(D.sf_fl[r] & RF_LIVE)) return;
+      int4 q = D.sf_v[r];
+      if (encroaches_face(PT(D, q.x), PT(D, q.y), PT(D, q.z), p)) f(1, r);
+    }
+  };
+  for (int nd = g.head[cell]; nd >= 0; nd = g.nodes[nd].y) test(g.nodes[nd].x);
+  int nb = *g.nbig;
+  for (int b = 0; b < nb; ++b) test(g.big[b]);
+}
+// post_round part 1 (refine.py:818-828): new vertices against all balls
+__global__ void k_grid_newverts(Dev D, CGrid g, int v0, int v1) {
+  for (int v = v0 + blockIdx.x * blockDim.x + threadIdx.x; v < v1; v += gridDim.x * blockDim.x) {
+    grid_encroached(D, g, PT(D, v), 3, [&](int kind, int r) {
+      unsigned int* fl = kind == 0 ? D.sg_fl + r : D.sf_fl + r;
+      if (!(*fl & RF_SKIP)) atomicOr(fl, RF_ENC);
+    });
+  }
+}
+// redirect hits of candidate points (refine.py:603-613, 636-654)
+__global__ void k_grid_cands(Dev D, CGrid g, Cand C, int n0, int n1) {
+  for (int c = n0 + blockIdx.x * blockDim.x + threadIdx.x; c < n1; c += gridDim.x * blockDim.x) {
+    int kind = C.kind[c];
+    C.nrseg[c] = 0; C.nrface[c] = 0;
+    if (kind == K_SEG || C.status[c] == CS_DROP) continue;
+    int ns = 0, nf = 0;
+    int* rs = C.rseg + (size_t)c * CRD;
+    int* rf = C.rface + (size_t)c * CRD;
+    grid_encroached(D, g, C.p + 3 * (size_t)c, kind == K_TET ? 3 : 1, [&](int k, int r) {
+      if (k == 0) { if (D.sg_fl[r] & RF_SKIP) return; if (ns < CRD) rs[ns++] = r; else raise_err(GQ_ERR_CAP); }
+      else { if (D.sf_fl[r] & RF_SKIP) return; if (nf < CRD) rf[nf++] = r; else raise_err(GQ_ERR_CAP); }
+    });
+    C.nrseg[c] = ns; C.nrface[c] = nf;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // filter: fixed-priority local-minimum iterations == greedy_oracle
 struct Owners { int* own; int toff, foff, soff; };   // [tets | faces (4*tcap) | seg records]
@@ -429,6 +541,10 @@ __global__ void k_reject(Dev D, Cand C, Owners W, int n, int* undecided) {
     if (hit) C.state[c] = 2;
     else atomicAdd(undecided, 1);
   }
+}
+__global__ void k_strict_state(Cand C, int n) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+    C.state[c] = C.state[c] == 10 ? 1 : 2;
 }
 __global__ void k_reset_claims(Dev D, Cand C, Owners W, int n, int all) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
@@ -1346,6 +1462,8 @@ struct gq_ctx {
   double init_ms = 0, dev_ms = 0, region_ms = 0;
   cudaEvent_t ev0, ev1, er0, er1;
   std::vector<std::vector<int>> polys;
+  CGrid G{};
+  int reg_seg = 0, reg_face = 0, reg_nv = 0;
   bool allocated = false;
 };
 
@@ -1541,6 +1659,21 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   alloc_scratch(c->S, 16384, CT * 2, 1024, 2048);
   alloc_scratch(c->SB, 128, CTB * 2, 16384, 65536);
   alloc_cands(c, 1 << 16, 256);
+  {
+    int g = (int)std::cbrt(std::max(1.0, n / 2.0));
+    g = std::min(std::max(g, 4), 160);
+    c->G.G = g;
+    c->G.head = dmalloc<int>((size_t)g * g * g);
+    CK(cudaMemset(c->G.head, 0xff, (size_t)g * g * g * 4));
+    c->G.node_cap = (int)std::min<size_t>(((size_t)sgcap + sfcap) * 8, (size_t)1 << 30);
+    c->G.nodes = dmalloc<int2>(c->G.node_cap);
+    c->G.big_cap = 1 << 20;
+    c->G.big = dmalloc<int>(c->G.big_cap);
+    c->G.nnodes = dmalloc<int>(2);
+    c->G.nbig = c->G.nnodes + 1;
+    CK(cudaMemset(c->G.nnodes, 0, 8));
+    c->reg_seg = c->reg_face = 0;
+  }
   c->allocated = true;
 }
 
@@ -1554,7 +1687,7 @@ static void free_all(gq_ctx* c) {
                 c->S.tkey, c->S.tval, c->S.tep, c->S.fkey, c->S.fep, c->S.epoch, c->S.list, c->S.stack, c->S.in,
                 c->S.comp, c->SB.tkey, c->SB.tval, c->SB.tep, c->SB.fkey, c->SB.fep, c->SB.epoch, c->SB.list,
                 c->SB.stack, c->SB.in, c->SB.comp, c->tmpA, c->tmpB, c->tmpC, c->k64a, c->k64b, c->k32a, c->k32b,
-                c->cub_tmp, c->d_order};
+                c->cub_tmp, c->d_order, c->G.head, c->G.nodes, c->G.big, c->G.nnodes};
   for (void* p : ps) if (p) cudaFree(p);
   free_cands(c->C);
   c->allocated = false;
@@ -1633,6 +1766,15 @@ static void run_filter(gq_ctx* c, int n, int* nacc_out) {
   (void)nacc_out;
 }
 
+// bulk construction: a point goes in this round only if no lower-order
+// pending point claims any of its elements (so it commutes with all of them)
+static void run_filter_strict(gq_ctx* c, int n) {
+  LAUNCH(k_claim, n, c->D, c->C, c->W, n);
+  LAUNCH(k_decide, n, c->D, c->C, c->W, n, 0);
+  LAUNCH(k_reset_claims, n, c->D, c->C, c->W, n, 1);
+  LAUNCH(k_strict_state, n, c->C, n);
+}
+
 static void upload_candidates(gq_ctx* c, int n0, const std::vector<int>& kinds, const std::vector<int>& tgts,
                               const std::vector<int>& pool) {
   int n = (int)tgts.size();
@@ -1702,6 +1844,13 @@ static std::vector<int> pending_sorted(gq_ctx* c, int phase) {
       return fv[a].z < fv[b].z; });
   }
   return recs;
+}
+
+// register records created since the last call (ConstraintIndex.add_*)
+static void grid_sync(gq_ctx* c) {
+  pull(c);
+  if (c->hc.nsegrec > c->reg_seg) { LAUNCH(k_grid_register, c->hc.nsegrec - c->reg_seg, c->D, c->G, 0, c->reg_seg, c->hc.nsegrec); c->reg_seg = c->hc.nsegrec; }
+  if (c->hc.nfacerec > c->reg_face) { LAUNCH(k_grid_register, c->hc.nfacerec - c->reg_face, c->D, c->G, 1, c->reg_face, c->hc.nfacerec); c->reg_face = c->hc.nfacerec; }
 }
 
 static bool full_verify(gq_ctx* c) {
@@ -1804,7 +1953,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     for (int k = 0; k < nwin; ++k) rk[k] = k;
     CK(cudaMemcpyAsync(c->C.rank, rk.data(), 4 * nwin, cudaMemcpyHostToDevice, c->st));
     CK(cudaMemcpyAsync(c->C.state, s0.data(), 4 * nwin, cudaMemcpyHostToDevice, c->st));
-    run_filter(c, nwin, nullptr);
+    run_filter_strict(c, nwin);
     std::vector<int> state(nwin), nbf(nwin);
     CK(cudaMemcpyAsync(state.data(), c->C.state, 4 * nwin, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(nbf.data(), c->C.nbf, 4 * nwin, cudaMemcpyDeviceToHost, c->st));
@@ -1975,7 +2124,9 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     upload_candidates(c, 0, kinds, tgts, pool);
     nbase = (int)tgts.size();
     LAUNCH_S(k_make_cands, nbase, c->D, c->C, c->S, 0, nbase, X, c->L, lmin2);
-    run_regions(c, 0, nbase, phase == 1 ? 1 : 2);
+    run_regions(c, 0, nbase, 0);
+    grid_sync(c);
+    LAUNCH(k_grid_cands, nbase, c->D, c->G, c->C, 0, nbase);
     LAUNCH(k_redirect, nbase, c->D, c->C, 0, nbase);
     sync(c);
     std::vector<int> rs = take_redirects(c, 0);
@@ -2050,9 +2201,12 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     R.inserted += read_int(c, c->d_int + 20);
     pull(c);
   }
-  // post round
+  // post round: new vertices vs every constraint ball, then new / dirty
+  // constraints vs the vertices around them
+  grid_sync(c);
+  if (c->hc.nv > c->reg_nv) LAUNCH(k_grid_newverts, c->hc.nv - c->reg_nv, c->D, c->G, c->reg_nv, c->hc.nv);
+  c->reg_nv = c->hc.nv;
   CK(cudaMemsetAsync(c->d_int, 0, 16, c->st));
-  pull(c);
   LAUNCH_S(k_check, c->hc.nsegrec + c->hc.nfacerec, c->D, c->S, 0, c->d_int);
   if (R.inserted > 0) LAUNCH(k_clear_flag, c->hc.nsegrec + c->hc.nfacerec, c->D, RF_BLOCK);
   sync(c);
@@ -2165,6 +2319,13 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   }
   LAUNCH(k_refresh_all, c->hc.nt, D);
   sync(c);
+  for (int k = 0; k < 3; ++k) {
+    c->G.lo[k] = lo[k];
+    double ext = hi[k] - lo[k];
+    c->G.inv[k] = ext > 0 ? c->G.G / ext : 0.0;
+  }
+  grid_sync(c);
+  c->reg_nv = c->hc.nv;
   full_verify(c);
   // rounds (refine.py:866-925)
   int round_no = 0;
