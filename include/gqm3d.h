@@ -48,7 +48,7 @@ typedef struct {
   double init_ms;              /* of which bulk Delaunay construction */
   int64_t kernel_launches;
   int64_t region_calls;
-  int64_t bytes_alg;           /* algorithmic HBM bytes (SURVEY 8(d) formula) */
+  int64_t bytes_alg;           /* region kernels' algorithmic HBM bytes (58 B/tet tested + 24 B/point) */
   double region_ms;            /* time in the region (cavity) kernels */
 } gq_counts;
 

@@ -293,9 +293,9 @@ __global__ void k_region(Dev D, Cand C, Scr SC, int n0, int n1, const int* list,
   Scratch S = scratch_for(SC, tid);
   int n = list ? n1 : n1 - n0;
   for (int w = tid; w < n; w += gridDim.x * blockDim.x) {
-    int c = list ? list[w] : n0 + w;
+    int c = list ? list[w] : n0 + w;   // with a list, n0 is the first big slab
     if (C.status[c] != CS_OK && !(big && C.status[c] == CS_OVF)) continue;
-    if (big) C.bigi[c] = w;
+    if (big) C.bigi[c] = n0 + w;
     SlabView v = slab(C, c);
     int seeds[32];
     int ns = cand_seeds(D, C, c, seeds, S);
@@ -305,9 +305,9 @@ __global__ void k_region(Dev D, Cand C, Scr SC, int n0, int n1, const int* list,
     atomicAdd(&g_region_calls, 1ull);
     int st = ns == 0 ? RS_CNSS : region_compute(D, C.p + 3 * (size_t)c, seeds, ns, allow_of(C, c), S, O);
     store_region(C, c, O);
+    if (st == RS_OK) atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf));
     if (st == RS_OK) {
       C.status[c] = (O.mind <= D.too_close_sq) ? CS_TOOCLOSE : CS_OK;
-      atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf));
     } else if (st == RS_OVERFLOW) {
       C.status[c] = big ? CS_CNSS : CS_OVF;
       if (big) raise_err(GQ_ERR_CAP);
@@ -971,14 +971,27 @@ __global__ void k_init_first(Dev D, const int* order, int n, int* first_out) {
   for (int k = 0; k < 4; ++k) first_out[k] = first[k];
 }
 
-// window points: locate + cavity; candidate c <-> pending position c
-__global__ void k_init_region(Dev D, Cand C, Scr SC, const int* pend, int* hint, int nwin, const int* succ) {
+// Candidate c == pending point c (its position in the insertion order after
+// the first tet).  A point's cavity stays cached across rounds while all its
+// tets are alive and none of them was rewired since it was computed.
+__global__ void k_init_region(Dev D, Cand C, Scr SC, const int* pend, const int* plist, int W, int* hint,
+                              const int* succ, const int* touched, int round, int big) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   Scratch S = scratch_for(SC, tid);
-  for (int c = tid; c < nwin; c += gridDim.x * blockDim.x) {
-    if (C.status[c] != CS_OK && C.status[c] != CS_OVF) continue;
-    bool big = C.status[c] == CS_OVF;
-    if (big && C.bigi[c] < 0) continue;
+  for (int w = tid; w < W; w += gridDim.x * blockDim.x) {
+    int c = plist[w];
+    int st = C.status[c];
+    if (big) { if (st != CS_OVF || C.bigi[c] < 0) continue; }
+    else if (st == CS_OK && C.memb[c] >= 0) {
+      // cached: valid unless a cavity tet died or was rewired after round memb[c]
+      SlabView v = slab(C, c);
+      bool ok = true;
+      for (int k = 0; k < C.ntet[c] && ok; ++k) {
+        int t = v.tets[k];
+        if (!D.alive[t] || touched[t] >= C.memb[c]) ok = false;   // rewired at/after computation
+      }
+      if (ok) continue;
+    } else if (st == CS_OVF) continue;   // waits for the big pass
     int v = pend[c];
     const double* p = PT(D, v);
     int h = hint[c];
@@ -990,28 +1003,88 @@ __global__ void k_init_region(Dev D, Cand C, Scr SC, const int* pend, int* hint,
     int seeds[1] = {t};
     Allow A; A.n = 0;
     atomicAdd(&g_region_calls, 1ull);
-    int st = region_compute(D, p, seeds, 1, A, S, O, true);
+    int r = region_compute(D, p, seeds, 1, A, S, O, true);
     store_region(C, c, O);
-    C.extra[c] = -1; C.kind[c] = K_TET;
-    if (st == RS_OK) C.status[c] = CS_OK;
-    else if (st == RS_OVERFLOW) { C.status[c] = CS_OVF; if (big) raise_err(GQ_ERR_CAP); }
+    C.extra[c] = -1; C.kind[c] = K_TET; C.rank[c] = c; C.memb[c] = round;
+    if (r == RS_OK) { C.status[c] = CS_OK; atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf)); }
+    else if (r == RS_OVERFLOW) { C.status[c] = CS_OVF; C.memb[c] = -1; if (big) raise_err(GQ_ERR_CAP); }
     else { C.status[c] = CS_CNSS; raise_err(GQ_ERR_DEGEN); }
   }
 }
-__global__ void k_init_star(Dev D, Cand C, const int* pend, const int* acc, int nacc, int* succ) {
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nacc; k += gridDim.x * blockDim.x) {
-    int c = acc[k];
-    SlabView v = slab(C, c);
-    if (C.mind[c] <= D.too_close_sq) raise_err(GQ_ERR_DEGEN);
-    for (int j = 0; j < C.ntet[c]; ++j) { D.alive[v.tets[j]] = 0; succ[v.tets[j]] = C.nt0[c]; }
+// window filter: claims of every window point, strict lower-order rule
+__global__ void k_init_claim(Dev D, Cand C, Owners W, const int* plist, int nw) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
+    int c = plist[w];
+    for_claims(D, C, W, c, [&](int k) { atomicMin(W.own + k, c); });
   }
 }
-__global__ void k_init_star2(Dev D, Cand C, const int* pend, const int* acc, int nacc) {
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nacc; k += gridDim.x * blockDim.x) {
-    int c = acc[k];
-    SlabView v = slab(C, c);
-    star_insert(D, pend[c], v.bf, C.nbf[c], C.nt0[c], true);
+__global__ void k_init_decide(Dev D, Cand C, Owners W, const int* plist, int nw, int* acc) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
+    int c = plist[w];
+    bool win = true;
+    for_claims(D, C, W, c, [&](int k) { if (W.own[k] != c) win = false; });
+    acc[w] = win ? 1 : 0;
   }
+}
+__global__ void k_init_unclaim(Dev D, Cand C, Owners W, const int* plist, int nw) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x)
+    for_claims(D, C, W, plist[w], [&](int k) { W.own[k] = INT_MAX; });
+}
+// accepted window points: new tet ids (scan of nbf in insertion order)
+__global__ void k_init_nbf(Cand C, const int* plist, const int* acc, int nw, int* nbfv) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x)
+    nbfv[w] = acc[w] ? C.nbf[plist[w]] : 0;
+}
+__global__ void k_init_kill(Dev D, Cand C, const int* plist, const int* acc, const int* scan, int nw, int nt,
+                            int* succ) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
+    if (!acc[w]) continue;
+    int c = plist[w];
+    int nt0 = nt + scan[w];
+    C.nt0[c] = nt0;
+    if (C.mind[c] <= D.too_close_sq) raise_err(GQ_ERR_DEGEN);
+    SlabView v = slab(C, c);
+    for (int j = 0; j < C.ntet[c]; ++j) { D.alive[v.tets[j]] = 0; succ[v.tets[j]] = nt0; }
+  }
+}
+__global__ void k_init_stars(Dev D, Cand C, const int* pend, const int* plist, const int* acc, int nw,
+                             int* touched, int round) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
+    if (!acc[w]) continue;
+    int c = plist[w];
+    SlabView v = slab(C, c);
+    for (int k = 0; k < C.nbf[c]; ++k) {      // survivors get rewired
+      int t = v.bf[k] >> 2, i = v.bf[k] & 3;
+      touched[tnk(D, t, i) >> 2] = round;
+    }
+    star_insert(D, pend[c], v.bf, C.nbf[c], C.nt0[c], true);
+    C.status[c] = CS_DROP;
+  }
+}
+__global__ void k_count_ovf(const Cand C, const int* plist, int W, int* out) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x)
+    if (C.status[plist[w]] == CS_OVF) atomicAdd(out, 1);
+}
+__global__ void k_gather_status(const Cand C, const int* plist, int W, int* out) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) out[w] = C.status[plist[w]];
+}
+__global__ void k_release_big(Cand C, const int* list, int n) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    int c = list[k];
+    if (C.status[c] != CS_DROP) { C.status[c] = CS_OK; C.memb[c] = -1; }
+    C.bigi[c] = -1;
+  }
+}
+// remove accepted points from the pending list (stable)
+__global__ void k_init_compact(const int* plist, const int* acc, const int* keepscan, int nw, int ntot, int* out) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < ntot; w += gridDim.x * blockDim.x) {
+    if (w < nw && acc[w]) continue;
+    int pos = w < nw ? keepscan[w] : (keepscan[nw - 1] + (acc[nw - 1] ? 0 : 1)) + (w - nw);
+    out[pos] = plist[w];
+  }
+}
+__global__ void k_init_keep(const int* acc, int nw, int* keep) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) keep[w] = acc[w] ? 0 : 1;
 }
 
 // facet bootstrap: one thread per polygon (facets.py:57-90, 342-372)
@@ -1464,6 +1537,7 @@ struct gq_ctx {
   std::vector<std::vector<int>> polys;
   CGrid G{};
   int reg_seg = 0, reg_face = 0, reg_nv = 0;
+  int big_used = 0;
   bool allocated = false;
 };
 
@@ -1502,6 +1576,9 @@ static void ensure_tmp(gq_ctx* c, size_t n) {
   c->tmpA = dmalloc<int>(c->tmpcap); c->tmpB = dmalloc<int>(c->tmpcap); c->tmpC = dmalloc<int>(c->tmpcap);
   c->k64a = dmalloc<unsigned long long>(c->tmpcap); c->k64b = dmalloc<unsigned long long>(c->tmpcap);
   c->k32a = dmalloc<unsigned int>(c->tmpcap); c->k32b = dmalloc<unsigned int>(c->tmpcap);
+}
+__global__ void k_scatter_ints(int* dst, const int* idx, const int* val, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[idx[i]] = val[i];
 }
 __global__ void k_scatter_flagged(const int* flags, const int* scan, int n, int* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -1601,6 +1678,22 @@ static void grow_cands_keep(gq_ctx* c, int need, int n_keep) {
   CK(cudaMemcpy(C.beseg, old.beseg, 4 * kb * CCB, cudaMemcpyDeviceToDevice));
   free_cands(old);
 }
+// big-region slabs: grow keeping the first c->big_used ones
+static void ensure_big(gq_ctx* c, int need) {
+  Cand& C = c->C;
+  if (need <= C.nbigcap) return;
+  int cap = std::max(need, 2 * C.nbigcap);
+  size_t keep = (size_t)c->big_used;
+  auto grow = [&](int*& ptr, size_t w) {
+    int* q = dmalloc<int>((size_t)cap * w);
+    if (keep) CK(cudaMemcpy(q, ptr, 4 * keep * w, cudaMemcpyDeviceToDevice));
+    cudaFree(ptr);
+    ptr = q;
+  };
+  grow(C.btets, CTB); grow(C.bbf, CFB); grow(C.bcr, CCB); grow(C.bcrf, CCB);
+  grow(C.bbsub, CCB); grow(C.bbseg, CCB); grow(C.beseg, CCB);
+  C.nbigcap = cap;
+}
 static unsigned int pow2_at_least(size_t n) { unsigned int p = 1024; while (p < n) p <<= 1; return p; }
 
 static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
@@ -1657,7 +1750,7 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   c->L.cap = 1 << 20; c->L.rows = dmalloc<int>((size_t)8 * c->L.cap);
   c->d_int = dmalloc<int>(64);
   alloc_scratch(c->S, 16384, CT * 2, 1024, 2048);
-  alloc_scratch(c->SB, 128, CTB * 2, 16384, 65536);
+  alloc_scratch(c->SB, 512, CTB * 2, 16384, 32768);
   alloc_cands(c, 1 << 16, 256);
   {
     int g = (int)std::cbrt(std::max(1.0, n / 2.0));
@@ -1696,10 +1789,18 @@ static void free_all(gq_ctx* c) {
 }
 
 // regions for candidates [n0,n1): normal pass, then the overflow ones with big slabs
+static void time_region(gq_ctx* c) {
+  CK(cudaEventSynchronize(c->er1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, c->er0, c->er1);
+  c->region_ms += ms;
+}
 static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   if (n1 <= n0) return;
   CK(cudaEventRecord(c->er0, c->st));
   LAUNCH_S(k_region, n1 - n0, c->D, c->C, c->S, n0, n1, (const int*)nullptr, probe, 0);
+  CK(cudaEventRecord(c->er1, c->st));
+  time_region(c);
   // overflow pass
   ensure_tmp(c, n1 + 1);
   std::vector<int> hs(n1 - n0);
@@ -1707,18 +1808,16 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   sync(c);
   std::vector<int> big;
   for (int k = 0; k < n1 - n0; ++k) if (hs[k] == CS_OVF) big.push_back(n0 + k);
-  for (size_t b0 = 0; b0 < big.size(); b0 += c->C.nbigcap) {
-    int nb = (int)std::min<size_t>(c->C.nbigcap, big.size() - b0);
-    CK(cudaMemcpyAsync(c->tmpC, big.data() + b0, sizeof(int) * nb, cudaMemcpyHostToDevice, c->st));
-    k_region<<<1, 128, 0, c->st>>>(c->D, c->C, c->SB, 0, nb, c->tmpC, probe, 1);
+  if (!big.empty()) {
+    int nb = (int)big.size();
+    ensure_big(c, c->big_used + nb);
+    CK(cudaMemcpyAsync(c->tmpC, big.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, c->st));
+    k_region<<<grid_for(nb, 128, c->SB.nthreads / 128), 128, 0, c->st>>>(c->D, c->C, c->SB, c->big_used, nb, c->tmpC, probe, 1);
     c->launches++;
     CK(cudaGetLastError());
+    c->big_used += nb;
     sync(c);
-    if (b0 + nb < big.size()) throw std::runtime_error("too many oversized regions in one stage");
   }
-  CK(cudaEventRecord(c->er1, c->st));
-  sync(c);
-  float ms = 0; cudaEventElapsedTime(&ms, c->er0, c->er1); c->region_ms += ms;
 }
 
 // candidates sorted by priority (rank, hash, canon): stable radix sorts
@@ -1891,6 +1990,7 @@ static void compact_tets(gq_ctx* c) {
 }
 
 // ------------------------------------------------------------------ init
+static void ensure_big(gq_ctx* c, int need);
 static void init_delaunay(gq_ctx* c, const int* order, int n) {
   CK(cudaMemcpyAsync(c->d_order, order, 4 * (size_t)n, cudaMemcpyHostToDevice, c->st));
   LAUNCH(k_init_first, 1, c->D, c->d_order, n, c->d_int + 8);
@@ -1904,88 +2004,108 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     if (v == first[0] || v == first[1] || v == first[2] || v == first[3]) continue;
     pend.push_back(v);
   }
-  int* d_pend = dmalloc<int>(std::max<size_t>(pend.size(), 1));
-  int* d_hint = dmalloc<int>(std::max<size_t>(pend.size(), 1));
+  int np = (int)pend.size();
+  if (np == 0) return;
+  ensure_cands(c, np);
+  Cand& C = c->C;
+  int* d_pend = dmalloc<int>(np);
+  int* d_hint = dmalloc<int>(np);
+  int* d_plist = dmalloc<int>(np);
+  int* d_plist2 = dmalloc<int>(np);
+  int* d_acc = dmalloc<int>(np);
+  int* d_scan = dmalloc<int>(np);
+  int* d_keep = dmalloc<int>(np);
   int* d_succ = dmalloc<int>(c->D.tcap);
+  int* d_touched = dmalloc<int>(c->D.tcap);
   CK(cudaMemsetAsync(d_succ, 0xff, 4 * (size_t)c->D.tcap, c->st));
-  std::vector<int> hint(pend.size(), 0);
-  CK(cudaMemcpyAsync(d_pend, pend.data(), 4 * pend.size(), cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemcpyAsync(d_hint, hint.data(), 4 * hint.size(), cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(d_touched, 0xff, 4 * (size_t)c->D.tcap, c->st));
+  CK(cudaMemsetAsync(d_hint, 0, 4 * (size_t)np, c->st));
+  CK(cudaMemsetAsync(C.status, 0, 4 * (size_t)np, c->st));          // CS_OK, not cached
+  CK(cudaMemsetAsync(C.memb, 0xff, 4 * (size_t)np, c->st));
+  CK(cudaMemsetAsync(C.bigi, 0xff, 4 * (size_t)np, c->st));
+  CK(cudaMemcpyAsync(d_pend, pend.data(), 4 * (size_t)np, cudaMemcpyHostToDevice, c->st));
+  std::vector<int> ident(np);
+  for (int k = 0; k < np; ++k) ident[k] = k;
+  CK(cudaMemcpyAsync(d_plist, ident.data(), 4 * (size_t)np, cudaMemcpyHostToDevice, c->st));
   pull(c);
-  size_t off = 0;
-  int inserted = 4;
-  while (off < pend.size()) {
-    int nwin = (int)std::min<size_t>(pend.size() - off, std::max(256, 2 * inserted));
-    ensure_cands(c, nwin);
-    ensure_tmp(c, nwin + 1);
-    const int* wp = d_pend + off;
-    int* wh = d_hint + off;
-    // status OK for all window points
-    std::vector<int> st(nwin, CS_OK), bi(nwin, -1);
-    CK(cudaMemcpyAsync(c->C.status, st.data(), 4 * nwin, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->C.bigi, bi.data(), 4 * nwin, cudaMemcpyHostToDevice, c->st));
-    LAUNCH_S(k_init_region, nwin, c->D, c->C, c->S, wp, wh, nwin, d_succ);
-    // overflow (large early cavities)
-    std::vector<int> hs(nwin);
-    CK(cudaMemcpyAsync(hs.data(), c->C.status, 4 * nwin, cudaMemcpyDeviceToHost, c->st));
-    sync(c);
-    std::vector<int> bigl;
-    for (int k = 0; k < nwin; ++k) if (hs[k] == CS_OVF) bigl.push_back(k);
-    if (!bigl.empty()) {
-      // only the lowest-order overflowing points matter this round: give big
-      // slabs to the first ones, the rest wait (they cannot be accepted
-      // before the first overflowing point anyway)
-      int nb = (int)std::min<size_t>(bigl.size(), c->C.nbigcap);
-      for (int k = 0; k < nb; ++k) bi[bigl[k]] = k;
-      CK(cudaMemcpyAsync(c->C.bigi, bi.data(), 4 * nwin, cudaMemcpyHostToDevice, c->st));
-      k_init_region<<<1, 128, 0, c->st>>>(c->D, c->C, c->SB, wp, wh, nwin, d_succ);
-      c->launches++;
-      CK(cudaGetLastError());
-      sync(c);
-      CK(cudaMemcpyAsync(hs.data(), c->C.status, 4 * nwin, cudaMemcpyDeviceToHost, c->st));
-      sync(c);
-      // truncate the window before the first still-unresolved point
-      for (int k = 0; k < nwin; ++k) if (hs[k] == CS_OVF) { nwin = k; break; }
+  int nt = c->hc.nt;
+  int left = np, inserted = 4;
+  double wf = getenv("GQ_INIT_WINDOW") ? atof(getenv("GQ_INIT_WINDOW")) : 1.0;
+  for (int round = 0; left > 0; ++round) {
+    int W = (int)std::min<double>(left, std::max(64.0, wf * inserted));
+    CK(cudaEventRecord(c->er0, c->st));
+    LAUNCH_S(k_init_region, W, c->D, C, c->S, d_pend, d_plist, W, d_hint, d_succ, d_touched, round, 0);
+    CK(cudaEventRecord(c->er1, c->st));
+    time_region(c);
+    // big cavities (early rounds): resolve the lowest-order ones, truncate the window at the rest
+    std::vector<int> bl;
+    {
+      CK(cudaMemsetAsync(c->d_int + 40, 0, 4, c->st));
+      LAUNCH(k_count_ovf, W, C, d_plist, W, c->d_int + 40);
+      int novf = read_int(c, c->d_int + 40);
+      if (novf > 0) {
+        std::vector<int> pl(W), sw(W);
+        LAUNCH(k_gather_status, W, C, d_plist, W, d_scan);
+        CK(cudaMemcpyAsync(pl.data(), d_plist, 4 * (size_t)W, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(sw.data(), d_scan, 4 * (size_t)W, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        for (int w = 0; w < W; ++w) if (sw[w] == CS_OVF) bl.push_back(pl[w]);
+        int nb = (int)std::min<size_t>(bl.size(), 4096);
+        bl.resize(nb);
+        ensure_big(c, nb);
+        ensure_tmp(c, nb + 1);
+        std::vector<int> bis(nb);
+        for (int k = 0; k < nb; ++k) bis[k] = k;
+        CK(cudaMemcpyAsync(d_keep, bl.data(), 4 * (size_t)nb, cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(d_acc, bis.data(), 4 * (size_t)nb, cudaMemcpyHostToDevice, c->st));
+        LAUNCH(k_scatter_ints, nb, C.bigi, d_keep, d_acc, nb);
+        k_init_region<<<grid_for(nb, 128, c->SB.nthreads / 128), 128, 0, c->st>>>(c->D, C, c->SB, d_pend, d_plist, W, d_hint, d_succ, d_touched, round, 1);
+        c->launches++;
+        CK(cudaGetLastError());
+        LAUNCH(k_gather_status, W, C, d_plist, W, d_scan);
+        CK(cudaMemcpyAsync(sw.data(), d_scan, 4 * (size_t)W, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        for (int w = 0; w < W; ++w) if (sw[w] == CS_OVF) { W = w; break; }
+        if (W == 0) throw std::runtime_error("init: cavity overflow");
+        CK(cudaMemcpyAsync(c->tmpC, bl.data(), 4 * (size_t)nb, cudaMemcpyHostToDevice, c->st));
+      }
     }
-    if (nwin == 0) throw std::runtime_error("init: cavity overflow");
-    // rank = window position; state 0 for all
-    std::vector<int> rk(nwin), s0(nwin, 0);
-    for (int k = 0; k < nwin; ++k) rk[k] = k;
-    CK(cudaMemcpyAsync(c->C.rank, rk.data(), 4 * nwin, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->C.state, s0.data(), 4 * nwin, cudaMemcpyHostToDevice, c->st));
-    run_filter_strict(c, nwin);
-    std::vector<int> state(nwin), nbf(nwin);
-    CK(cudaMemcpyAsync(state.data(), c->C.state, 4 * nwin, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(nbf.data(), c->C.nbf, 4 * nwin, cudaMemcpyDeviceToHost, c->st));
+    LAUNCH(k_init_claim, W, c->D, C, c->W, d_plist, W);
+    LAUNCH(k_init_decide, W, c->D, C, c->W, d_plist, W, d_acc);
+    LAUNCH(k_init_unclaim, W, c->D, C, c->W, d_plist, W);
+    LAUNCH(k_init_nbf, W, C, d_plist, d_acc, W, d_keep);
+    exclusive_scan(c, d_keep, d_scan, W);
+    int lastn = 0, lasts = 0, lasta = 0;
+    CK(cudaMemcpyAsync(&lastn, d_keep + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&lasts, d_scan + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
+    // number accepted
+    exclusive_scan(c, d_acc, d_plist2, W);
+    int lastacc_scan = 0;
+    CK(cudaMemcpyAsync(&lastacc_scan, d_plist2 + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&lasta, d_acc + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
     sync(c);
-    std::vector<int> acc, nt0(nwin, 0), keep;
-    pull(c);
-    int nt = c->hc.nt;
-    for (int k = 0; k < nwin; ++k) {
-      if (state[k] == 1) { acc.push_back(k); nt0[k] = nt; nt += nbf[k]; }
-    }
-    if (nt > c->D.tcap) throw std::runtime_error("tet capacity exceeded in init");
-    CK(cudaMemcpyAsync(c->C.nt0, nt0.data(), 4 * nwin, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->tmpA, acc.data(), 4 * acc.size(), cudaMemcpyHostToDevice, c->st));
-    LAUNCH(k_init_star, acc.size(), c->D, c->C, wp, c->tmpA, (int)acc.size(), d_succ);
-    LAUNCH(k_init_star2, acc.size(), c->D, c->C, wp, c->tmpA, (int)acc.size());
+    int nacc = lastacc_scan + lasta;
+    int add_t = lasts + lastn;
+    if (nt + add_t > c->D.tcap) throw std::runtime_error("tet capacity exceeded in init");
+    LAUNCH(k_init_kill, W, c->D, C, d_plist, d_acc, d_scan, W, nt, d_succ);
+    LAUNCH(k_init_stars, W, c->D, C, d_pend, d_plist, d_acc, W, d_touched, round);
+    nt += add_t;
+    // release big slabs (big regions are recomputed next round if still pending)
+    LAUNCH(k_init_keep, W, d_acc, W, d_keep);
+    exclusive_scan(c, d_keep, d_scan, W);
+    LAUNCH(k_init_compact, left, d_plist, d_acc, d_scan, W, left, d_plist2);
+    std::swap(d_plist, d_plist2);
+    if (!bl.empty()) LAUNCH(k_release_big, bl.size(), C, c->tmpC, (int)bl.size());
+    left -= nacc;
+    inserted += nacc;
     c->hc.nt = nt;
     push(c);
-    inserted += (int)acc.size();
-    // compact the pending list: accepted points leave, order kept
-    std::vector<int> wpend(nwin), whint(nwin);
-    CK(cudaMemcpyAsync(wpend.data(), wp, 4 * nwin, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(whint.data(), wh, 4 * nwin, cudaMemcpyDeviceToHost, c->st));
-    sync(c);
-    std::vector<int> np, nh;
-    for (int k = 0; k < nwin; ++k) if (state[k] != 1) { np.push_back(wpend[k]); nh.push_back(whint[k]); }
-    size_t newoff = off + nwin - np.size();
-    CK(cudaMemcpyAsync(d_pend + newoff, np.data(), 4 * np.size(), cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(d_hint + newoff, nh.data(), 4 * nh.size(), cudaMemcpyHostToDevice, c->st));
-    off = newoff;
-    sync(c);
+    if (nacc == 0) throw std::runtime_error("init made no progress");
   }
-  cudaFree(d_pend); cudaFree(d_hint); cudaFree(d_succ);
+  // big-slab candidates must not keep stale bigi for the refinement rounds
+  sync(c);
+  cudaFree(d_pend); cudaFree(d_hint); cudaFree(d_plist); cudaFree(d_plist2); cudaFree(d_acc);
+  cudaFree(d_scan); cudaFree(d_keep); cudaFree(d_succ); cudaFree(d_touched);
 }
 
 // ------------------------------------------------------------------ round
@@ -2087,6 +2207,7 @@ static void insert_accepted(gq_ctx* c, const std::vector<int>& acc_sorted, long 
 
 static RoundOut run_round(gq_ctx* c, int round_no) {
   RoundOut R;
+  c->big_used = 0;
   CandCtx X; X.round_no = round_no; X.seed = c->seed; X.with_facets = c->npoly > 0;
   double lmin2 = c->D.lmin2;
   std::vector<int> kinds, tgts, pool;
@@ -2241,7 +2362,6 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   alloc_mesh(c, n, m, f, npidx);
   c->d_order = dmalloc<int>(n);
   Dev& D = c->D;
-  CK(cudaEventRecord(c->ev0, c->st));
   // bbox / lmin (mesh.py:883-885, refine.py:532)
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int i = 0; i < n; ++i) for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], xyz[3 * i + k]); hi[k] = std::max(hi[k], xyz[3 * i + k]); }
@@ -2259,6 +2379,7 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   c->hc = Counters{};
   c->hc.nv = n;
   push(c);
+  CK(cudaEventRecord(c->ev0, c->st));
   // polygon info
   c->polys.assign(m, {});
   std::vector<int> spo(m + 1, 0), sp;
@@ -2383,7 +2504,11 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
     for (auto& r : c->rounds) ncand += r[2];
     created = (long long)c->hc.nt;   // lower bound proxy (slots created since last compaction)
     long long steiner = c->hc.nv - n;
-    out->bytes_alg = 144 * ncand + 58 * (long long)tested + 8 * (long long)tested + 51 * created + 29 * steiner;
+    (void)ncand; (void)created; (void)steiner;
+    // region kernels' algorithmic bytes: 58 B per tet tested
+    // (cavity + boundary neighbours: tv 16 + tn 16 + masks 2 + one vertex 24)
+    // + 24 B per candidate point
+    out->bytes_alg = 58 * (long long)tested + 24 * (long long)rc;
   }
 }
 
