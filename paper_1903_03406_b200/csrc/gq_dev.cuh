@@ -495,26 +495,36 @@ __device__ __noinline__ int region_compute(const Dev& D, const double* p, const 
   // peel to the largest star-shaped subset, keep the seed component, repeat
   int seedk = 0;
   while (true) {
-    bool changed = true;
-    while (changed) {
-      changed = false;
-      for (int k = 0; k < n; ++k) {
-        if (!S.in[k]) continue;
-        int t = S.list[k];
-        int4 q = D.tv[t];
-        for (int i = 0; i < 4; ++i) {
-          int u = tnk(D, t, i) >> 2;
-          bool blk = blocked(D, A, t, i);
-          int ku = S.tset.find(u);
-          bool uin = ku >= 0 && S.in[ku];
-          if (uin && !blk) continue;
-          int f[3]; face_verts(q, i, f);
-          if (f[0] == GHOST || f[1] == GHOST || f[2] == GHOST) continue;
-          if (orient3d(PT(D, f[0]), PT(D, f[1]), PT(D, f[2]), p) >= 0) { S.in[k] = 0; changed = true; break; }
-        }
+    // worklist form of the confluent peel: only neighbours of a removed tet
+    // can change state, so each tet is re-examined O(1) times.  comp[] marks
+    // queued entries; stack holds the queue.
+    int qn = 0;
+    for (int k = 0; k < n; ++k) if (S.in[k]) { S.stack[qn++] = k; S.comp[k] = 1; } else S.comp[k] = 0;
+    while (qn > 0) {
+      int k = S.stack[--qn];
+      S.comp[k] = 0;
+      if (!S.in[k]) continue;
+      int t = S.list[k];
+      int4 q = D.tv[t];
+      bool rm = false;
+      for (int i = 0; i < 4 && !rm; ++i) {
+        int u = tnk(D, t, i) >> 2;
+        bool blk = blocked(D, A, t, i);
+        int ku = S.tset.find(u);
+        bool uin = ku >= 0 && S.in[ku];
+        if (uin && !blk) continue;
+        int f[3]; face_verts(q, i, f);
+        if (f[0] == GHOST || f[1] == GHOST || f[2] == GHOST) continue;
+        if (orient3d(PT(D, f[0]), PT(D, f[1]), PT(D, f[2]), p) >= 0) rm = true;
       }
-      if (!S.in[seedk]) return RS_CNSS;   // seed shrunk away
+      if (!rm) continue;
+      S.in[k] = 0;
+      for (int i = 0; i < 4; ++i) {
+        int ku = S.tset.find(tnk(D, t, i) >> 2);
+        if (ku >= 0 && S.in[ku] && !S.comp[ku]) { S.comp[ku] = 1; S.stack[qn++] = ku; }
+      }
     }
+    if (!S.in[seedk]) return RS_CNSS;   // seed shrunk away
     int live = 0;
     for (int k = 0; k < n; ++k) { live += S.in[k]; S.comp[k] = 0; }
     int ncomp = 1;
@@ -538,10 +548,25 @@ __device__ __noinline__ int region_compute(const Dev& D, const double* p, const 
   // finish: cavity tets sorted by id
   int m = 0;
   for (int k = 0; k < n; ++k) if (S.in[k]) S.stack[m++] = S.list[k];
-  for (int a = 1; a < m; ++a) {           // insertion sort (regions are small)
-    int x = S.stack[a], b = a - 1;
-    while (b >= 0 && S.stack[b] > x) { S.stack[b + 1] = S.stack[b]; --b; }
-    S.stack[b + 1] = x;
+  if (m <= 48) {
+    for (int a = 1; a < m; ++a) {         // insertion sort (typical regions are small)
+      int x = S.stack[a], b = a - 1;
+      while (b >= 0 && S.stack[b] > x) { S.stack[b + 1] = S.stack[b]; --b; }
+      S.stack[b + 1] = x;
+    }
+  } else {
+    int* h = S.stack;                      // heap sort for big cavities
+    auto sift = [&](int root, int end) {
+      while (2 * root + 1 < end) {
+        int ch = 2 * root + 1;
+        if (ch + 1 < end && h[ch] < h[ch + 1]) ++ch;
+        if (h[root] >= h[ch]) return;
+        int t = h[root]; h[root] = h[ch]; h[ch] = t;
+        root = ch;
+      }
+    };
+    for (int a = m / 2 - 1; a >= 0; --a) sift(a, m);
+    for (int e = m - 1; e > 0; --e) { int t = h[0]; h[0] = h[e]; h[e] = t; sift(0, e); }
   }
   if (m > O.ctet) return RS_OVERFLOW;
   O.ntet = m; O.nbf = 0; O.ncr = 0; O.nbsub = 0; O.nbseg = 0; O.neseg = 0;

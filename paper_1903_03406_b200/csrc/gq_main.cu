@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "gq_dev.cuh"
+#include "gq_block.cuh"
 #include "../../include/gqm3d.h"
 
 using namespace gq;
@@ -316,6 +317,70 @@ __global__ void k_region(Dev D, Cand C, Scr SC, int n0, int n1, const int* list,
     } else {
       C.status[c] = CS_CNSS;
     }
+  }
+}
+
+// oversized cavities: one block per candidate (threads in proportion to
+// region size); big slabs base+w
+__global__ void __launch_bounds__(BR_THREADS) k_region_block(Dev D, Cand C, Scr SB, const int* list, int nb, int base) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BlockShared& B = *reinterpret_cast<BlockShared*>(smem_raw);
+  Scratch S = scratch_for(SB, blockIdx.x);
+  for (int w = blockIdx.x; w < nb; w += gridDim.x) {
+    int c = list[w];
+    if (threadIdx.x == 0) C.bigi[c] = base + w;
+    __syncthreads();
+    SlabView v = slab(C, c);
+    __shared__ int s_seeds[32];
+    __shared__ int s_ns;
+    if (threadIdx.x == 0) s_ns = cand_seeds(D, C, c, s_seeds, S);
+    __syncthreads();
+    RegionOut O = region_view(C, c, v, 0);
+    int st = s_ns == 0 ? RS_CNSS : region_block(D, C.p + 3 * (size_t)c, s_seeds, s_ns, allow_of(C, c), B, S, O);
+    if (threadIdx.x == 0) {
+      atomicAdd(&g_region_calls, 1ull);
+      store_region(C, c, O);
+      if (st == RS_OK) {
+        atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf));
+        C.status[c] = (O.mind <= D.too_close_sq) ? CS_TOOCLOSE : CS_OK;
+      } else if (st == RS_OVERFLOW) { C.status[c] = CS_CNSS; raise_err(GQ_ERR_CAP); }
+      else if (st == RS_MEMBRANE) { C.status[c] = CS_MEMB; C.memb[c] = O.memb; }
+      else C.status[c] = CS_CNSS;
+    }
+    __syncthreads();
+  }
+}
+__global__ void __launch_bounds__(BR_THREADS) k_init_region_block(Dev D, Cand C, Scr SB, const int* pend, const int* list, int nb,
+                                                                  int* hint, const int* succ, int round) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BlockShared& B = *reinterpret_cast<BlockShared*>(smem_raw);
+  Scratch S = scratch_for(SB, blockIdx.x);
+  for (int w = blockIdx.x; w < nb; w += gridDim.x) {
+    int c = list[w];
+    __shared__ int s_t;
+    if (threadIdx.x == 0) {
+      C.bigi[c] = w;
+      const double* p = PT(D, pend[c]);
+      int h = hint[c];
+      while (h >= 0 && !D.alive[h]) h = succ[h];
+      s_t = walk(D, p, h);
+      hint[c] = s_t;
+    }
+    __syncthreads();
+    SlabView v = slab(C, c);
+    RegionOut O = region_view(C, c, v, 0);
+    int seeds[1] = {s_t};
+    Allow A; A.n = 0;
+    int st = region_block(D, PT(D, pend[c]), seeds, 1, A, B, S, O);
+    if (threadIdx.x == 0) {
+      atomicAdd(&g_region_calls, 1ull);
+      store_region(C, c, O);
+      C.extra[c] = -1; C.kind[c] = K_TET; C.rank[c] = c; C.memb[c] = round;
+      if (st == RS_OK) { C.status[c] = CS_OK; atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf)); }
+      else if (st == RS_OVERFLOW) { C.status[c] = CS_OVF; C.memb[c] = -1; raise_err(GQ_ERR_CAP); }
+      else { C.status[c] = CS_CNSS; raise_err(GQ_ERR_DEGEN); }
+    }
+    __syncthreads();
   }
 }
 
@@ -889,6 +954,9 @@ __global__ void k_flag_pending_keys(Dev D, int phase, unsigned int need, unsigne
     if (phase == 0) { int2 e = D.sg_uv[r]; k1[r] = key2(e.x, e.y); }
     else { int4 q = D.sf_v[r]; k1[r] = key2(q.y, q.z); k2[r] = (unsigned int)q.x; }
   }
+}
+__global__ void k_face_a(Dev D, const int* recs, int n, unsigned int* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = (unsigned int)D.sf_v[recs[i]].x;
 }
 __global__ void k_flag_bad(Dev D, double B, int* flags) {
   int nt = D.ctr->nt;
@@ -1538,6 +1606,8 @@ struct gq_ctx {
   CGrid G{};
   int reg_seg = 0, reg_face = 0, reg_nv = 0;
   int big_used = 0;
+  int init_rounds = 0;
+  struct QBuf { int *a, *b, *c, *d, *e, *f, *g, *h; size_t cap; } Q{};
   bool allocated = false;
 };
 
@@ -1576,6 +1646,12 @@ static void ensure_tmp(gq_ctx* c, size_t n) {
   c->tmpA = dmalloc<int>(c->tmpcap); c->tmpB = dmalloc<int>(c->tmpcap); c->tmpC = dmalloc<int>(c->tmpcap);
   c->k64a = dmalloc<unsigned long long>(c->tmpcap); c->k64b = dmalloc<unsigned long long>(c->tmpcap);
   c->k32a = dmalloc<unsigned int>(c->tmpcap); c->k32b = dmalloc<unsigned int>(c->tmpcap);
+}
+__global__ void k_gather_u32(const unsigned int* src, const int* idx, int n, unsigned int* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[idx[i]];
+}
+__global__ void k_gather_u64(const unsigned long long* src, const int* idx, int n, unsigned long long* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[idx[i]];
 }
 __global__ void k_scatter_ints(int* dst, const int* idx, const int* val, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[idx[i]] = val[i];
@@ -1780,12 +1856,14 @@ static void free_all(gq_ctx* c) {
                 c->S.tkey, c->S.tval, c->S.tep, c->S.fkey, c->S.fep, c->S.epoch, c->S.list, c->S.stack, c->S.in,
                 c->S.comp, c->SB.tkey, c->SB.tval, c->SB.tep, c->SB.fkey, c->SB.fep, c->SB.epoch, c->SB.list,
                 c->SB.stack, c->SB.in, c->SB.comp, c->tmpA, c->tmpB, c->tmpC, c->k64a, c->k64b, c->k32a, c->k32b,
-                c->cub_tmp, c->d_order, c->G.head, c->G.nodes, c->G.big, c->G.nnodes};
+                c->cub_tmp, c->d_order, c->G.head, c->G.nodes, c->G.big, c->G.nnodes, c->Q.a, c->Q.b, c->Q.c,
+                c->Q.d, c->Q.e, c->Q.f, c->Q.g, c->Q.h};
   for (void* p : ps) if (p) cudaFree(p);
   free_cands(c->C);
   c->allocated = false;
   c->tmpcap = 0; c->cub_cap = 0; c->cub_tmp = nullptr;
   c->tmpA = c->tmpB = c->tmpC = nullptr; c->k64a = c->k64b = nullptr; c->k32a = c->k32b = nullptr; c->d_order = nullptr;
+  c->Q = {};
 }
 
 // regions for candidates [n0,n1): normal pass, then the overflow ones with big slabs
@@ -1812,7 +1890,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
     int nb = (int)big.size();
     ensure_big(c, c->big_used + nb);
     CK(cudaMemcpyAsync(c->tmpC, big.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, c->st));
-    k_region<<<grid_for(nb, 128, c->SB.nthreads / 128), 128, 0, c->st>>>(c->D, c->C, c->SB, c->big_used, nb, c->tmpC, probe, 1);
+    k_region_block<<<std::min(nb, c->SB.nthreads), BR_THREADS, sizeof(BlockShared), c->st>>>(c->D, c->C, c->SB, c->tmpC, nb, c->big_used);
     c->launches++;
     CK(cudaGetLastError());
     c->big_used += nb;
@@ -1820,31 +1898,30 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   }
 }
 
-// candidates sorted by priority (rank, hash, canon): stable radix sorts
-static void rank_candidates(gq_ctx* c, const std::vector<int>& ok) {
-  int n = (int)ok.size();
-  if (n == 0) return;
+// candidates sorted by priority (class rank, hash); smaller first
+// (refine.py:45-52).  Equal hashes would fall back to the canonical tuple in
+// the reference; a 64-bit splitmix collision inside one round is ignored.
+__global__ void k_rank_keys(Cand C, int n, unsigned long long* kh, unsigned int* kk, int* idx) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    bool ok = C.status[c] == CS_OK;
+    kh[c] = ok ? C.h[c] : ~0ull;
+    kk[c] = ok ? (unsigned int)C.kind[c] : 7u;
+    idx[c] = c;
+  }
+}
+static void rank_candidates(gq_ctx* c, int n) {
+  if (n <= 0) return;
   ensure_tmp(c, n + 1);
-  // host-side sort of (kind, h, canon) -- keys pulled back (n is the round's pool)
-  std::vector<unsigned long long> h(c->C.cap);
-  std::vector<int4> canon(c->C.cap);
-  std::vector<int> kind(c->C.cap);
-  int nmax = 0; for (int x : ok) nmax = std::max(nmax, x + 1);
-  CK(cudaMemcpyAsync(h.data(), c->C.h, 8 * (size_t)nmax, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(canon.data(), c->C.canon, 16 * (size_t)nmax, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(kind.data(), c->C.kind, 4 * (size_t)nmax, cudaMemcpyDeviceToHost, c->st));
-  sync(c);
-  std::vector<int> order = ok;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-    if (kind[a] != kind[b]) return kind[a] < kind[b];
-    if (h[a] != h[b]) return h[a] < h[b];
-    const int4 &x = canon[a], &y = canon[b];
-    if (x.x != y.x) return x.x < y.x;
-    if (x.y != y.y) return x.y < y.y;
-    if (x.z != y.z) return x.z < y.z;
-    return x.w < y.w;
-  });
-  CK(cudaMemcpyAsync(c->tmpA, order.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->st));
+  LAUNCH(k_rank_keys, n, c->C, n, c->k64a, c->k32a, c->tmpA);
+  size_t need = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, need, c->k64a, c->k64b, c->tmpA, c->tmpB, n, 0, 64, c->st);
+  ensure_cub(c, need);
+  cub::DeviceRadixSort::SortPairs(c->cub_tmp, need, c->k64a, c->k64b, c->tmpA, c->tmpB, n, 0, 64, c->st);
+  LAUNCH(k_gather_u32, n, c->k32a, c->tmpB, n, c->k32b);
+  need = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, need, c->k32b, c->k32a, c->tmpB, c->tmpA, n, 0, 3, c->st);
+  ensure_cub(c, need);
+  cub::DeviceRadixSort::SortPairs(c->cub_tmp, need, c->k32b, c->k32a, c->tmpB, c->tmpA, n, 0, 3, c->st);
   LAUNCH(k_rank_scatter, n, c->C, c->tmpA, n);
 }
 
@@ -1874,75 +1951,34 @@ static void run_filter_strict(gq_ctx* c, int n) {
   LAUNCH(k_strict_state, n, c->C, n);
 }
 
-static void upload_candidates(gq_ctx* c, int n0, const std::vector<int>& kinds, const std::vector<int>& tgts,
-                              const std::vector<int>& pool) {
-  int n = (int)tgts.size();
-  if (!n) return;
-  std::vector<int> st(n, CS_OK), bi(n, -1);
-  CK(cudaMemcpyAsync(c->C.kind + n0, kinds.data(), 4 * n, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemcpyAsync(c->C.tgt + n0, tgts.data(), 4 * n, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemcpyAsync(c->C.pool + n0, pool.data(), 4 * n, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemcpyAsync(c->C.status + n0, st.data(), 4 * n, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemcpyAsync(c->C.bigi + n0, bi.data(), 4 * n, cudaMemcpyHostToDevice, c->st));
-  sync(c);
-}
-
-// records with RF_REDIR, sorted by key (refine.py: sorted(redirect_*)), cleared
-static std::vector<int> take_redirects(gq_ctx* c, int phase) {
-  pull(c);
+// live records of a phase with all `need` flags and none of `deny`, sorted
+// by vertex key (refine.py:587, 595: sorted(enc_* - blocked_*)); ids -> out
+static int sorted_records(gq_ctx* c, int phase, unsigned int need, unsigned int deny, int* out) {
   int n = phase == 0 ? c->hc.nsegrec : c->hc.nfacerec;
-  std::vector<unsigned int> fl(n);
-  CK(cudaMemcpyAsync(fl.data(), phase == 0 ? c->D.sg_fl : c->D.sf_fl, 4 * (size_t)n, cudaMemcpyDeviceToHost, c->st));
-  sync(c);
-  std::vector<int> recs;
-  for (int r = 0; r < n; ++r) if ((fl[r] & RF_REDIR) && (fl[r] & RF_LIVE)) recs.push_back(r);
-  if (recs.empty()) return recs;
-  LAUNCH(k_clear_redir, n, c->D, phase);
+  if (n <= 0) return 0;
+  ensure_tmp(c, n + 1);
+  LAUNCH(k_flag_pending_keys, n, c->D, phase, need, deny, c->Q.e, c->k64a, c->k32a);
+  int cnt = select_flagged(c, c->Q.e, n, c->tmpA);       // record ids, ascending
+  if (cnt == 0) return 0;
+  size_t nb = 0;
   if (phase == 0) {
-    std::vector<int2> uv(n);
-    CK(cudaMemcpyAsync(uv.data(), c->D.sg_uv, 8 * (size_t)n, cudaMemcpyDeviceToHost, c->st));
-    sync(c);
-    std::sort(recs.begin(), recs.end(), [&](int a, int b) { return uv[a].x != uv[b].x ? uv[a].x < uv[b].x : uv[a].y < uv[b].y; });
+    LAUNCH(k_gather_u64, cnt, c->k64a, c->tmpA, cnt, c->k64b);
+    cub::DeviceRadixSort::SortPairs(nullptr, nb, c->k64b, c->k64a, c->tmpA, out, cnt, 0, 64, c->st);
+    ensure_cub(c, nb);
+    cub::DeviceRadixSort::SortPairs(c->cub_tmp, nb, c->k64b, c->k64a, c->tmpA, out, cnt, 0, 64, c->st);
   } else {
-    std::vector<int4> fv(n);
-    CK(cudaMemcpyAsync(fv.data(), c->D.sf_v, 16 * (size_t)n, cudaMemcpyDeviceToHost, c->st));
-    sync(c);
-    std::sort(recs.begin(), recs.end(), [&](int a, int b) {
-      if (fv[a].x != fv[b].x) return fv[a].x < fv[b].x;
-      if (fv[a].y != fv[b].y) return fv[a].y < fv[b].y;
-      return fv[a].z < fv[b].z; });
+    // (b,c) then a: two stable passes
+    LAUNCH(k_gather_u64, cnt, c->k64a, c->tmpA, cnt, c->k64b);
+    cub::DeviceRadixSort::SortPairs(nullptr, nb, c->k64b, c->k64a, c->tmpA, c->tmpB, cnt, 0, 64, c->st);
+    ensure_cub(c, nb);
+    cub::DeviceRadixSort::SortPairs(c->cub_tmp, nb, c->k64b, c->k64a, c->tmpA, c->tmpB, cnt, 0, 64, c->st);
+    LAUNCH(k_face_a, cnt, c->D, c->tmpB, cnt, c->k32b);
+    nb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, nb, c->k32b, c->k32a, c->tmpB, out, cnt, 0, 32, c->st);
+    ensure_cub(c, nb);
+    cub::DeviceRadixSort::SortPairs(c->cub_tmp, nb, c->k32b, c->k32a, c->tmpB, out, cnt, 0, 32, c->st);
   }
-  return recs;
-}
-
-// pending constraint records of a phase, sorted by vertex key
-static std::vector<int> pending_sorted(gq_ctx* c, int phase) {
-  pull(c);
-  int n = phase == 0 ? c->hc.nsegrec : c->hc.nfacerec;
-  std::vector<unsigned int> fl(n);
-  CK(cudaMemcpyAsync(fl.data(), phase == 0 ? c->D.sg_fl : c->D.sf_fl, 4 * (size_t)n, cudaMemcpyDeviceToHost, c->st));
-  sync(c);
-  std::vector<int> recs;
-  for (int r = 0; r < n; ++r) {
-    unsigned int f = fl[r];
-    if ((f & RF_LIVE) && (f & RF_ENC) && !(f & RF_BLOCK) && !(f & RF_SKIP)) recs.push_back(r);
-  }
-  if (recs.empty()) return recs;
-  if (phase == 0) {
-    std::vector<int2> uv(n);
-    CK(cudaMemcpyAsync(uv.data(), c->D.sg_uv, 8 * (size_t)n, cudaMemcpyDeviceToHost, c->st));
-    sync(c);
-    std::sort(recs.begin(), recs.end(), [&](int a, int b) { return uv[a].x != uv[b].x ? uv[a].x < uv[b].x : uv[a].y < uv[b].y; });
-  } else {
-    std::vector<int4> fv(n);
-    CK(cudaMemcpyAsync(fv.data(), c->D.sf_v, 16 * (size_t)n, cudaMemcpyDeviceToHost, c->st));
-    sync(c);
-    std::sort(recs.begin(), recs.end(), [&](int a, int b) {
-      if (fv[a].x != fv[b].x) return fv[a].x < fv[b].x;
-      if (fv[a].y != fv[b].y) return fv[a].y < fv[b].y;
-      return fv[a].z < fv[b].z; });
-  }
-  return recs;
+  return cnt;
 }
 
 // register records created since the last call (ConstraintIndex.add_*)
@@ -2059,7 +2095,8 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
         CK(cudaMemcpyAsync(d_keep, bl.data(), 4 * (size_t)nb, cudaMemcpyHostToDevice, c->st));
         CK(cudaMemcpyAsync(d_acc, bis.data(), 4 * (size_t)nb, cudaMemcpyHostToDevice, c->st));
         LAUNCH(k_scatter_ints, nb, C.bigi, d_keep, d_acc, nb);
-        k_init_region<<<grid_for(nb, 128, c->SB.nthreads / 128), 128, 0, c->st>>>(c->D, C, c->SB, d_pend, d_plist, W, d_hint, d_succ, d_touched, round, 1);
+        CK(cudaMemcpyAsync(c->tmpA, bl.data(), 4 * (size_t)nb, cudaMemcpyHostToDevice, c->st));
+        k_init_region_block<<<std::min(nb, c->SB.nthreads), BR_THREADS, sizeof(BlockShared), c->st>>>(c->D, C, c->SB, d_pend, c->tmpA, nb, d_hint, d_succ, round);
         c->launches++;
         CK(cudaGetLastError());
         LAUNCH(k_gather_status, W, C, d_plist, W, d_scan);
@@ -2101,6 +2138,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     c->hc.nt = nt;
     push(c);
     if (nacc == 0) throw std::runtime_error("init made no progress");
+    c->init_rounds = round + 1;
   }
   // big-slab candidates must not keep stale bigi for the refinement rounds
   sync(c);
@@ -2109,219 +2147,238 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
 }
 
 // ------------------------------------------------------------------ round
-struct RoundOut { int phase = -1; long long ncand = 0, acc = 0, rej = 0, failed = 0, inserted = 0; };
 
-static void insert_accepted(gq_ctx* c, const std::vector<int>& acc_sorted, long long* inserted, int round_no) {
-  int na = (int)acc_sorted.size();
-  if (na == 0) return;
-  ensure_tmp(c, na + 1);
-  CK(cudaMemcpyAsync(c->tmpA, acc_sorted.data(), 4 * na, cudaMemcpyHostToDevice, c->st));
-  LAUNCH(k_accept_flags, na, c->D, c->C, c->tmpA, na, c->tmpB, c->L, round_no, c->D.lmin2);
-  std::vector<int> fl(na);
-  CK(cudaMemcpyAsync(fl.data(), c->tmpB, 4 * na, cudaMemcpyDeviceToHost, c->st));
-  sync(c);
-  std::vector<int> ins;
-  for (int k = 0; k < na; ++k) if (fl[k]) ins.push_back(acc_sorted[k]);
-  int ni = (int)ins.size();
-  *inserted += ni;
-  if (ni == 0) return;
-  pull(c);
-  std::vector<int> kinds(c->C.cap), nbf(c->C.cap);
-  CK(cudaMemcpyAsync(nbf.data(), c->C.nbf, 4 * (size_t)c->C.cap, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(kinds.data(), c->C.kind, 4 * (size_t)c->C.cap, cudaMemcpyDeviceToHost, c->st));
-  std::vector<int> tg(c->C.cap);
-  CK(cudaMemcpyAsync(tg.data(), c->C.tgt, 4 * (size_t)c->C.cap, cudaMemcpyDeviceToHost, c->st));
-  sync(c);
-  std::vector<int> vids(c->C.cap, -1), nt0s(c->C.cap, -1);
-  int nt = c->hc.nt, nv = c->hc.nv;
-  for (int k = 0; k < ni; ++k) { vids[ins[k]] = nv + k; nt0s[ins[k]] = nt; nt += nbf[ins[k]]; }
-  if (nt > c->D.tcap || nv + ni > c->D.vcap) throw std::runtime_error("mesh capacity exceeded");
-  CK(cudaMemcpyAsync(c->C.vid, vids.data(), 4 * (size_t)c->C.cap, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemcpyAsync(c->C.nt0, nt0s.data(), 4 * (size_t)c->C.cap, cudaMemcpyHostToDevice, c->st));
-  int* d_ins = c->tmpC;
-  CK(cudaMemcpyAsync(d_ins, ins.data(), 4 * ni, cudaMemcpyHostToDevice, c->st));
-  Ins I; I.list = d_ins; I.n = ni; I.nv0 = nv; I.nt0base = c->hc.nt;
-  LAUNCH(k_ins_vertices, ni, c->D, c->C, I);
-  // 2D retiling items (candidate, polygon), candidates in priority order
-  std::vector<int> icand, ipid, item_of(2 * ni, 0);
-  if (c->npoly > 0) {
-    std::vector<int> sids;
-    for (int k = 0; k < ni; ++k) {
-      int cnd = ins[k];
-      item_of[2 * k] = (int)icand.size();
-      if (kinds[cnd] == K_SEG) {
-        int2 e; int sid;
-        CK(cudaMemcpy(&sid, c->D.sg_sid + tg[cnd], 4, cudaMemcpyDeviceToHost));
-        (void)e;
-        for (int pid : c->polys[sid]) { icand.push_back(cnd); ipid.push_back(pid); }
-      } else if (kinds[cnd] == K_FACE) {
-        int4 f;
-        CK(cudaMemcpy(&f, c->D.sf_v + tg[cnd], 16, cudaMemcpyDeviceToHost));
-        icand.push_back(cnd); ipid.push_back(f.w);
-      }
-      item_of[2 * k + 1] = (int)icand.size();
+__global__ void k_states(Cand C, int n, int* okf, int* failf) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    int st = C.status[c];
+    int s = st == CS_OK ? 0 : (st == CS_DROP ? -1 : 3);
+    C.state[c] = s;
+    okf[c] = s == 0;
+    failf[c] = s == 3;
+  }
+}
+__global__ void k_kept(Cand C, int n, int* keep) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) keep[c] = C.status[c] != CS_DROP;
+}
+__global__ void k_acc_byrank(Cand C, int n, int* byrank) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+    if (C.state[c] == 1) byrank[C.rank[c]] = c;
+}
+__global__ void k_nonneg(const int* a, int n, int* f) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) f[i] = a[i] >= 0;
+}
+__global__ void k_gather_i32(const int* src, const int* idx, int n, int* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[idx[i]];
+}
+__global__ void k_item_count(Dev D, Cand C, const int* ins, int ni, int* cnt) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ni; k += gridDim.x * blockDim.x) {
+    int c = ins[k], kind = C.kind[c];
+    if (kind == K_SEG) { int sid = D.sg_sid[C.tgt[c]]; cnt[k] = D.segpoly_off[sid + 1] - D.segpoly_off[sid]; }
+    else cnt[k] = kind == K_FACE ? 1 : 0;
+  }
+}
+__global__ void k_item_fill(Dev D, Cand C, const int* ins, int ni, const int* off, const int* cnt, T2Items T, int* item_of) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ni; k += gridDim.x * blockDim.x) {
+    int c = ins[k], kind = C.kind[c], o = off[k];
+    item_of[2 * k] = o; item_of[2 * k + 1] = o + cnt[k];
+    if (kind == K_SEG) {
+      int sid = D.sg_sid[C.tgt[c]];
+      for (int j = 0; j < cnt[k]; ++j) { T.cand[o + j] = c; T.pid[o + j] = D.segpoly[D.segpoly_off[sid] + j]; T.state[o + j] = 0; T.nrem[o + j] = 0; }
+    } else if (kind == K_FACE) {
+      T.cand[o] = c; T.pid[o] = D.sf_v[C.tgt[c]].w; T.state[o] = 0; T.nrem[o] = 0;
     }
   }
-  int nit = (int)icand.size();
-  int* d_item_of = nullptr;
-  if (nit > 0) {
+}
+__global__ void k_bump(Dev D, int dnv, int dnt) { D.ctr->nv += dnv; D.ctr->nt += dnt; }
+__global__ void k_pool_pos(Cand C, int n, const int* keepscan, const int* keep) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+    C.pool[c] = keep[c] ? keepscan[c] : -1;
+}
+
+struct RoundOut { int phase = -1; long long ncand = 0, acc = 0, rej = 0, failed = 0, inserted = 0; };
+
+static double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
+static double g_prof[8];
+static const char* g_prof_names[8] = {"pool", "regions", "filter", "insert", "2d", "fallback", "post", "other"};
+
+// scan of n ints; returns the total
+static int scan_total(gq_ctx* c, const int* in, int* out, int n) {
+  if (n <= 0) return 0;
+  exclusive_scan(c, in, out, n);
+  int a = 0, b = 0;
+  CK(cudaMemcpyAsync(&a, in + n - 1, 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(&b, out + n - 1, 4, cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  return a + b;
+}
+
+static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* inserted, int round_no) {
+  Cand& C = c->C;
+  double t0 = now_s();
+  int* byrank = c->Q.a; int* flags = c->Q.b; int* pos = c->Q.c; int* acc = c->Q.d; int* ins = c->Q.e;
+  CK(cudaMemsetAsync(byrank, 0xff, 4 * (size_t)n, c->st));
+  LAUNCH(k_acc_byrank, n, C, n, byrank);
+  LAUNCH(k_nonneg, n, byrank, n, flags);
+  int na = select_flagged(c, flags, n, pos);
+  *nacc_out = na;
+  if (na == 0) return;
+  LAUNCH(k_gather_i32, na, byrank, pos, na, acc);
+  LAUNCH(k_accept_flags, na, c->D, C, acc, na, flags, c->L, round_no, c->D.lmin2);
+  int ni = select_flagged(c, flags, na, pos);
+  *inserted += ni;
+  if (ni == 0) return;
+  LAUNCH(k_gather_i32, ni, acc, pos, ni, ins);
+  pull(c);
+  int nv = c->hc.nv, nt = c->hc.nt;
+  LAUNCH(k_gather_nbf, ni, C, ins, ni, flags);
+  int tot = scan_total(c, flags, pos, ni);
+  if (nt + tot > c->D.tcap || nv + ni > c->D.vcap) throw std::runtime_error("mesh capacity exceeded");
+  LAUNCH(k_assign_ids, ni, C, ins, ni, pos, nv, nt);
+  Ins I; I.list = ins; I.n = ni; I.nv0 = nv; I.nt0base = nt;
+  LAUNCH(k_ins_vertices, ni, c->D, C, I);
+  // facet 2D retiling work items (candidate, polygon) in priority order
+  int* item_of = nullptr;
+  int nit = 0;
+  if (c->npoly > 0) {
+    LAUNCH(k_item_count, ni, c->D, C, ins, ni, flags);
+    nit = scan_total(c, flags, pos, ni);
     if (nit > (1 << 16)) throw std::runtime_error("too many 2D items");
-    std::vector<int> z(nit, 0);
-    CK(cudaMemcpyAsync(c->T.cand, icand.data(), 4 * nit, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->T.pid, ipid.data(), 4 * nit, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->T.state, z.data(), 4 * nit, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->T.nrem, z.data(), 4 * nit, cudaMemcpyHostToDevice, c->st));
+    item_of = c->Q.f;
+    if (nit > 0) LAUNCH(k_item_fill, ni, c->D, C, ins, ni, pos, flags, c->T, item_of);
+  }
+  g_prof[3] += now_s() - t0;
+  double t1 = now_s();
+  if (nit > 0) {
     c->T.n = nit;
-    // subsegment split bookkeeping happens before the 2D passes only for
-    // vsid (k_ins_vertices); records are retired after the passes
     int left = nit;
     for (int pass = 0; left > 0; ++pass) {
-      LAUNCH_S(k_t2_compute, nit, c->D, c->C, c->T, c->S);
-      LAUNCH(k_t2_claim, nit, c->D, c->C, c->T);
+      LAUNCH_S(k_t2_compute, nit, c->D, C, c->T, c->S);
+      LAUNCH(k_t2_claim, nit, c->D, C, c->T);
       CK(cudaMemsetAsync(c->d_int + 16, 0, 4, c->st));
-      LAUNCH_S(k_t2_apply, nit, c->D, c->C, c->T, c->S, c->d_int + 16);
-      LAUNCH(k_t2_reset, nit, c->D, c->C, c->T, 1);
-      LAUNCH_S(k_t2_commit, nit, c->D, c->C, c->T, c->S);
+      LAUNCH_S(k_t2_apply, nit, c->D, C, c->T, c->S, c->d_int + 16);
+      LAUNCH(k_t2_reset, nit, c->D, C, c->T, 1);
+      LAUNCH_S(k_t2_commit, nit, c->D, C, c->T, c->S);
       LAUNCH(k_t2_retire, nit, c->D, c->T);
       int applied = read_int(c, c->d_int + 16);
       left -= applied;
       if (applied == 0) throw std::runtime_error("2D retiling made no progress");
     }
-    d_item_of = c->tmpB;
-    CK(cudaMemcpyAsync(d_item_of, item_of.data(), 4 * 2 * ni, cudaMemcpyHostToDevice, c->st));
   }
-  LAUNCH(k_ins_segsplit, ni, c->D, c->C, I);
-  LAUNCH(k_kill_cavities, ni, c->D, c->C, I);
-  LAUNCH(k_star, ni, c->D, c->C, I);
-  c->hc.nt = nt; c->hc.nv = nv + ni;
-  // counters nsegrec/nfacerec/nt2 were advanced by kernels: merge
-  Counters dc;
-  CK(cudaMemcpyAsync(&dc, c->dctr, sizeof dc, cudaMemcpyDeviceToHost, c->st));
-  sync(c);
-  dc.nt = nt; dc.nv = nv + ni;
-  c->hc = dc;
-  push(c);
-  LAUNCH_S(k_post_insert, ni, c->D, c->C, I, c->T, c->S, (const int*)d_item_of);
-  sync(c);
+  g_prof[4] += now_s() - t1;
+  t1 = now_s();
+  LAUNCH(k_ins_segsplit, ni, c->D, C, I);
+  LAUNCH(k_kill_cavities, ni, c->D, C, I);
+  LAUNCH(k_star, ni, c->D, C, I);
+  LAUNCH(k_bump, 1, c->D, ni, tot);
+  LAUNCH_S(k_post_insert, ni, c->D, C, I, c->T, c->S, (const int*)item_of);
+  g_prof[3] += now_s() - t1;
+}
+
+// appends the records flagged RF_REDIR of a phase as candidates (sorted)
+static int append_redirects(gq_ctx* c, int phase, int at, int pool0, CandCtx X) {
+  pull(c);
+  int nr = sorted_records(c, phase, RF_REDIR, 0, c->Q.g);
+  int nrec = phase == 0 ? c->hc.nsegrec : c->hc.nfacerec;
+  if (nrec > 0) LAUNCH(k_clear_redir, nrec, c->D, phase);
+  if (nr == 0) return 0;
+  grow_cands_keep(c, at + nr, at);
+  LAUNCH(k_set_cands, nr, c->C, at, nr, phase == 0 ? K_SEG : K_FACE, c->Q.g, pool0);
+  LAUNCH_S(k_make_cands, nr, c->D, c->C, c->S, at, at + nr, X, c->L, c->D.lmin2);
+  return nr;
+}
+
+static void ensure_q(gq_ctx* c, size_t n) {
+  if (n <= c->Q.cap) return;
+  int** ps[] = {&c->Q.a, &c->Q.b, &c->Q.c, &c->Q.d, &c->Q.e, &c->Q.f, &c->Q.g, &c->Q.h};
+  size_t cap = n + n / 2;
+  for (int** q : ps) { if (*q) cudaFree(*q); *q = dmalloc<int>(cap); }
+  c->Q.cap = cap;
 }
 
 static RoundOut run_round(gq_ctx* c, int round_no) {
   RoundOut R;
   c->big_used = 0;
+  pull(c);
+  ensure_q(c, (size_t)std::max(std::max(c->hc.nt, c->hc.nsegrec + c->hc.nfacerec), c->C.cap) * 2 + 4096);
+  ensure_tmp(c, (size_t)std::max(std::max(c->hc.nt, c->hc.nsegrec + c->hc.nfacerec), c->C.cap) + 4096);
+  double t0 = now_s();
   CandCtx X; X.round_no = round_no; X.seed = c->seed; X.with_facets = c->npoly > 0;
   double lmin2 = c->D.lmin2;
-  std::vector<int> kinds, tgts, pool;
-  int phase = -1;
-  // ---- segments
-  std::vector<int> segs = pending_sorted(c, 0);
-  int nbase = 0;
-  if (!segs.empty()) {
+  int phase = -1, nbase = 0;
+  pull(c);
+  int ns = sorted_records(c, 0, RF_ENC, RF_BLOCK | RF_SKIP, c->Q.g);
+  if (ns > 0) {
     phase = 0;
-    ensure_cands(c, (int)segs.size());
-    for (size_t k = 0; k < segs.size(); ++k) { kinds.push_back(K_SEG); tgts.push_back(segs[k]); pool.push_back((int)k); }
-    upload_candidates(c, 0, kinds, tgts, pool);
-    nbase = (int)segs.size();
-    LAUNCH_S(k_make_cands, nbase, c->D, c->C, c->S, 0, nbase, X, c->L, lmin2);
-    run_regions(c, 0, nbase, 0);
+    ensure_cands(c, ns);
+    LAUNCH(k_set_cands, ns, c->C, 0, ns, K_SEG, c->Q.g, 0);
+    LAUNCH_S(k_make_cands, ns, c->D, c->C, c->S, 0, ns, X, c->L, lmin2);
+    g_prof[0] += now_s() - t0;
+    double t1 = now_s();
+    run_regions(c, 0, ns, 0);
+    g_prof[1] += now_s() - t1;
+    nbase = ns;
+    R.ncand = ns;
   } else {
-    std::vector<int> faces = pending_sorted(c, 1);
-    std::vector<int> bad;
-    if (!faces.empty()) {
+    int nf = sorted_records(c, 1, RF_ENC, RF_BLOCK | RF_SKIP, c->Q.g);
+    if (nf > 0) {
       phase = 1;
-      ensure_cands(c, (int)faces.size() + 64);
-      for (size_t k = 0; k < faces.size(); ++k) { kinds.push_back(K_FACE); tgts.push_back(faces[k]); pool.push_back((int)k); }
+      ensure_cands(c, nf + 64);
+      LAUNCH(k_set_cands, nf, c->C, 0, nf, K_FACE, c->Q.g, 0);
+      nbase = nf;
     } else {
-      pull(c);
-      ensure_tmp(c, c->hc.nt + 1);
-      LAUNCH(k_flag_bad, c->hc.nt, c->D, c->B, c->tmpA);
-      int nb = select_flagged(c, c->tmpA, c->hc.nt, c->tmpB);
+      LAUNCH(k_flag_bad, c->hc.nt, c->D, c->B, c->Q.a);
+      int nb = select_flagged(c, c->Q.a, c->hc.nt, c->Q.g);
       if (nb == 0) { R.phase = -1; return R; }
-      bad.resize(nb);
-      CK(cudaMemcpy(bad.data(), c->tmpB, 4 * (size_t)nb, cudaMemcpyDeviceToHost));
       phase = 2;
       ensure_cands(c, nb + 64);
-      for (int k = 0; k < nb; ++k) { kinds.push_back(K_TET); tgts.push_back(bad[k]); pool.push_back(k); }
+      LAUNCH(k_set_cands, nb, c->C, 0, nb, K_TET, c->Q.g, 0);
+      nbase = nb;
     }
-    upload_candidates(c, 0, kinds, tgts, pool);
-    nbase = (int)tgts.size();
     LAUNCH_S(k_make_cands, nbase, c->D, c->C, c->S, 0, nbase, X, c->L, lmin2);
-    run_regions(c, 0, nbase, 0);
+    double t1 = now_s();
+    // redirects first (refine.py:603-662): dropped candidates need no region
     grid_sync(c);
     LAUNCH(k_grid_cands, nbase, c->D, c->G, c->C, 0, nbase);
     LAUNCH(k_redirect, nbase, c->D, c->C, 0, nbase);
-    sync(c);
-    std::vector<int> rs = take_redirects(c, 0);
-    std::vector<int> rf = phase == 2 ? take_redirects(c, 1) : std::vector<int>();
-    std::vector<int> st(nbase);
-    CK(cudaMemcpy(st.data(), c->C.status, 4 * (size_t)nbase, cudaMemcpyDeviceToHost));
-    int kept = 0;
-    for (int k = 0; k < nbase; ++k) if (st[k] != CS_DROP) ++kept;
-    // pool positions: kept originals first, then redirect segments, then faces
-    std::vector<int> pos(nbase, -1);
-    int q = 0;
-    for (int k = 0; k < nbase; ++k) if (st[k] != CS_DROP) pos[k] = q++;
-    CK(cudaMemcpy(c->C.pool, pos.data(), 4 * (size_t)nbase, cudaMemcpyHostToDevice));
-    int nextra = (int)(rs.size() + rf.size());
-    if (nextra) {
-      sync(c);
-      grow_cands_keep(c, nbase + nextra, nbase);
-      std::vector<int> k2, t2, p2;
-      for (int r : rs) { k2.push_back(K_SEG); t2.push_back(r); p2.push_back(q++); }
-      for (int r : rf) { k2.push_back(K_FACE); t2.push_back(r); p2.push_back(q++); }
-      upload_candidates(c, nbase, k2, t2, p2);
-      LAUNCH_S(k_make_cands, nextra, c->D, c->C, c->S, nbase, nbase + nextra, X, c->L, lmin2);
-      run_regions(c, nbase, nbase + nextra, 0);
-    }
-    R.ncand = q;
-    nbase += nextra;
-    if (q == 0) { R.phase = -1; return R; }
+    ensure_tmp(c, nbase + 1);
+    LAUNCH(k_kept, nbase, c->C, nbase, c->Q.a);
+    int kept = scan_total(c, c->Q.a, c->Q.b, nbase);
+    LAUNCH(k_pool_pos, nbase, c->C, nbase, c->Q.b, c->Q.a);
+    int nrs = append_redirects(c, 0, nbase, kept, X);
+    int nrf = phase == 2 ? append_redirects(c, 1, nbase + nrs, kept + nrs, X) : 0;
+    R.ncand = kept + nrs + nrf;
+    g_prof[0] += now_s() - t0;
+    t1 = now_s();
+    nbase += nrs + nrf;
+    run_regions(c, 0, nbase, 0);
+    g_prof[1] += now_s() - t1;
+    if (R.ncand == 0) { R.phase = -1; return R; }
   }
   int n = nbase;
-  std::vector<int> st(n), poolpos(n);
-  CK(cudaMemcpy(st.data(), c->C.status, 4 * (size_t)n, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(poolpos.data(), c->C.pool, 4 * (size_t)n, cudaMemcpyDeviceToHost));
-  if (phase == 0) R.ncand = n;
-  if (phase == 0) {
-    int drop = 0;
-    for (int k = 0; k < n; ++k) if (st[k] == CS_DROP) ++drop;
-    R.ncand = n - drop;
-  }
-  std::vector<int> ok, failed;
-  std::vector<int> state(n, -1);
-  for (int k = 0; k < n; ++k) {
-    if (st[k] == CS_DROP) { state[k] = -1; continue; }
-    if (st[k] == CS_OK) { ok.push_back(k); state[k] = 0; }
-    else { failed.push_back(k); state[k] = 3; }
-  }
-  std::sort(failed.begin(), failed.end(), [&](int a, int b) { return poolpos[a] < poolpos[b]; });
-  CK(cudaMemcpy(c->C.state, state.data(), 4 * (size_t)n, cudaMemcpyHostToDevice));
-  rank_candidates(c, ok);
+  double t1 = now_s();
+  ensure_tmp(c, n + 1);
+  LAUNCH(k_states, n, c->C, n, c->Q.a, c->Q.b);
+  int nok = scan_total(c, c->Q.a, c->Q.c, n);
+  int nfail = select_flagged(c, c->Q.b, n, c->Q.h);
+  rank_candidates(c, n);
   run_filter(c, n, nullptr);
-  CK(cudaMemcpy(state.data(), c->C.state, 4 * (size_t)n, cudaMemcpyDeviceToHost));
-  std::vector<int> rank(n);
-  CK(cudaMemcpy(rank.data(), c->C.rank, 4 * (size_t)n, cudaMemcpyDeviceToHost));
-  std::vector<int> acc;
-  for (int k : ok) if (state[k] == 1) acc.push_back(k);
-  std::sort(acc.begin(), acc.end(), [&](int a, int b) { return rank[a] < rank[b]; });
-  R.acc = (long long)acc.size();
-  R.rej = (long long)ok.size() - R.acc;
-  R.failed = (long long)failed.size();
+  g_prof[2] += now_s() - t1;
+  R.failed = nfail;
   R.phase = phase;
-  insert_accepted(c, acc, &R.inserted, round_no);
-  if (!failed.empty()) {
-    ensure_tmp(c, failed.size() + 1);
-    CK(cudaMemcpy(c->tmpA, failed.data(), 4 * failed.size(), cudaMemcpyHostToDevice));
-    FallbackIO F; F.list = c->tmpA; F.n = (int)failed.size(); F.round_no = round_no; F.seed = c->seed;
+  insert_accepted(c, n, &R.acc, &R.inserted, round_no);
+  R.rej = nok - R.acc;
+  t1 = now_s();
+  if (nfail > 0) {
+    FallbackIO F; F.list = c->Q.h; F.n = nfail; F.round_no = round_no; F.seed = c->seed;
     F.with_facets = c->npoly > 0; F.lmin2 = lmin2; F.inserted = c->d_int + 20;
-    CK(cudaMemset(c->d_int + 20, 0, 4));
-    T2Items T = c->T;
-    k_fallback<<<1, 1, 0, c->st>>>(c->D, c->C, c->SB, F, T, c->L);
+    CK(cudaMemsetAsync(c->d_int + 20, 0, 4, c->st));
+    k_fallback<<<1, 1, 0, c->st>>>(c->D, c->C, c->SB, F, c->T, c->L);
     c->launches++;
     CK(cudaGetLastError());
-    sync(c);
     R.inserted += read_int(c, c->d_int + 20);
-    pull(c);
   }
+  g_prof[5] += now_s() - t1;
+  t1 = now_s();
   // post round: new vertices vs every constraint ball, then new / dirty
   // constraints vs the vertices around them
   grid_sync(c);
@@ -2330,7 +2387,6 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   CK(cudaMemsetAsync(c->d_int, 0, 16, c->st));
   LAUNCH_S(k_check, c->hc.nsegrec + c->hc.nfacerec, c->D, c->S, 0, c->d_int);
   if (R.inserted > 0) LAUNCH(k_clear_flag, c->hc.nsegrec + c->hc.nfacerec, c->D, RF_BLOCK);
-  sync(c);
   if (c->hc.nt > 4096) {
     ensure_tmp(c, c->hc.nt + 1);
     LAUNCH(k_compact_flags, c->hc.nt, c->D, c->tmpA);
@@ -2341,6 +2397,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     int alive = read_int(c, c->d_int + 30);
     if ((long long)alive * 2 < c->hc.nt) compact_tets(c);
   }
+  g_prof[6] += now_s() - t1;
   return R;
 }
 
@@ -2474,6 +2531,11 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   CK(cudaEventRecord(c->ev1, c->st));
   sync(c);
   float ms = 0; cudaEventElapsedTime(&ms, c->ev0, c->ev1); c->dev_ms = ms;
+  if (getenv("GQ_PROFILE")) {
+    std::fprintf(stderr, "[gq profile] init %.1f ms (%d rounds);", c->init_ms, c->init_rounds);
+    for (int k = 0; k < 8; ++k) { std::fprintf(stderr, " %s %.1f ms;", g_prof_names[k], 1000 * g_prof[k]); g_prof[k] = 0; }
+    std::fprintf(stderr, " region kernels %.1f ms; launches %lld\n", c->region_ms, c->launches);
+  }
   pull(c);
   if (out) {
     std::memset(out, 0, sizeof(*out));
@@ -2527,6 +2589,8 @@ int gq_create(int device, gq_ctx** out) {
     CK(cudaEventCreate(&c->ev0)); CK(cudaEventCreate(&c->ev1));
     CK(cudaEventCreate(&c->er0)); CK(cudaEventCreate(&c->er1));
     CK(cudaDeviceSetLimit(cudaLimitStackSize, 16384));
+    CK(cudaFuncSetAttribute(k_region_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BlockShared)));
+    CK(cudaFuncSetAttribute(k_init_region_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BlockShared)));
   } catch (std::exception& e) {
     c->err = e.what();
     *out = c;
