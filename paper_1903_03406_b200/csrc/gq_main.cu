@@ -1611,6 +1611,16 @@ struct gq_ctx {
   bool allocated = false;
 };
 
+static double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
+static double g_prof[8];
+// fine stage timers (GQ_PROFILE=2): synchronise and charge the elapsed time
+static bool g_fine = false;
+static double g_fine_t[24];
+static const char* g_fine_names[24] = {"i.region", "i.big", "i.filter", "i.scan", "i.kill", "i.stars", "i.compact",
+  "p.gridsync", "p.newverts", "p.check", "p.compact", "r.sorted", "r.make", "r.redirect", "r.append", "f.states",
+  "f.rank", "f.lfmis", "x.acc", "x.ids", "x.star", "x.postins", "i.misc", "r.misc"};
+static double g_fine_last = 0;
+static void fine(gq_ctx* c, int k);
 static void sync(gq_ctx* c) {
   CK(cudaStreamSynchronize(c->st));
   unsigned int e = 0;
@@ -2067,12 +2077,15 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
   int nt = c->hc.nt;
   int left = np, inserted = 4;
   double wf = getenv("GQ_INIT_WINDOW") ? atof(getenv("GQ_INIT_WINDOW")) : 1.0;
+  fine(c, -1);
   for (int round = 0; left > 0; ++round) {
     int W = (int)std::min<double>(left, std::max(64.0, wf * inserted));
+    fine(c, 22);
     CK(cudaEventRecord(c->er0, c->st));
     LAUNCH_S(k_init_region, W, c->D, C, c->S, d_pend, d_plist, W, d_hint, d_succ, d_touched, round, 0);
     CK(cudaEventRecord(c->er1, c->st));
     time_region(c);
+    fine(c, 0);
     // big cavities (early rounds): resolve the lowest-order ones, truncate the window at the rest
     std::vector<int> bl;
     {
@@ -2107,9 +2120,11 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
         CK(cudaMemcpyAsync(c->tmpC, bl.data(), 4 * (size_t)nb, cudaMemcpyHostToDevice, c->st));
       }
     }
+    fine(c, 1);
     LAUNCH(k_init_claim, W, c->D, C, c->W, d_plist, W);
     LAUNCH(k_init_decide, W, c->D, C, c->W, d_plist, W, d_acc);
     LAUNCH(k_init_unclaim, W, c->D, C, c->W, d_plist, W);
+    fine(c, 2);
     LAUNCH(k_init_nbf, W, C, d_plist, d_acc, W, d_keep);
     exclusive_scan(c, d_keep, d_scan, W);
     int lastn = 0, lasts = 0, lasta = 0;
@@ -2124,8 +2139,11 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     int nacc = lastacc_scan + lasta;
     int add_t = lasts + lastn;
     if (nt + add_t > c->D.tcap) throw std::runtime_error("tet capacity exceeded in init");
+    fine(c, 3);
     LAUNCH(k_init_kill, W, c->D, C, d_plist, d_acc, d_scan, W, nt, d_succ);
+    fine(c, 4);
     LAUNCH(k_init_stars, W, c->D, C, d_pend, d_plist, d_acc, W, d_touched, round);
+    fine(c, 5);
     nt += add_t;
     // release big slabs (big regions are recomputed next round if still pending)
     LAUNCH(k_init_keep, W, d_acc, W, d_keep);
@@ -2139,6 +2157,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     push(c);
     if (nacc == 0) throw std::runtime_error("init made no progress");
     c->init_rounds = round + 1;
+    fine(c, 6);
   }
   // big-slab candidates must not keep stale bigi for the refinement rounds
   sync(c);
@@ -2197,8 +2216,7 @@ __global__ void k_pool_pos(Cand C, int n, const int* keepscan, const int* keep) 
 
 struct RoundOut { int phase = -1; long long ncand = 0, acc = 0, rej = 0, failed = 0, inserted = 0; };
 
-static double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
-static double g_prof[8];
+
 static const char* g_prof_names[8] = {"pool", "regions", "filter", "insert", "2d", "fallback", "post", "other"};
 
 // scan of n ints; returns the total
@@ -2295,6 +2313,14 @@ static void ensure_q(gq_ctx* c, size_t n) {
   c->Q.cap = cap;
 }
 
+static void fine(gq_ctx* c, int k) {
+  if (!g_fine) return;
+  CK(cudaStreamSynchronize(c->st));
+  double t = now_s();
+  if (k >= 0) g_fine_t[k] += t - g_fine_last;
+  g_fine_last = t;
+}
+
 static RoundOut run_round(gq_ctx* c, int round_no) {
   RoundOut R;
   c->big_used = 0;
@@ -2302,6 +2328,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   ensure_q(c, (size_t)std::max(std::max(c->hc.nt, c->hc.nsegrec + c->hc.nfacerec), c->C.cap) * 2 + 4096);
   ensure_tmp(c, (size_t)std::max(std::max(c->hc.nt, c->hc.nsegrec + c->hc.nfacerec), c->C.cap) + 4096);
   double t0 = now_s();
+  fine(c, -1);
   CandCtx X; X.round_no = round_no; X.seed = c->seed; X.with_facets = c->npoly > 0;
   double lmin2 = c->D.lmin2;
   int phase = -1, nbase = 0;
@@ -2355,13 +2382,17 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     if (R.ncand == 0) { R.phase = -1; return R; }
   }
   int n = nbase;
+  fine(c, 23);
   double t1 = now_s();
   ensure_tmp(c, n + 1);
   LAUNCH(k_states, n, c->C, n, c->Q.a, c->Q.b);
   int nok = scan_total(c, c->Q.a, c->Q.c, n);
   int nfail = select_flagged(c, c->Q.b, n, c->Q.h);
+  fine(c, 15);
   rank_candidates(c, n);
+  fine(c, 16);
   run_filter(c, n, nullptr);
+  fine(c, 17);
   g_prof[2] += now_s() - t1;
   R.failed = nfail;
   R.phase = phase;
@@ -2381,12 +2412,16 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   t1 = now_s();
   // post round: new vertices vs every constraint ball, then new / dirty
   // constraints vs the vertices around them
+  fine(c, -1);
   grid_sync(c);
+  fine(c, 7);
   if (c->hc.nv > c->reg_nv) LAUNCH(k_grid_newverts, c->hc.nv - c->reg_nv, c->D, c->G, c->reg_nv, c->hc.nv);
   c->reg_nv = c->hc.nv;
+  fine(c, 8);
   CK(cudaMemsetAsync(c->d_int, 0, 16, c->st));
   LAUNCH_S(k_check, c->hc.nsegrec + c->hc.nfacerec, c->D, c->S, 0, c->d_int);
   if (R.inserted > 0) LAUNCH(k_clear_flag, c->hc.nsegrec + c->hc.nfacerec, c->D, RF_BLOCK);
+  fine(c, 9);
   if (c->hc.nt > 4096) {
     ensure_tmp(c, c->hc.nt + 1);
     LAUNCH(k_compact_flags, c->hc.nt, c->D, c->tmpA);
@@ -2397,6 +2432,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     int alive = read_int(c, c->d_int + 30);
     if ((long long)alive * 2 < c->hc.nt) compact_tets(c);
   }
+  fine(c, 10);
   g_prof[6] += now_s() - t1;
   return R;
 }
@@ -2405,6 +2441,7 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
                         const int* pidx, int f, const int* keep, const int* order, const gq_config* cfg,
                         gq_counts* out) {
   c->B = cfg->B; c->max_rounds = cfg->max_rounds; c->seed = cfg->seed; c->verbose = cfg->flags & 1;
+  g_fine = getenv("GQ_PROFILE") && atoi(getenv("GQ_PROFILE")) >= 2;
   c->n_input = n_input; c->npoly = f;
   c->rounds.clear(); c->rtimes.clear(); c->launches = 0; c->region_ms = 0;
   free_all(c);
@@ -2531,6 +2568,11 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   CK(cudaEventRecord(c->ev1, c->st));
   sync(c);
   float ms = 0; cudaEventElapsedTime(&ms, c->ev0, c->ev1); c->dev_ms = ms;
+  if (g_fine) {
+    std::fprintf(stderr, "[gq fine]");
+    for (int k = 0; k < 24; ++k) if (g_fine_t[k] > 0) { std::fprintf(stderr, " %s %.1f;", g_fine_names[k], 1000 * g_fine_t[k]); g_fine_t[k] = 0; }
+    std::fprintf(stderr, "\n");
+  }
   if (getenv("GQ_PROFILE")) {
     std::fprintf(stderr, "[gq profile] init %.1f ms (%d rounds);", c->init_ms, c->init_rounds);
     for (int k = 0; k < 8; ++k) { std::fprintf(stderr, " %s %.1f ms;", g_prof_names[k], 1000 * g_prof[k]); g_prof[k] = 0; }
