@@ -89,7 +89,7 @@ __device__ inline int region_block(const Dev& D, const double* p, const int* see
   if (B.status != RS_OK) return B.status;
   if (tid == 0) {
     int s = bh_claim(B, B.seed);
-    B.hval[s] = 0;
+    if (s >= 0) B.hval[s] = 0;
     B.cav[0] = B.seed; B.n = 1;
     B.f0[0] = B.seed; B.nf0 = 1;
   }

@@ -31,6 +31,7 @@
 
 #include "gq_dev.cuh"
 #include "gq_block.cuh"
+#include "gq_warp.cuh"
 #include "../../include/gqm3d.h"
 
 using namespace gq;
@@ -214,6 +215,7 @@ __device__ inline Allow allow_of(const Cand& C, int c) {
 __device__ __noinline__ int cand_seeds(const Dev& D, const Cand& C, int c, int* out, Scratch& S) {
   if (C.seed[c] >= 0) { out[0] = C.seed[c]; return 1; }
   int kind = C.kind[c], tgt = C.tgt[c];
+  DCHK(kind >= 0 && kind <= 2);
   if (kind == K_TET) { out[0] = tgt; return 1; }
   if (kind == K_SEG) {
     int2 e = D.sg_uv[tgt];
@@ -317,6 +319,91 @@ __global__ void k_region(Dev D, Cand C, Scr SC, int n0, int n1, const int* list,
     } else {
       C.status[c] = CS_CNSS;
     }
+  }
+}
+
+// one warp per candidate (the common case); overflowing cavities are marked
+// CS_OVF for the block kernel
+__global__ void __launch_bounds__(32 * WR_WARPS) k_region_warp(Dev D, Cand C, Scr SC, int n0, int n1) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpShared& W = reinterpret_cast<WarpShared*>(smem_raw)[wib];
+  const int gw = blockIdx.x * WR_WARPS + wib, nw = gridDim.x * WR_WARPS;
+  Scratch S = scratch_for(SC, gw);
+  for (int c = n0 + gw; c < n1; c += nw) {
+    if (C.status[c] != CS_OK) continue;
+    DCHK(C.bigi[c] == -1);
+    if (lane == 0) W.nseeds = cand_seeds(D, C, c, W.seeds, S);
+    __syncwarp();
+    int ns = W.nseeds;
+    DCHK(ns >= 0 && ns <= 32);
+    SlabView v = slab(C, c);
+    RegionOut O = region_view(C, c, v, 0);
+    int st = ns == 0 ? RS_CNSS : region_warp(D, C.p + 3 * (size_t)c, W.seeds, ns, allow_of(C, c), W, S, O);
+    if (lane == 0) {
+      atomicAdd(&g_region_calls, 1ull);
+      store_region(C, c, O);
+      if (st == RS_OK) {
+        atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf));
+        C.status[c] = (O.mind <= D.too_close_sq) ? CS_TOOCLOSE : CS_OK;
+      } else if (st == RS_OVERFLOW) C.status[c] = CS_OVF;
+      else if (st == RS_MEMBRANE) { C.status[c] = CS_MEMB; C.memb[c] = O.memb; }
+      else C.status[c] = CS_CNSS;
+    }
+    __syncwarp();
+  }
+}
+// bulk construction, warp per pending point (cached cavities re-validated)
+__global__ void __launch_bounds__(32 * WR_WARPS) k_init_region_warp(Dev D, Cand C, Scr SC, const int* pend, const int* plist,
+                                                                    int Wn, int* hint, const int* succ, const int* touched, int round) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpShared& W = reinterpret_cast<WarpShared*>(smem_raw)[wib];
+  const int gw = blockIdx.x * WR_WARPS + wib, nw = gridDim.x * WR_WARPS;
+  Scratch S = scratch_for(SC, gw);
+  for (int w = gw; w < Wn; w += nw) {
+    int c = plist[w];
+    if (lane == 0 && g_wdbg) { g_wdbg[2 * gw] = c; g_wdbg[2 * gw + 1] = 0; }
+    DCHK(c >= 0 && c < C.cap);
+    int st0 = C.status[c];
+    if (st0 == CS_OVF) continue;
+    if (st0 == CS_OK && C.memb[c] >= 0) {
+      SlabView v = slab(C, c);
+      bool bad = false;
+      for (int k = lane; k < C.ntet[c]; k += 32) {
+        int t = v.tets[k];
+        if (!D.alive[t] || touched[t] >= C.memb[c]) bad = true;
+      }
+      if (!__any_sync(0xffffffffu, bad)) continue;
+    }
+    int vtx = pend[c];
+    if (lane == 0 && g_wdbg) { g_wdbg[2 * gw] = c; g_wdbg[2 * gw + 1] = 1; }
+    DCHK(vtx >= 0 && vtx < D.vcap);
+    const double* p = PT(D, vtx);
+    if (lane == 0) {
+      int h = hint[c];
+      DCHK(h >= -1 && h < D.tcap);
+      while (h >= 0 && !D.alive[h]) h = succ[h];
+      int t = walk(D, p, h);
+      hint[c] = t;
+      W.seeds[0] = t;
+    }
+    __syncwarp();
+    SlabView sv = slab(C, c);
+    RegionOut O = region_view(C, c, sv, 0);
+    Allow A; A.n = 0;
+    if (lane == 0 && g_wdbg) g_wdbg[2 * gw + 1] = 2;
+    int r = region_warp(D, p, W.seeds, 1, A, W, S, O, true);
+    if (lane == 0 && g_wdbg) g_wdbg[2 * gw + 1] = 99;
+    if (lane == 0) {
+      atomicAdd(&g_region_calls, 1ull);
+      store_region(C, c, O);
+      C.extra[c] = -1; C.kind[c] = K_TET; C.rank[c] = c; C.memb[c] = round;
+      if (r == RS_OK) { C.status[c] = CS_OK; atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf)); }
+      else if (r == RS_OVERFLOW) { C.status[c] = CS_OVF; C.memb[c] = -1; }
+      else { C.status[c] = CS_CNSS; raise_err(GQ_ERR_DEGEN); }
+    }
+    __syncwarp();
   }
 }
 
@@ -1607,6 +1694,7 @@ struct gq_ctx {
   int reg_seg = 0, reg_face = 0, reg_nv = 0;
   int big_used = 0;
   int init_rounds = 0;
+  int4 *tv2 = nullptr, *tn2 = nullptr; uint8_t *sub2 = nullptr, *seg2 = nullptr, *skip2 = nullptr; double* ratio2 = nullptr;
   struct QBuf { int *a, *b, *c, *d, *e, *f, *g, *h; size_t cap; } Q{};
   bool allocated = false;
 };
@@ -1785,7 +1873,7 @@ static unsigned int pow2_at_least(size_t n) { unsigned int p = 1024; while (p < 
 static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   Dev& D = c->D;
   size_t vcap = std::max<size_t>(65536, (size_t)n * 24);
-  size_t tcap = std::max<size_t>(1 << 20, vcap * 16);
+  size_t tcap = std::max<size_t>(1 << 21, (size_t)n * 64);
   D.vcap = (int)vcap; D.tcap = (int)tcap;
   D.P = dmalloc<double>(3 * vcap); D.vorigin = dmalloc<uint8_t>(vcap); D.vert_tet = dmalloc<int>(vcap);
   D.vsid = dmalloc<int>(vcap);
@@ -1793,6 +1881,7 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   D.sub = dmalloc<uint8_t>(tcap); D.seg = dmalloc<uint8_t>(tcap); D.skip = dmalloc<uint8_t>(tcap);
   D.ratio = dmalloc<double>(tcap);
   CK(cudaMemset(D.alive, 0, tcap));
+  if (getenv("GQ_PROFILE")) std::fprintf(stderr, "[gq] capacities: verts %zu tets %zu\n", vcap, tcap);
   size_t sgcap = std::max<size_t>(4096, (size_t)m * 64 + vcap);
   D.sgcap = (int)sgcap;
   D.sg_uv = dmalloc<int2>(sgcap); D.sg_sid = dmalloc<int>(sgcap); D.sg_fl = dmalloc<unsigned int>(sgcap);
@@ -1867,13 +1956,14 @@ static void free_all(gq_ctx* c) {
                 c->S.comp, c->SB.tkey, c->SB.tval, c->SB.tep, c->SB.fkey, c->SB.fep, c->SB.epoch, c->SB.list,
                 c->SB.stack, c->SB.in, c->SB.comp, c->tmpA, c->tmpB, c->tmpC, c->k64a, c->k64b, c->k32a, c->k32b,
                 c->cub_tmp, c->d_order, c->G.head, c->G.nodes, c->G.big, c->G.nnodes, c->Q.a, c->Q.b, c->Q.c,
-                c->Q.d, c->Q.e, c->Q.f, c->Q.g, c->Q.h};
+                c->Q.d, c->Q.e, c->Q.f, c->Q.g, c->Q.h, c->tv2, c->tn2, c->sub2, c->seg2, c->skip2, c->ratio2};
   for (void* p : ps) if (p) cudaFree(p);
   free_cands(c->C);
   c->allocated = false;
   c->tmpcap = 0; c->cub_cap = 0; c->cub_tmp = nullptr;
   c->tmpA = c->tmpB = c->tmpC = nullptr; c->k64a = c->k64b = nullptr; c->k32a = c->k32b = nullptr; c->d_order = nullptr;
   c->Q = {};
+  c->tv2 = c->tn2 = nullptr; c->sub2 = c->seg2 = c->skip2 = nullptr; c->ratio2 = nullptr;
 }
 
 // regions for candidates [n0,n1): normal pass, then the overflow ones with big slabs
@@ -1886,7 +1976,15 @@ static void time_region(gq_ctx* c) {
 static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   if (n1 <= n0) return;
   CK(cudaEventRecord(c->er0, c->st));
-  LAUNCH_S(k_region, n1 - n0, c->D, c->C, c->S, n0, n1, (const int*)nullptr, probe, 0);
+  if (!getenv("GQ_THREAD_REGIONS")) {   // debug switch: per-thread kernel
+    long long nw = n1 - n0;
+    int blocks = (int)std::min<long long>((nw + WR_WARPS - 1) / WR_WARPS, c->S.nthreads / WR_WARPS);
+    k_region_warp<<<std::max(blocks, 1), 32 * WR_WARPS, WR_WARPS * sizeof(WarpShared), c->st>>>(c->D, c->C, c->S, n0, n1);
+    c->launches++;
+    CK(cudaGetLastError());
+  } else {
+    LAUNCH_S(k_region, n1 - n0, c->D, c->C, c->S, n0, n1, (const int*)nullptr, probe, 0);
+  }
   CK(cudaEventRecord(c->er1, c->st));
   time_region(c);
   // overflow pass
@@ -2020,22 +2118,22 @@ static void compact_tets(gq_ctx* c) {
   int last_flag = read_int(c, c->tmpA + nt - 1), last_scan = read_int(c, c->tmpB + nt - 1);
   int na = last_scan + last_flag;
   Dev& D = c->D;
-  int4* tv2 = dmalloc<int4>(D.tcap); int4* tn2 = dmalloc<int4>(D.tcap);
-  uint8_t* sub2 = dmalloc<uint8_t>(D.tcap); uint8_t* seg2 = dmalloc<uint8_t>(D.tcap);
-  double* r2 = dmalloc<double>(D.tcap); uint8_t* sk2 = dmalloc<uint8_t>(D.tcap);
-  LAUNCH(k_compact_move, nt, D, c->tmpB, nt, tv2, tn2, sub2, seg2, r2, sk2);
+  // double buffers, allocated once per context
+  if (!c->tv2) {
+    c->tv2 = dmalloc<int4>(D.tcap); c->tn2 = dmalloc<int4>(D.tcap);
+    c->sub2 = dmalloc<uint8_t>(D.tcap); c->seg2 = dmalloc<uint8_t>(D.tcap);
+    c->ratio2 = dmalloc<double>(D.tcap); c->skip2 = dmalloc<uint8_t>(D.tcap);
+  }
+  LAUNCH(k_compact_move, nt, D, c->tmpB, nt, c->tv2, c->tn2, c->sub2, c->seg2, c->ratio2, c->skip2);
   LAUNCH(k_compact_vt, c->hc.nv, D, c->tmpB, c->tmpA, c->hc.nv);
-  sync(c);
-  cudaFree(D.tv); cudaFree(D.tn); cudaFree(D.sub); cudaFree(D.seg); cudaFree(D.ratio); cudaFree(D.skip);
-  D.tv = tv2; D.tn = tn2; D.sub = sub2; D.seg = seg2; D.ratio = r2; D.skip = sk2;
-  CK(cudaMemsetAsync(D.alive, 0, D.tcap, c->st));
+  std::swap(D.tv, c->tv2); std::swap(D.tn, c->tn2); std::swap(D.sub, c->sub2); std::swap(D.seg, c->seg2);
+  std::swap(D.ratio, c->ratio2); std::swap(D.skip, c->skip2);
+  CK(cudaMemsetAsync(D.alive, 0, nt, c->st));
   CK(cudaMemsetAsync(D.alive, 1, na, c->st));
   c->hc.nt = na;
   push(c);
-  sync(c);
 }
 
-// ------------------------------------------------------------------ init
 static void ensure_big(gq_ctx* c, int need);
 static void init_delaunay(gq_ctx* c, const int* order, int n) {
   CK(cudaMemcpyAsync(c->d_order, order, 4 * (size_t)n, cudaMemcpyHostToDevice, c->st));
@@ -2082,7 +2180,38 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     int W = (int)std::min<double>(left, std::max(64.0, wf * inserted));
     fine(c, 22);
     CK(cudaEventRecord(c->er0, c->st));
-    LAUNCH_S(k_init_region, W, c->D, C, c->S, d_pend, d_plist, W, d_hint, d_succ, d_touched, round, 0);
+    if (!getenv("GQ_THREAD_INIT")) {
+      int blocks = std::min((W + WR_WARPS - 1) / WR_WARPS, c->S.nthreads / WR_WARPS);
+      static int* h_wdbg = nullptr;
+      if (getenv("GQ_WATCHDOG") && !h_wdbg) {
+        CK(cudaHostAlloc(&h_wdbg, 200000 * sizeof(int), cudaHostAllocMapped));
+        int* dptr; CK(cudaHostGetDevicePointer(&dptr, h_wdbg, 0));
+        CK(cudaMemcpyToSymbol(g_wdbg, &dptr, sizeof(dptr)));
+      }
+      if (h_wdbg) std::memset(h_wdbg, 0xff, 200000 * sizeof(int));
+      k_init_region_warp<<<std::max(blocks, 1), 32 * WR_WARPS, WR_WARPS * sizeof(WarpShared), c->st>>>(
+          c->D, C, c->S, d_pend, d_plist, W, d_hint, d_succ, d_touched, round);
+      c->launches++;
+      CK(cudaGetLastError());
+      if (h_wdbg) {
+        CK(cudaEventRecord(c->er1, c->st));
+        double t0w = now_s();
+        while (cudaEventQuery(c->er1) == cudaErrorNotReady && now_s() - t0w < 5.0) {}
+        if (cudaEventQuery(c->er1) == cudaErrorNotReady) {
+          int shown = 0, nstart = 0, ndone = 0;
+          for (int g = 0; g < 2 * 16384; g += 2) { nstart += h_wdbg[g] >= 0; ndone += h_wdbg[g + 1] == 99; }
+          std::fprintf(stderr, "[watchdog] round %d W %d warps started %d at-99 %d\n", round, W, nstart, ndone);
+          for (int g = 0; g < 2 * 16384 && shown < 20; g += 2) {
+            if (h_wdbg[g] >= 0 && h_wdbg[g + 1] != 99) { std::fprintf(stderr, "[watchdog] round %d warp %d cand %d stage %d\n", round, g / 2, h_wdbg[g], h_wdbg[g + 1]); ++shown; }
+          }
+          for (int g = 0; g < 64 * 32; ++g) if (h_wdbg[40000 + g] >= 0) std::fprintf(stderr, "%d:%d ", g, h_wdbg[40000 + g]);
+          std::fprintf(stderr, "\n[watchdog] kernel stuck; exiting\n");
+          std::_Exit(3);
+        }
+      }
+    } else {
+      LAUNCH_S(k_init_region, W, c->D, C, c->S, d_pend, d_plist, W, d_hint, d_succ, d_touched, round, 0);
+    }
     CK(cudaEventRecord(c->er1, c->st));
     time_region(c);
     fine(c, 0);
@@ -2313,7 +2442,9 @@ static void ensure_q(gq_ctx* c, size_t n) {
   c->Q.cap = cap;
 }
 
+static bool g_trace = false;
 static void fine(gq_ctx* c, int k) {
+  if (g_trace) { CK(cudaStreamSynchronize(c->st)); std::fprintf(stderr, "[trace] stage %d ok\n", k); }
   if (!g_fine) return;
   CK(cudaStreamSynchronize(c->st));
   double t = now_s();
@@ -2334,11 +2465,14 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   int phase = -1, nbase = 0;
   pull(c);
   int ns = sorted_records(c, 0, RF_ENC, RF_BLOCK | RF_SKIP, c->Q.g);
+  fine(c, 11);
   if (ns > 0) {
     phase = 0;
     ensure_cands(c, ns);
     LAUNCH(k_set_cands, ns, c->C, 0, ns, K_SEG, c->Q.g, 0);
+    fine(c, 12);
     LAUNCH_S(k_make_cands, ns, c->D, c->C, c->S, 0, ns, X, c->L, lmin2);
+    fine(c, 13);
     g_prof[0] += now_s() - t0;
     double t1 = now_s();
     run_regions(c, 0, ns, 0);
@@ -2442,6 +2576,8 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
                         gq_counts* out) {
   c->B = cfg->B; c->max_rounds = cfg->max_rounds; c->seed = cfg->seed; c->verbose = cfg->flags & 1;
   g_fine = getenv("GQ_PROFILE") && atoi(getenv("GQ_PROFILE")) >= 2;
+  g_trace = getenv("GQ_TRACE") != nullptr;
+  { int ws = getenv("GQ_WSTOP") ? atoi(getenv("GQ_WSTOP")) : 0; CK(cudaMemcpyToSymbol(g_wstop, &ws, 4)); }
   c->n_input = n_input; c->npoly = f;
   c->rounds.clear(); c->rtimes.clear(); c->launches = 0; c->region_ms = 0;
   free_all(c);
@@ -2632,6 +2768,8 @@ int gq_create(int device, gq_ctx** out) {
     CK(cudaEventCreate(&c->er0)); CK(cudaEventCreate(&c->er1));
     CK(cudaDeviceSetLimit(cudaLimitStackSize, 16384));
     CK(cudaFuncSetAttribute(k_region_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BlockShared)));
+    CK(cudaFuncSetAttribute(k_region_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared))));
+    CK(cudaFuncSetAttribute(k_init_region_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared))));
     CK(cudaFuncSetAttribute(k_init_region_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BlockShared)));
   } catch (std::exception& e) {
     c->err = e.what();

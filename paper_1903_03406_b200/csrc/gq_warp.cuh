@@ -1,0 +1,398 @@
+// gq_warp.cuh -- warp-cooperative Delaunay region (the common case).
+//
+// One warp computes one candidate's region with the decisions of
+// region_compute() (mesh.py:450-521 / _kernels.py:392-635): the 32 lanes
+// test the frontier's neighbours in parallel (FP-filtered insphere /
+// orient3d with the exact fallback), the grown set is a per-warp
+// shared-memory hash, peel / component are warp passes, and the finished
+// cavity is sorted (warp bitonic) and its boundary faces emitted through a
+// warp scan in the reference order.  Cavities larger than WR_MAXT tets
+// report RS_OVERFLOW and go to the block kernel (gq_block.cuh).
+#pragma once
+#include "gq_dev.cuh"
+
+namespace gq {
+
+#ifdef GQ_DCHECK
+#define DCHK(cond, ...) do { if (!(cond)) { printf("DCHECK %s:%d " #cond "\n", __FILE__, __LINE__); raise_err(GQ_ERR_CAP); } } while (0)
+#else
+#define DCHK(cond, ...) do {} while (0)
+#endif
+
+__device__ int g_wstop;
+__device__ volatile int* g_wdbg;      // pinned host mirror: [warp][2] = candidate, checkpoint
+#ifdef GQ_DCHECK
+#define WMARK(k) do { if (g_wdbg) { int gt_ = blockIdx.x * blockDim.x + threadIdx.x; g_wdbg[40000 + gt_] = (k) * 1000 + __LINE__ % 1000; } } while (0)
+#else
+#define WMARK(k) do {} while (0)
+#endif
+#define WSTOP(k) do { if (g_wstop == (k)) return RS_CNSS; } while (0)
+#define WR_MAXT 128
+#ifndef CC_DBG
+#define CC_DBG 96
+#endif
+#define WR_HASH 512
+#define WR_WARPS 8          // warps per block
+
+struct WarpShared {
+  int hkey[WR_HASH];
+  int hval[WR_HASH];
+  int cav[WR_MAXT];
+  int f0[WR_MAXT];
+  int f1[WR_MAXT];
+  int comp[WR_MAXT];
+  unsigned char in[WR_MAXT];
+  int n, nf, cnt, flag, memb, seed;
+  unsigned long long mind;
+  int seeds[32];
+  int nseeds;
+};
+
+__device__ __forceinline__ unsigned int wh(int k) { return ((unsigned int)k * 2654435761u) & (WR_HASH - 1); }
+__device__ inline int wh_claim(WarpShared& W, int k) {
+  unsigned int i = wh(k);
+  for (int p = 0; p < WR_HASH; ++p) {
+    int cur = W.hkey[i];
+    if (cur == k) return -1;
+    if (cur == INT_MIN) {
+      int old = atomicCAS(&W.hkey[i], INT_MIN, k);
+      if (old == INT_MIN) return (int)i;
+      if (old == k) return -1;
+    }
+    i = (i + 1) & (WR_HASH - 1);
+  }
+  return -2;
+}
+__device__ inline int wh_find(const WarpShared& W, int k) {
+  unsigned int i = wh(k);
+  for (int p = 0; p < WR_HASH; ++p) {
+    int cur = W.hkey[i];
+    if (cur == k) return W.hval[i];
+    if (cur == INT_MIN) return -1;
+    i = (i + 1) & (WR_HASH - 1);
+  }
+  return -1;
+}
+
+// All 32 lanes of the warp call this with the same arguments.  S is the
+// warp's global scratch (lane 0 only: walks and the constraint pass).
+__device__ inline int region_warp(const Dev& D, const double* p, const int* seeds, int nseeds, const Allow& A,
+                                  WarpShared& W, Scratch& S, RegionOut& O, bool walk_on_miss = true) {
+  const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  for (int i = lane; i < WR_HASH; i += 32) W.hkey[i] = INT_MIN;
+  __syncwarp();
+  // seed: first listed alive tet whose region contains p (tests in parallel)
+  int nc = nseeds < 32 ? nseeds : 32;
+  int t0 = lane < nc ? seeds[lane] : -1;
+  DCHK(t0 < D.tcap);
+  bool ok = t0 >= 0 && D.alive[t0] && in_region(D, t0, p, A);
+  unsigned bal = __ballot_sync(FULL, ok);
+  int seed = bal ? __shfl_sync(FULL, t0, __ffs(bal) - 1) : -1;
+  if (seed < 0) {
+    WMARK(50);
+    if (!walk_on_miss) return RS_CNSS;
+    if (lane == 0) {
+      int t = walk(D, p, nc > 0 ? seeds[0] : -1);
+      W.seed = (t >= 0 && D.alive[t] && in_region(D, t, p, A)) ? t : -1;
+    }
+    __syncwarp();
+    seed = W.seed;
+    WMARK(50);
+    if (seed < 0) return RS_CNSS;
+  }
+  O.seed = seed;
+  WSTOP(1);
+  WMARK(11);
+  if (lane == 0) {
+    int s = wh_claim(W, seed);       // the table is empty: always inserts
+    if (s >= 0) W.hval[s] = 0;
+    W.cav[0] = seed; W.n = 1; W.f0[0] = seed; W.flag = 0; W.memb = INT_MAX;
+  }
+  __syncwarp();
+  // ---- grow
+  int* cur = W.f0; int* nxt = W.f1;
+  int ncur = 1;
+  while (ncur > 0) {
+    if (lane == 0) W.nf = 0;
+    __syncwarp();
+    for (int j = lane; j < 4 * ncur; j += 32) {
+      DCHK((j >> 2) < WR_MAXT);
+      int t = cur[j >> 2], i = j & 3;
+      DCHK(t >= 0 && t < D.tcap);
+      int u = tnk(D, t, i) >> 2;
+      DCHK(u < D.tcap);
+      if (u < 0 || !D.alive[u]) continue;
+      if (blocked(D, A, t, i)) continue;
+      int slot = wh_claim(W, u);
+      if (slot == -1) continue;
+      if (slot == -2) { W.flag = 1; continue; }
+      if (in_region(D, u, p, A)) {
+        int idx = atomicAdd(&W.n, 1);
+        if (idx >= WR_MAXT) { W.flag = 1; W.hval[slot] = -2; continue; }
+        W.cav[idx] = u;
+        W.hval[slot] = idx;
+        nxt[atomicAdd(&W.nf, 1)] = u;
+      } else {
+        W.hval[slot] = -2;
+      }
+    }
+    __syncwarp();
+    WMARK(50);
+    if (W.flag) return RS_OVERFLOW;
+    ncur = W.nf;
+    int* tmp = cur; cur = nxt; nxt = tmp;
+    __syncwarp();
+  }
+  const int n = W.n;
+  WSTOP(2);
+  WMARK(12);
+  // ---- peel / seed component (confluent fixpoint)
+  for (int k = lane; k < n; k += 32) W.in[k] = 1;
+  __syncwarp();
+  while (true) {
+    while (true) {
+      WMARK(20);
+      bool changed = false;
+      for (int k = lane; k < n; k += 32) {
+        if (!W.in[k]) continue;
+        int t = W.cav[k];
+        DCHK(t >= 0 && t < D.tcap);
+        int4 q = D.tv[t];
+        for (int i = 0; i < 4; ++i) {
+          int u = tnk(D, t, i) >> 2;
+          bool blk = blocked(D, A, t, i);
+          int ku = wh_find(W, u);
+          DCHK(ku < WR_MAXT);
+          bool uin = ku >= 0 && W.in[ku];
+          if (uin && !blk) continue;
+          int f[3]; face_verts(q, i, f);
+          if (f[0] == GHOST || f[1] == GHOST || f[2] == GHOST) continue;
+          if (orient3d(PT(D, f[0]), PT(D, f[1]), PT(D, f[2]), p) >= 0) { W.in[k] = 0; changed = true; break; }
+        }
+      }
+      __syncwarp();
+      if (!__any_sync(FULL, changed)) break;
+    }
+    WMARK(50);
+    const bool shrunk = !W.in[0];
+    __syncwarp();
+    if (shrunk) return RS_CNSS;          // seed shrunk away
+    for (int k = lane; k < n; k += 32) W.comp[k] = 0;
+    __syncwarp();
+    if (lane == 0) { W.comp[0] = 1; W.f0[0] = 0; W.cnt = 1; }
+    __syncwarp();
+    WMARK(21);
+    int* fa = W.f0; int* fb = W.f1;
+    int nfa = 1;
+    while (nfa > 0) {
+      if (lane == 0) W.nf = 0;
+      __syncwarp();
+      for (int j = lane; j < 4 * nfa; j += 32) {
+        int k = fa[j >> 2], i = j & 3;
+        int t = W.cav[k];
+        int u = tnk(D, t, i) >> 2;
+        int ku = wh_find(W, u);
+        if (ku < 0 || !W.in[ku]) continue;
+        if (blocked(D, A, t, i)) continue;
+        if (atomicCAS(&W.comp[ku], 0, 1) != 0) continue;
+        atomicAdd(&W.cnt, 1);
+        fb[atomicAdd(&W.nf, 1)] = ku;
+      }
+      __syncwarp();
+      nfa = W.nf;
+      int* tmp = fa; fa = fb; fb = tmp;
+      __syncwarp();
+    }
+    int live = 0;
+    for (int k = lane; k < n; k += 32) live += W.in[k];
+    for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(FULL, live, o);
+    const bool done = W.cnt == live;
+    __syncwarp();                 // every lane has read W.cnt before anyone moves on
+    if (done) break;
+    for (int k = lane; k < n; k += 32) W.in[k] = (unsigned char)W.comp[k];
+    __syncwarp();
+  }
+  WSTOP(3);
+  WMARK(13);
+  // ---- finish: members, sorted by tet id (warp bitonic over 128 slots)
+  if (lane == 0) W.cnt = 0;
+  __syncwarp();
+  for (int k = lane; k < n; k += 32) if (W.in[k]) W.f0[atomicAdd(&W.cnt, 1)] = W.cav[k];
+  __syncwarp();
+  const int m = W.cnt;
+  DCHK(m >= 1 && m <= n);
+  WMARK(50);
+  if (m > O.ctet) return RS_OVERFLOW;
+  int P2 = 32;
+  while (P2 < m) P2 <<= 1;
+  for (int k = m + lane; k < P2; k += 32) W.f0[k] = INT_MAX;
+  __syncwarp();
+  for (int size = 2; size <= P2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int k = lane; k < P2; k += 32) {
+        int l = k ^ stride;
+        if (l > k) {
+          int a = W.f0[k], b = W.f0[l];
+          bool up = (k & size) == 0;
+          if ((a > b) == up) { W.f0[k] = b; W.f0[l] = a; }
+        }
+      }
+      __syncwarp();
+    }
+  WSTOP(4);
+  WMARK(14);
+  // boundary faces per tet (consecutive chunks per lane keep the order)
+  const int per = (m + 31) >> 5;
+  const int lo = lane * per, hi = min(lo + per, m);
+  int mycnt = 0;
+  for (int a = lo; a < hi; ++a) {
+    int t = W.f0[a];
+    O.tets[a] = t;
+    for (int i = 0; i < 4; ++i) {
+      int u = tnk(D, t, i) >> 2;
+      bool blk = blocked(D, A, t, i);
+      int ku = wh_find(W, u);
+      bool uin = ku >= 0 && W.in[ku];
+      if (uin && !blk) continue;
+      if (uin && blk) { atomicMin(&W.memb, 4 * a + i); continue; }
+      ++mycnt;
+    }
+  }
+  __syncwarp();
+  DCHK(W.memb == INT_MAX || (W.memb >> 2) < m);
+  if (W.memb != INT_MAX) { O.memb = 4 * O.tets[W.memb >> 2] + (W.memb & 3); return RS_MEMBRANE; }
+  int incl = mycnt;
+  for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(FULL, incl, o); if (lane >= o) incl += v; }
+  const int nbf = __shfl_sync(FULL, incl, 31);
+  WMARK(50);
+  if (nbf > O.cbf) return RS_OVERFLOW;
+  int off = incl - mycnt;
+  for (int a = lo; a < hi; ++a) {
+    int t = W.f0[a];
+    for (int i = 0; i < 4; ++i) {
+      int u = tnk(D, t, i) >> 2;
+      bool blk = blocked(D, A, t, i);
+      int ku = wh_find(W, u);
+      bool uin = ku >= 0 && W.in[ku];
+      if (uin && !blk) continue;
+      O.bf[off++] = 4 * t + i;
+    }
+  }
+  __syncwarp();
+  WSTOP(5);
+  WMARK(15);
+  // boundary vertices: min distance and the swallow check (hash reused)
+  for (int i = lane; i < WR_HASH; i += 32) W.hkey[i] = INT_MIN;
+  if (lane == 0) W.flag = 0;
+  __syncwarp();
+  double mymin = __longlong_as_double(0x7ff0000000000000ll);
+  for (int k = lane; k < nbf; k += 32) {
+    int t = O.bf[k] >> 2, i = O.bf[k] & 3;
+    DCHK(t >= 0 && t < D.tcap);
+    int f[3]; face_verts(D.tv[t], i, f);
+    for (int j = 0; j < 3; ++j) {
+      if (f[j] == GHOST) continue;
+      DCHK(f[j] >= 0 && f[j] < D.vcap);
+      int s = wh_claim(W, f[j]);
+      if (s == -2) { W.flag = 1; continue; }
+      if (s < 0) continue;
+      W.hval[s] = 0;
+      const double* qv = PT(D, f[j]);
+      double d = (qv[0] - p[0]) * (qv[0] - p[0]) + (qv[1] - p[1]) * (qv[1] - p[1]) + (qv[2] - p[2]) * (qv[2] - p[2]);
+      if (d < mymin) mymin = d;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) { double v = __shfl_xor_sync(FULL, mymin, o); if (v < mymin) mymin = v; }
+  __syncwarp();
+  WMARK(50);
+  if (W.flag) return RS_OVERFLOW;
+  bool swallow = false;
+  for (int a = lane; a < m; a += 32) {
+    int4 q = D.tv[W.f0[a]];
+    for (int k = 0; k < 4; ++k) {
+      int v = tvk(q, k);
+      if (v != GHOST && wh_find(W, v) == -1) swallow = true;
+    }
+  }
+  WMARK(50);
+  if (__any_sync(FULL, swallow)) return RS_CNSS;
+  WSTOP(6);
+  WMARK(16);
+  O.ntet = m; O.nbf = nbf; O.mind = mymin;
+  O.ncr = 0; O.nbsub = 0; O.nbseg = 0; O.neseg = 0;
+  // ---- constraint classification (first-met order): lane 0, serial
+  bool cons = false;
+  for (int a = lane; a < m; a += 32) if (D.sub[W.f0[a]] || D.seg[W.f0[a]]) cons = true;
+  WMARK(50);
+  if (!__any_sync(FULL, cons)) return RS_OK;
+  WSTOP(7);
+  int st = RS_OK;
+  if (lane == 0) {
+    S.fset.clear();
+    const unsigned long long TE = 2ull << 60, TSF = 3ull << 60, TSG = 4ull << 60;
+    auto member = [&](int u) {   // binary search in the sorted cavity
+      int l = 0, h = m - 1;
+      while (l <= h) { int mid = (l + h) >> 1; int v = W.f0[mid]; if (v == u) return true; if (v < u) l = mid + 1; else h = mid - 1; }
+      return false;
+    };
+    for (int a = 0; a < m && st == RS_OK; ++a) {
+      int t = W.f0[a];
+      int4 q = D.tv[t];
+      for (int i = 0; i < 4; ++i) {
+        int u = tnk(D, t, i) >> 2;
+        bool blk = blocked(D, A, t, i);
+        if (member(u) && !blk) continue;
+        int f[3]; face_verts(q, i, f);
+        for (int k = 0; k < 3; ++k) {
+          int x = f[k], y = f[(k + 1) % 3];
+          if (x == GHOST || y == GHOST) continue;
+          if (x > y) { int tt = x; x = y; y = tt; }
+          if (S.fset.add(TE | ((unsigned long long)x << 30) | (unsigned long long)y) < 0) st = RS_OVERFLOW;
+        }
+      }
+      int sm = D.sub[t];
+      for (int i = 0; sm && i < 4 && st == RS_OK; ++i) {
+        if (!(sm & (1 << i))) continue;
+        int f[3]; face_verts(q, i, f);
+        int a0 = f[0], b0 = f[1], c0 = f[2];
+        sort3(a0, b0, c0);
+        int ins = S.fset.add(TSF | (key3(a0, b0, c0) & ((1ull << 60) - 1)));
+        if (ins < 0) { st = RS_OVERFLOW; break; }
+        if (ins == 0) continue;
+        bool uin = member(tnk(D, t, i) >> 2);
+        int rec = face_lookup(D, a0, b0, c0);
+        DCHK(rec < D.sfcap);
+        bool crossed = uin && rec >= 0 && A.n > 0 && allowed_face(D, A, a0, b0, c0);
+        DCHK(O.ncr >= 0 && O.nbsub >= 0 && O.ccon == CC_DBG);
+        if (crossed) {
+          if (O.ncr >= O.ccon) { st = RS_OVERFLOW; break; }
+          O.cr[O.ncr] = rec; O.crf[O.ncr] = min(4 * t + i, tnk(D, t, i)); O.ncr++;
+        } else {
+          if (O.nbsub >= O.ccon) { st = RS_OVERFLOW; break; }
+          O.bsub[O.nbsub++] = rec;
+        }
+      }
+      int em = D.seg[t];
+      for (int i = 0; em && i < 6 && st == RS_OK; ++i) {
+        if (!(em & (1 << i))) continue;
+        int x = tvk(q, c_edges[i][0]), y = tvk(q, c_edges[i][1]);
+        if (x > y) { int tt = x; x = y; y = tt; }
+        int ins = S.fset.add(TSG | ((unsigned long long)x << 30) | (unsigned long long)y);
+        if (ins < 0) { st = RS_OVERFLOW; break; }
+        if (ins == 0) continue;
+        int rec = seg_lookup(D, x, y);
+        bool bound = S.fset.has(TE | ((unsigned long long)x << 30) | (unsigned long long)y);
+        if (O.nbseg + O.neseg >= O.ccon) { st = RS_OVERFLOW; break; }
+        if (bound) O.bseg[O.nbseg++] = rec; else O.eseg[O.neseg++] = rec;
+      }
+    }
+  }
+  st = __shfl_sync(FULL, st, 0);
+  O.ncr = __shfl_sync(FULL, O.ncr, 0); O.nbsub = __shfl_sync(FULL, O.nbsub, 0);
+  O.nbseg = __shfl_sync(FULL, O.nbseg, 0); O.neseg = __shfl_sync(FULL, O.neseg, 0);
+  WMARK(60);
+  return st;
+}
+
+}  // namespace gq
