@@ -616,6 +616,19 @@ __device__ inline void grid_encroached(const Dev& D, const CGrid& g, const doubl
   int nb = *g.nbig;
   for (int b = 0; b < nb; ++b) test(g.big[b]);
 }
+__global__ void k_big_live(Dev D, CGrid g, int n, int* flags) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) {
+    int code = g.big[b], kind = code & 1, r = code >> 1;
+    flags[b] = kind == 0 ? (D.sg_fl[r] & RF_LIVE) != 0 : (D.sf_fl[r] & RF_LIVE) != 0;
+  }
+}
+__global__ void k_big_gather(CGrid g, const int* pos, int n, int* out) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) out[b] = g.big[pos[b]];
+}
+__global__ void k_big_set(CGrid g, const int* src, int n) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) g.big[b] = src[b];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *g.nbig = n;
+}
 // post_round part 1 (refine.py:818-828): new vertices against all balls
 __global__ void k_grid_newverts(Dev D, CGrid g, int v0, int v1) {
   for (int v = v0 + blockIdx.x * blockDim.x + threadIdx.x; v < v1; v += gridDim.x * blockDim.x) {
@@ -928,6 +941,51 @@ __global__ void k_star(Dev D, Cand C, Ins I) {
     star_insert(D, C.vid[c], v.bf, C.nbf[c], C.nt0[c], true);
   }
 }
+// warp per inserted cavity (serial star for oversized boundaries)
+// global-memory pairing hash for stars of oversized cavities: the big
+// scratch arena of warp gw % SB.nthreads (keys: fkey, partners: tkey/tval)
+__device__ inline StarHash big_star_hash(const Scr& SB, int gw, int* flag) {
+  int slot = gw % SB.nthreads;
+  StarHash h;
+  h.key = SB.fkey + (size_t)slot * SB.fcap;
+  h.v0 = SB.tkey + (size_t)slot * SB.tcap;
+  h.v1 = SB.tval + (size_t)slot * SB.tcap;
+  h.cap = SB.tcap < SB.fcap ? SB.tcap : SB.fcap;
+  h.flag = flag;
+  return h;
+}
+__global__ void __launch_bounds__(32 * WS_WARPS) k_star_warp(Dev D, Cand C, Ins I, Scr SB) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  StarShared& X = reinterpret_cast<StarShared*>(smem_raw)[wib];
+  const int gw = blockIdx.x * WS_WARPS + wib, nw = gridDim.x * WS_WARPS;
+  for (int k = gw; k < I.n; k += nw) {
+    int c = I.list[k];
+    SlabView v = slab(C, c);
+    int nbf = C.nbf[c];
+    if (nbf <= WS_MAXF) star_warp(D, C.vid[c], v.bf, nbf, C.nt0[c], true, star_hash_shared(X), nullptr, 0);
+    else star_warp(D, C.vid[c], v.bf, nbf, C.nt0[c], true, big_star_hash(SB, gw, &X.flag), nullptr, 0);
+    __syncwarp();
+  }
+}
+__global__ void __launch_bounds__(32 * WS_WARPS) k_init_stars_warp(Dev D, Cand C, const int* pend, const int* plist,
+                                                                   const int* acc, int nw_, int* touched, int round, Scr SB) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  StarShared& X = reinterpret_cast<StarShared*>(smem_raw)[wib];
+  const int gw = blockIdx.x * WS_WARPS + wib, nw = gridDim.x * WS_WARPS;
+  for (int w = gw; w < nw_; w += nw) {
+    if (!acc[w]) continue;
+    int c = plist[w];
+    SlabView v = slab(C, c);
+    int nbf = C.nbf[c];
+    if (nbf <= WS_MAXF) star_warp(D, pend[c], v.bf, nbf, C.nt0[c], true, star_hash_shared(X), touched, round);
+    else star_warp(D, pend[c], v.bf, nbf, C.nt0[c], true, big_star_hash(SB, gw, &X.flag), touched, round);
+    __syncwarp();
+    if (lane == 0) C.status[c] = CS_DROP;
+  }
+}
+
 // dirty constraints + survivor mask refresh for subfaces retiled in 2D but
 // not crossed by the 3D cavity (refine.py:720-736)
 __global__ void k_post_insert(Dev D, Cand C, Ins I, T2Items T, Scr SC, const int* item_of) {
@@ -1694,6 +1752,7 @@ struct gq_ctx {
   int reg_seg = 0, reg_face = 0, reg_nv = 0;
   int big_used = 0;
   int init_rounds = 0;
+  long long grid_calls = 0;
   int4 *tv2 = nullptr, *tn2 = nullptr; uint8_t *sub2 = nullptr, *seg2 = nullptr, *skip2 = nullptr; double* ratio2 = nullptr;
   struct QBuf { int *a, *b, *c, *d, *e, *f, *g, *h; size_t cap; } Q{};
   bool allocated = false;
@@ -1703,10 +1762,11 @@ static double now_s() { return std::chrono::duration<double>(std::chrono::steady
 static double g_prof[8];
 // fine stage timers (GQ_PROFILE=2): synchronise and charge the elapsed time
 static bool g_fine = false;
-static double g_fine_t[24];
-static const char* g_fine_names[24] = {"i.region", "i.big", "i.filter", "i.scan", "i.kill", "i.stars", "i.compact",
+static double g_fine_t[32];
+static const char* g_fine_names[32] = {"i.region", "i.big", "i.filter", "i.scan", "i.kill", "i.stars", "i.compact",
   "p.gridsync", "p.newverts", "p.check", "p.compact", "r.sorted", "r.make", "r.redirect", "r.append", "f.states",
-  "f.rank", "f.lfmis", "x.acc", "x.ids", "x.star", "x.postins", "i.misc", "r.misc"};
+  "f.rank", "f.lfmis", "x.acc", "x.ids", "x.star", "x.postins", "i.misc", "r.misc", "g.warp", "g.ovfscan", "g.block",
+  "r.setup", "r.gridc", "r.kept", "x.fallback", "r.misc2"};
 static double g_fine_last = 0;
 static void fine(gq_ctx* c, int k);
 static void sync(gq_ctx* c) {
@@ -1872,7 +1932,7 @@ static unsigned int pow2_at_least(size_t n) { unsigned int p = 1024; while (p < 
 
 static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   Dev& D = c->D;
-  size_t vcap = std::max<size_t>(65536, (size_t)n * 24);
+  size_t vcap = 65536 + (size_t)n * 8;
   size_t tcap = std::max<size_t>(1 << 21, (size_t)n * 64);
   D.vcap = (int)vcap; D.tcap = (int)tcap;
   D.P = dmalloc<double>(3 * vcap); D.vorigin = dmalloc<uint8_t>(vcap); D.vert_tet = dmalloc<int>(vcap);
@@ -1882,19 +1942,19 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   D.ratio = dmalloc<double>(tcap);
   CK(cudaMemset(D.alive, 0, tcap));
   if (getenv("GQ_PROFILE")) std::fprintf(stderr, "[gq] capacities: verts %zu tets %zu\n", vcap, tcap);
-  size_t sgcap = std::max<size_t>(4096, (size_t)m * 64 + vcap);
+  size_t sgcap = 65536 + (size_t)m * 32 + vcap / 8;
   D.sgcap = (int)sgcap;
   D.sg_uv = dmalloc<int2>(sgcap); D.sg_sid = dmalloc<int>(sgcap); D.sg_fl = dmalloc<unsigned int>(sgcap);
   unsigned int sgh = pow2_at_least(2 * sgcap);
   D.sg_hk = dmalloc<unsigned long long>(sgh); D.sg_hv = dmalloc<int>(sgh); D.sg_hmask = sgh - 1;
   CK(cudaMemset(D.sg_hk, 0xff, (size_t)sgh * 8));
-  size_t sfcap = std::max<size_t>(8192, (size_t)f * 64 + 4 * vcap);
+  size_t sfcap = 65536 + (size_t)npidx * 32 + vcap;
   D.sfcap = (int)sfcap;
   D.sf_v = dmalloc<int4>(sfcap); D.sf_fl = dmalloc<unsigned int>(sfcap);
   unsigned int sfh = pow2_at_least(2 * sfcap);
   D.sf_hk = dmalloc<unsigned long long>(sfh); D.sf_hv = dmalloc<int>(sfh); D.sf_hmask = sfh - 1;
   CK(cudaMemset(D.sf_hk, 0xff, (size_t)sfh * 8));
-  size_t t2cap = std::max<size_t>(8192, (size_t)npidx * 8 + 16 * vcap);
+  size_t t2cap = 65536 + (size_t)npidx * 8 + 2 * vcap;
   D.t2cap = (int)t2cap;
   D.t2v = dmalloc<int4>(t2cap); D.t2alive = dmalloc<uint8_t>(t2cap);
   CK(cudaMemset(D.t2alive, 0, t2cap));
@@ -1925,7 +1985,7 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   c->L.cap = 1 << 20; c->L.rows = dmalloc<int>((size_t)8 * c->L.cap);
   c->d_int = dmalloc<int>(64);
   alloc_scratch(c->S, 16384, CT * 2, 1024, 2048);
-  alloc_scratch(c->SB, 512, CTB * 2, 16384, 32768);
+  alloc_scratch(c->SB, 512, CTB * 2, 32768, 32768);
   alloc_cands(c, 1 << 16, 256);
   {
     int g = (int)std::cbrt(std::max(1.0, n / 2.0));
@@ -1975,6 +2035,7 @@ static void time_region(gq_ctx* c) {
 }
 static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   if (n1 <= n0) return;
+  fine(c, 31);
   CK(cudaEventRecord(c->er0, c->st));
   if (!getenv("GQ_THREAD_REGIONS")) {   // debug switch: per-thread kernel
     long long nw = n1 - n0;
@@ -1987,6 +2048,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   }
   CK(cudaEventRecord(c->er1, c->st));
   time_region(c);
+  fine(c, 24);
   // overflow pass
   ensure_tmp(c, n1 + 1);
   std::vector<int> hs(n1 - n0);
@@ -1994,6 +2056,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   sync(c);
   std::vector<int> big;
   for (int k = 0; k < n1 - n0; ++k) if (hs[k] == CS_OVF) big.push_back(n0 + k);
+  fine(c, 25);
   if (!big.empty()) {
     int nb = (int)big.size();
     ensure_big(c, c->big_used + nb);
@@ -2004,6 +2067,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
     c->big_used += nb;
     sync(c);
   }
+  fine(c, 26);
 }
 
 // candidates sorted by priority (class rank, hash); smaller first
@@ -2035,6 +2099,7 @@ static void rank_candidates(gq_ctx* c, int n) {
 
 // LFMIS filter over candidates [0,n): state 0 for ok ones, 3 for the rest.
 static void run_filter(gq_ctx* c, int n, int* nacc_out) {
+  // iterations are idempotent once nothing is undecided: check every 3rd
   for (int it = 0;; ++it) {
     CK(cudaMemsetAsync(c->d_int, 0, 4, c->st));
     LAUNCH(k_claim, n, c->D, c->C, c->W, n);
@@ -2042,6 +2107,7 @@ static void run_filter(gq_ctx* c, int n, int* nacc_out) {
     LAUNCH(k_mark, n, c->D, c->C, c->W, n, it);
     LAUNCH(k_reject, n, c->D, c->C, c->W, n, c->d_int);
     LAUNCH(k_reset_claims, n, c->D, c->C, c->W, n, 0);
+    if (it % 3 != 2) continue;
     int und = read_int(c, c->d_int);
     if (und == 0) break;
     if (it > 100000) throw std::runtime_error("filter did not converge");
@@ -2092,6 +2158,17 @@ static int sorted_records(gq_ctx* c, int phase, unsigned int need, unsigned int 
 // register records created since the last call (ConstraintIndex.add_*)
 static void grid_sync(gq_ctx* c) {
   pull(c);
+  // drop dead entries from the big-ball list (scanned by every query)
+  if (++c->grid_calls % 4 == 0) {
+    int nb = read_int(c, c->G.nbig);
+    if (nb > 256) {
+      ensure_tmp(c, nb + 1);
+      LAUNCH(k_big_live, nb, c->D, c->G, nb, c->tmpB);
+      int live = select_flagged(c, c->tmpB, nb, c->tmpA);
+      LAUNCH(k_big_gather, std::max(live, 1), c->G, c->tmpA, live, c->tmpB);
+      LAUNCH(k_big_set, std::max(live, 1), c->G, c->tmpB, live);
+    }
+  }
   if (c->hc.nsegrec > c->reg_seg) { LAUNCH(k_grid_register, c->hc.nsegrec - c->reg_seg, c->D, c->G, 0, c->reg_seg, c->hc.nsegrec); c->reg_seg = c->hc.nsegrec; }
   if (c->hc.nfacerec > c->reg_face) { LAUNCH(k_grid_register, c->hc.nfacerec - c->reg_face, c->D, c->G, 1, c->reg_face, c->hc.nfacerec); c->reg_face = c->hc.nfacerec; }
 }
@@ -2271,7 +2348,12 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     fine(c, 3);
     LAUNCH(k_init_kill, W, c->D, C, d_plist, d_acc, d_scan, W, nt, d_succ);
     fine(c, 4);
-    LAUNCH(k_init_stars, W, c->D, C, d_pend, d_plist, d_acc, W, d_touched, round);
+    {
+      int blocks = std::max(1, std::min((W + WS_WARPS - 1) / WS_WARPS, c->SB.nthreads / WS_WARPS));
+      k_init_stars_warp<<<blocks, 32 * WS_WARPS, WS_WARPS * sizeof(StarShared), c->st>>>(c->D, C, d_pend, d_plist, d_acc, W, d_touched, round, c->SB);
+      c->launches++;
+      CK(cudaGetLastError());
+    }
     fine(c, 5);
     nt += add_t;
     // release big slabs (big regions are recomputed next round if still pending)
@@ -2382,6 +2464,7 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
   if (nt + tot > c->D.tcap || nv + ni > c->D.vcap) throw std::runtime_error("mesh capacity exceeded");
   LAUNCH(k_assign_ids, ni, C, ins, ni, pos, nv, nt);
   Ins I; I.list = ins; I.n = ni; I.nv0 = nv; I.nt0base = nt;
+  fine(c, 18);
   LAUNCH(k_ins_vertices, ni, c->D, C, I);
   // facet 2D retiling work items (candidate, polygon) in priority order
   int* item_of = nullptr;
@@ -2413,11 +2496,19 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
   }
   g_prof[4] += now_s() - t1;
   t1 = now_s();
+  fine(c, 19);
   LAUNCH(k_ins_segsplit, ni, c->D, C, I);
   LAUNCH(k_kill_cavities, ni, c->D, C, I);
-  LAUNCH(k_star, ni, c->D, C, I);
+  {
+    int blocks = std::max(1, std::min((ni + WS_WARPS - 1) / WS_WARPS, c->SB.nthreads / WS_WARPS));
+    k_star_warp<<<blocks, 32 * WS_WARPS, WS_WARPS * sizeof(StarShared), c->st>>>(c->D, C, I, c->SB);
+    c->launches++;
+    CK(cudaGetLastError());
+  }
   LAUNCH(k_bump, 1, c->D, ni, tot);
+  fine(c, 20);
   LAUNCH_S(k_post_insert, ni, c->D, C, I, c->T, c->S, (const int*)item_of);
+  fine(c, 21);
   g_prof[3] += now_s() - t1;
 }
 
@@ -2495,18 +2586,24 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
       LAUNCH(k_set_cands, nb, c->C, 0, nb, K_TET, c->Q.g, 0);
       nbase = nb;
     }
+    fine(c, 27);
     LAUNCH_S(k_make_cands, nbase, c->D, c->C, c->S, 0, nbase, X, c->L, lmin2);
+    fine(c, 12);
     double t1 = now_s();
     // redirects first (refine.py:603-662): dropped candidates need no region
     grid_sync(c);
     LAUNCH(k_grid_cands, nbase, c->D, c->G, c->C, 0, nbase);
+    fine(c, 28);
     LAUNCH(k_redirect, nbase, c->D, c->C, 0, nbase);
+    fine(c, 13);
     ensure_tmp(c, nbase + 1);
     LAUNCH(k_kept, nbase, c->C, nbase, c->Q.a);
     int kept = scan_total(c, c->Q.a, c->Q.b, nbase);
     LAUNCH(k_pool_pos, nbase, c->C, nbase, c->Q.b, c->Q.a);
+    fine(c, 29);
     int nrs = append_redirects(c, 0, nbase, kept, X);
     int nrf = phase == 2 ? append_redirects(c, 1, nbase + nrs, kept + nrs, X) : 0;
+    fine(c, 14);
     R.ncand = kept + nrs + nrf;
     g_prof[0] += now_s() - t0;
     t1 = now_s();
@@ -2533,6 +2630,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   insert_accepted(c, n, &R.acc, &R.inserted, round_no);
   R.rej = nok - R.acc;
   t1 = now_s();
+  fine(c, -1);
   if (nfail > 0) {
     FallbackIO F; F.list = c->Q.h; F.n = nfail; F.round_no = round_no; F.seed = c->seed;
     F.with_facets = c->npoly > 0; F.lmin2 = lmin2; F.inserted = c->d_int + 20;
@@ -2542,6 +2640,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     CK(cudaGetLastError());
     R.inserted += read_int(c, c->d_int + 20);
   }
+  fine(c, 30);
   g_prof[5] += now_s() - t1;
   t1 = now_s();
   // post round: new vertices vs every constraint ball, then new / dirty
@@ -2589,7 +2688,10 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   CK(cudaMemcpyToSymbol(g_region_calls, &z1, 8));
   CK(cudaMemcpyToSymbol(g_tested, &z1, 8));
   int npidx = f > 0 ? poff[f] : 0;
+  double ta = now_s();
   alloc_mesh(c, n, m, f, npidx);
+  CK(cudaDeviceSynchronize());
+  if (getenv("GQ_PROFILE")) std::fprintf(stderr, "[gq] alloc %.1f ms\n", 1000 * (now_s() - ta));
   c->d_order = dmalloc<int>(n);
   Dev& D = c->D;
   // bbox / lmin (mesh.py:883-885, refine.py:532)
@@ -2706,7 +2808,7 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   float ms = 0; cudaEventElapsedTime(&ms, c->ev0, c->ev1); c->dev_ms = ms;
   if (g_fine) {
     std::fprintf(stderr, "[gq fine]");
-    for (int k = 0; k < 24; ++k) if (g_fine_t[k] > 0) { std::fprintf(stderr, " %s %.1f;", g_fine_names[k], 1000 * g_fine_t[k]); g_fine_t[k] = 0; }
+    for (int k = 0; k < 32; ++k) if (g_fine_t[k] > 0) { std::fprintf(stderr, " %s %.1f;", g_fine_names[k], 1000 * g_fine_t[k]); g_fine_t[k] = 0; }
     std::fprintf(stderr, "\n");
   }
   if (getenv("GQ_PROFILE")) {
@@ -2769,6 +2871,8 @@ int gq_create(int device, gq_ctx** out) {
     CK(cudaDeviceSetLimit(cudaLimitStackSize, 16384));
     CK(cudaFuncSetAttribute(k_region_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BlockShared)));
     CK(cudaFuncSetAttribute(k_region_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared))));
+    CK(cudaFuncSetAttribute(k_star_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WS_WARPS * sizeof(StarShared))));
+    CK(cudaFuncSetAttribute(k_init_stars_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WS_WARPS * sizeof(StarShared))));
     CK(cudaFuncSetAttribute(k_init_region_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared))));
     CK(cudaFuncSetAttribute(k_init_region_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BlockShared)));
   } catch (std::exception& e) {

@@ -396,3 +396,129 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
 }
 
 }  // namespace gq
+
+namespace gq {
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative Bowyer-Watson star (mesh.py:736-771, _kernels.py:641-807):
+// lane-parallel tet creation and outer wiring; the inner faces (those through
+// the new vertex) are paired through a per-warp shared hash keyed by the edge
+// of the boundary face they stand on (phase A inserts both sides, phase B
+// reads the partner).  Same tets, ids and adjacency as star_insert().
+#define WS_MAXF 272
+#define WS_HASH 1024
+#define WS_WARPS 4
+struct StarShared {
+  unsigned long long key[WS_HASH];
+  int v0[WS_HASH];
+  int v1[WS_HASH];
+  int flag;
+};
+struct StarHash {            // view on shared (normal) or global (big cavities) storage
+  unsigned long long* key;
+  int* v0;
+  int* v1;
+  int cap;                   // power of two
+  int* flag;
+};
+
+__device__ __forceinline__ int star_slot(const StarHash& X, unsigned long long key, bool insert) {
+  unsigned int h = (unsigned int)mix64(key) & (X.cap - 1);
+  for (int pr = 0; pr < X.cap; ++pr) {
+    unsigned long long cur = X.key[h];
+    if (cur == key) return (int)h;
+    if (cur == EMPTY_KEY) {
+      if (!insert) return -1;
+      unsigned long long old = atomicCAS(&X.key[h], EMPTY_KEY, key);
+      if (old == EMPTY_KEY || old == key) return (int)h;
+    }
+    h = (h + 1) & (X.cap - 1);
+  }
+  return -1;
+}
+__device__ __forceinline__ unsigned long long inner_key(const int* g, int vid) {
+  int x = g[0] == vid ? g[1] : g[0];
+  int y = g[2] == vid ? g[1] : g[2];
+  if (x > y) { int tt = x; x = y; y = tt; }
+  return ((unsigned long long)(unsigned int)(x + 1) << 32) | (unsigned int)(y + 1);
+}
+
+__device__ __forceinline__ StarHash star_hash_shared(StarShared& S) {
+  StarHash h; h.key = S.key; h.v0 = S.v0; h.v1 = S.v1; h.cap = WS_HASH; h.flag = &S.flag; return h;
+}
+__device__ inline bool star_warp(const Dev& D, int vid, const int* bf, int nbf, int nt0, bool max_vt,
+                                 const StarHash& X, int* touched, int stamp) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < X.cap; i += 32) { X.key[i] = EMPTY_KEY; X.v0[i] = -1; X.v1[i] = -1; }
+  if (lane == 0) *X.flag = 0;
+  __syncwarp();
+  // phase A: new tets, outer links, inner faces into the hash
+  for (int k = lane; k < nbf; k += 32) {
+    int t = bf[k] >> 2, i = bf[k] & 3;
+    int packed = tnk(D, t, i);
+    int u = packed >> 2, j = packed & 3;
+    if (touched) touched[u] = stamp;
+    int f[3]; face_verts(D.tv[u], j, f);
+    int nt = nt0 + k;
+    int4 q;
+    if (f[0] == GHOST || f[1] == GHOST || f[2] == GHOST) {
+      int e0, e1;
+      if (f[0] == GHOST) { e0 = f[1]; e1 = f[2]; }
+      else if (f[1] == GHOST) { e0 = f[2]; e1 = f[0]; }
+      else { e0 = f[0]; e1 = f[1]; }
+      q = make_int4(e1, e0, vid, GHOST);
+    } else {
+      q = make_int4(f[0], f[1], f[2], vid);
+    }
+    D.tv[nt] = q;
+    D.alive[nt] = 1; D.skip[nt] = 0;
+    int a0 = f[0], b0 = f[1], c0 = f[2];
+    sort3(a0, b0, c0);
+    int om = -1;
+    for (int m = 0; m < 4; ++m) {
+      int g[3]; face_verts(q, m, g);
+      int x = g[0], y = g[1], z = g[2];
+      sort3(x, y, z);
+      if (om < 0 && x == a0 && y == b0 && z == c0) { om = m; continue; }
+      int h = star_slot(X, inner_key(g, vid), true);
+      if (h < 0) { *X.flag = 1; continue; }
+      int mine = 4 * nt + m;
+      if (atomicCAS(&X.v0[h], -1, mine) != -1 && atomicCAS(&X.v1[h], -1, mine) != -1) *X.flag = 1;
+    }
+    if (om < 0) { *X.flag = 1; continue; }
+    set_tn(D, nt, om, 4 * u + j);
+    set_tn(D, u, j, 4 * nt + om);
+    for (int m = 0; m < 4; ++m) {
+      int v = tvk(q, m);
+      if (v == GHOST || v == vid) continue;
+      if (max_vt) atomicMax(D.vert_tet + v, nt); else D.vert_tet[v] = nt;
+    }
+  }
+  __syncwarp();
+  if (*X.flag) { if (lane == 0) raise_err(GQ_ERR_STAR); return false; }
+  // phase B: inner links from the partner entries
+  for (int k = lane; k < nbf; k += 32) {
+    int nt = nt0 + k;
+    int4 q = D.tv[nt];
+    for (int m = 0; m < 4; ++m) {
+      int g[3]; face_verts(q, m, g);
+      if (g[0] != vid && g[1] != vid && g[2] != vid) continue;   // outer face
+      int h = star_slot(X, inner_key(g, vid), false);
+      int mine = 4 * nt + m;
+      int other = h < 0 ? -1 : (X.v0[h] == mine ? X.v1[h] : X.v0[h]);
+      if (other < 0) { *X.flag = 1; continue; }
+      set_tn(D, nt, m, other);
+    }
+  }
+  __syncwarp();
+  if (*X.flag) { if (lane == 0) raise_err(GQ_ERR_STAR); return false; }
+  for (int k = lane; k < nbf; k += 32) {
+    refresh_masks(D, nt0 + k);
+    star_ratio(D, nt0 + k);
+  }
+  __syncwarp();
+  if (lane == 0) D.vert_tet[vid] = nt0;
+  return true;
+}
+
+}  // namespace gq
