@@ -1,7 +1,14 @@
-"""GPU parity: the CUDA path (through the C ABI) against the reference's
-golden outputs and the CPU oracle.  Needs a B200 (pytest -m gpu)."""
+"""GPU parity: the CUDA path, called through the C ABI, against the
+reference's golden outputs (tests/golden/, generated from /root/reference)
+and the CPU oracle.  Needs a B200: pytest -m gpu.
 
-import json
+Bar (BASELINE north_star): predicate signs bit-exact; output a conforming
+mesh (audit: orientation, symmetric adjacency, masks, every subsegment an
+edge and every subface a face); Steiner and residual bad-tet counts within
+2% of the reference; coordinates within 1e-12 relative.  In practice every
+case below is bit-identical (same points, same ordered tets).
+"""
+
 import os
 
 import numpy as np
@@ -31,36 +38,102 @@ def test_predicates_bit_exact(gq, golden_dir):
     cs = gq.batch("circumsphere_tet", g["o3d_in"][: len(g["out_csph"])])
     m = ~np.isnan(g["out_csph"])
     assert np.array_equal(np.isnan(cs), ~m)
-    assert np.array_equal(cs[m], g["out_csph"][m])
+    assert np.array_equal(cs[m], g["out_csph"][m])            # constructions bit-identical
     cc = gq.batch("circumcircle_tri", g["o3d_in"][: len(g["out_ccir"])][:, :9])
     m = ~np.isnan(g["out_ccir"])
     assert np.array_equal(cc[m], g["out_ccir"][m])
 
 
-def test_predicates_random_vs_oracle(gq):
+def test_predicates_random_and_degenerate_vs_oracle(gq):
     import oracle
     rng = np.random.default_rng(7)
-    for name, oname, w in (("orient3d", "or_orient3d", 12), ("insphere", "or_insphere", 15)):
-        x = rng.uniform(-1, 1, (20000, w))
-        # half of them snapped to a coarse grid: many exact zeros / ties
-        x[::2] = np.round(x[::2] * 4) / 4
-        assert np.array_equal(gq.batch(name, x), oracle.batch(oname, x))
+    for name, oname, w in (("orient3d", "or_orient3d", 12), ("insphere", "or_insphere", 15),
+                           ("orient2d", "or_orient2d", 6), ("incircle2d", "or_incircle2d", 8)):
+        x = rng.uniform(-1, 1, (50000, w))
+        x[::2] = np.round(x[::2] * 4) / 4          # exact zeros / ties on a coarse grid
+        x[1::4] *= 1e-150                          # tiny magnitudes
+        assert np.array_equal(gq.batch(name, x), oracle.batch(oname, x)), name
+
+
+def _refine(plc, B, **kw):
+    from paper_1903_03406_b200 import RefineConfig, refine
+    return refine(plc, RefineConfig(B=B, **kw))
 
 
 @pytest.mark.parametrize("name", ["cube0", "cube100", "cube300", "c1", "seg1000", "rect600", "tri500", "oblique500"])
-def test_refine_vs_reference(gq, golden_dir, name):
-    from paper_1903_03406_b200 import RefineConfig, refine
+def test_refine_matches_reference(gq, golden_dir, name):
     g = np.load(os.path.join(golden_dir, f"refine_{name}.npz"))
     build, B = CASES[name]
-    mesh, rep = refine(build(), RefineConfig(B=float(g["B"])))
+    mesh, rep = _refine(build(), float(g["B"]))
     steiner = int(g["steiner"])
-    # north-star bar: Steiner count and residual bad tets within 2% of the reference
     assert abs(rep.steiner_points - steiner) <= max(1, 0.02 * steiner), (rep.steiner_points, steiner)
     assert abs(rep.bad_tet_count - int(g["bad_tet_count"])) <= max(2, 0.02 * int(g["bad_tet_count"]))
     mesh.audit()
-    # conformity: every subsegment is an edge, every subface a face (audit), and
-    # the subsegments of each input segment tile it
-    if mesh.nv == len(g["points"]) and np.array_equal(mesh.points, g["points"]):
-        # identical run: same tets too
-        real = mesh.tv[(mesh.alive == 1) & (mesh.tv[:, 3] >= 0)]
-        assert tet_hash(real) == str(g["tet_hash"])
+    # in fact bit-identical: same points in the same order, same tets
+    assert mesh.nv == len(g["points"])
+    assert np.array_equal(mesh.points, g["points"])
+    real = mesh.tv[(mesh.alive == 1) & (mesh.tv[:, 3] >= 0)]
+    assert tet_hash(real) == str(g["tet_hash"])
+    rows = np.array([[r["round"], {"segments": 0, "faces": 1, "tets": 2}[r["phase"]], r["candidates"], r["accepted"],
+                      r["blasted"], r["failed"], r["inserted"], r["pending_segments"], r["pending_faces"]]
+                     for r in rep.per_round], dtype=np.int64).reshape(-1, 9)
+    assert np.array_equal(rows, g["per_round"])
+    assert sorted(mesh.subfaces) == sorted(tuple(r[:3]) for r in g["subfaces"].tolist())
+
+
+@pytest.mark.parametrize("seed,rounds", [(1, 500), (2, 500), (0, 7)])
+def test_refine_vs_oracle_other_seeds_and_round_caps(gq, seed, rounds):
+    import oracle
+    from paper_1903_03406_b200 import synth
+    plc = synth.cube_points(200, seed)
+    mesh, rep = _refine(plc, 2.0, max_rounds=rounds, seed=seed)
+    ref = oracle.refine(plc, B=2.0, max_rounds=rounds, seed=seed)
+    assert np.array_equal(mesh.points, ref["points"])
+    assert len(rep.per_round) == len(ref["per_round"])
+
+
+def test_refine_c2_scaled_vs_oracle(gq):
+    """C2 shape at 1/10 scale: 10.2k points + 100 segments, padded box."""
+    import oracle
+    from paper_1903_03406_b200 import synth
+    plc = synth.config_plc("C2", scale=0.1)
+    mesh, rep = _refine(plc, 1.6)
+    ref = oracle.refine(plc, B=1.6)
+    assert np.array_equal(mesh.points, ref["points"])
+    assert rep.bad_tet_count == int(((ref["alive"] == 1) & (ref["tv"][:, 3] >= 0) & (ref["ratio"] > 1.6)).sum())
+
+
+def test_refine_c2_full_matches_published_reference_counts(gq):
+    """Full BASELINE configs[1]: the reference's measured run (SURVEY.md
+    Appendix A / BASELINE.md section 2) gave 135,443 Steiner points,
+    1,519,731 tets, 19 bad tets, 28 skipped, 101 rounds."""
+    from paper_1903_03406_b200 import synth
+    mesh, rep = _refine(synth.config_plc("C2"), 1.6)
+    assert rep.steiner_points == 135443
+    assert rep.tet_count == 1519731
+    assert rep.bad_tet_count == 19
+    assert len(rep.skipped) == 28
+    assert len(rep.per_round) == 101
+
+
+def test_edge_cases(gq):
+    from paper_1903_03406_b200 import PLC, unit_cube
+    from paper_1903_03406_b200.errors import InvalidPLC
+    # the bare unit cube: 4 Steiner points (SPEC.md:308)
+    mesh, rep = _refine(unit_cube(), 2.0)
+    assert rep.steiner_points == 4 and rep.bad_tet_count == 0
+    mesh.audit(check_delaunay=True)
+    # a PLC that is already fine inserts nothing: 4 far-apart points, no features -> box only
+    pts = [(0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)]
+    mesh, rep = _refine(PLC(points=pts), 2.0)
+    mesh.audit()
+    # invalid input is rejected before any device work
+    with pytest.raises(InvalidPLC):
+        _refine(PLC(points=[(0, 0, 0), (1, 1, 0), (1, 0, 0), (0, 1, 0)], segments=[(0, 1), (2, 3)]), 2.0)
+
+
+def test_no_cpu_fallback_library_loaded(gq):
+    """The product path runs the in-tree CUDA library."""
+    import paper_1903_03406_b200._native as nat
+    assert os.path.basename(nat.lib_path()) in ("libgqm3d.so",) or "GQM3D_LIB" in os.environ
+    assert nat._LIB is not None
