@@ -27,6 +27,8 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "gq_dev.cuh"
@@ -322,6 +324,21 @@ __global__ void k_region(Dev D, Cand C, Scr SC, int n0, int n1, const int* list,
   }
 }
 
+// coarse grid of inserted vertices: a pending point's first walk starts next
+// to an already inserted vertex instead of at the initial tet
+struct CellHint { double lo[3], inv[3]; int G; int* cellv; };
+__device__ __forceinline__ int cell_of(const CellHint& H, const double* p) {
+  int c[3];
+  for (int k = 0; k < 3; ++k) {
+    double f = (p[k] - H.lo[k]) * H.inv[k];
+    c[k] = f >= 0.0 ? (f < (double)H.G ? (int)f : H.G - 1) : 0;
+  }
+  return (c[0] * H.G + c[1]) * H.G + c[2];
+}
+__global__ void k_init_cellmark(Dev D, CellHint H, const int* pend, const int* plist, const int* acc, int nw) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x)
+    if (acc[w]) { int v = pend[plist[w]]; H.cellv[cell_of(H, PT(D, v))] = v; }
+}
 // one warp per candidate (the common case); overflowing cavities are marked
 // CS_OVF for the block kernel
 __global__ void __launch_bounds__(32 * WR_WARPS) k_region_warp(Dev D, Cand C, Scr SC, int n0, int n1) {
@@ -355,7 +372,8 @@ __global__ void __launch_bounds__(32 * WR_WARPS) k_region_warp(Dev D, Cand C, Sc
 }
 // bulk construction, warp per pending point (cached cavities re-validated)
 __global__ void __launch_bounds__(32 * WR_WARPS) k_init_region_warp(Dev D, Cand C, Scr SC, const int* pend, const int* plist,
-                                                                    int Wn, int* hint, const int* succ, const int* touched, int round) {
+                                                                    int Wn, int* hint, const int* succ, const int* touched, int round,
+                                                                    CellHint H) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpShared& W = reinterpret_cast<WarpShared*>(smem_raw)[wib];
@@ -383,6 +401,10 @@ __global__ void __launch_bounds__(32 * WR_WARPS) k_init_region_warp(Dev D, Cand 
     if (lane == 0) {
       int h = hint[c];
       DCHK(h >= -1 && h < D.tcap);
+      if (h < 0) {                      // first walk: start beside a nearby inserted vertex
+        int cv = H.cellv[cell_of(H, p)];
+        h = cv >= 0 ? D.vert_tet[cv] : 0;
+      }
       while (h >= 0 && !D.alive[h]) h = succ[h];
       int t = walk(D, p, h);
       hint[c] = t;
@@ -449,6 +471,7 @@ __global__ void __launch_bounds__(BR_THREADS) k_init_region_block(Dev D, Cand C,
       C.bigi[c] = w;
       const double* p = PT(D, pend[c]);
       int h = hint[c];
+      if (h < 0) h = 0;
       while (h >= 0 && !D.alive[h]) h = succ[h];
       s_t = walk(D, p, h);
       hint[c] = s_t;
@@ -1208,6 +1231,7 @@ __global__ void k_init_region(Dev D, Cand C, Scr SC, const int* pend, const int*
     int v = pend[c];
     const double* p = PT(D, v);
     int h = hint[c];
+    if (h < 0) h = 0;
     while (h >= 0 && !D.alive[h]) h = succ[h];
     int t = walk(D, p, h);
     hint[c] = t;
@@ -1714,11 +1738,62 @@ __global__ void k_batch(int which, const double* in, int n, signed char* out8, d
 // host driver
 // ===========================================================================
 
-template <class T> static T* dmalloc(size_t n) {
+// Caching device allocator.  A refine allocates a few GB of mesh, candidate and
+// scratch arrays; repeated refines on a context (bench steps, batches of PLCs)
+// reuse them instead of paying cudaMalloc / cudaFree (a device-wide sync) in
+// the middle of the rounds.  Blocks are binned in size classes (<= 25% slack);
+// everything runs on the context's single stream, so reuse is stream-ordered.
+struct DevCache {
+  std::mutex mu;
+  std::unordered_multimap<size_t, void*> free_blocks;
+  std::unordered_map<void*, size_t> live;
+};
+static DevCache& dev_cache() {
+  static DevCache caches[64];
+  int d = 0;
+  cudaGetDevice(&d);
+  return caches[d & 63];
+}
+static size_t size_class(size_t b) {
+  if (b <= 4096) return 4096;
+  size_t p = 4096;
+  while (p < b) p <<= 1;
+  size_t step = p / 8;
+  return (b + step - 1) / step * step;
+}
+static void cache_trim(DevCache& C) {
+  for (auto& kv : C.free_blocks) cudaFree(kv.second);
+  C.free_blocks.clear();
+}
+static void* cache_alloc(size_t bytes) {
+  DevCache& C = dev_cache();
+  std::lock_guard<std::mutex> g(C.mu);
+  size_t cls = size_class(bytes);
+  auto it = C.free_blocks.find(cls);
   void* p = nullptr;
+  if (it != C.free_blocks.end()) {
+    p = it->second;
+    C.free_blocks.erase(it);
+  } else if (cudaMalloc(&p, cls) != cudaSuccess) {
+    cudaGetLastError();
+    cache_trim(C);                       // out of memory: return the cached blocks, retry once
+    CK(cudaMalloc(&p, cls));
+  }
+  C.live[p] = cls;
+  return p;
+}
+static void dfree(void* p) {
+  if (!p) return;
+  DevCache& C = dev_cache();
+  std::lock_guard<std::mutex> g(C.mu);
+  auto it = C.live.find(p);
+  if (it == C.live.end()) { cudaFree(p); return; }
+  C.free_blocks.emplace(it->second, p);
+  C.live.erase(it);
+}
+template <class T> static T* dmalloc(size_t n) {
   if (n == 0) n = 1;
-  CK(cudaMalloc(&p, n * sizeof(T)));
-  return (T*)p;
+  return (T*)cache_alloc(n * sizeof(T));
 }
 
 struct gq_ctx {
@@ -1747,6 +1822,12 @@ struct gq_ctx {
   long long launches = 0;
   double init_ms = 0, dev_ms = 0, region_ms = 0;
   cudaEvent_t ev0, ev1, er0, er1;
+  // event pool: region-kernel timing and the GQ_PROFILE=3 stage timeline are
+  // resolved once at the end of a refine, never by a per-launch sync
+  std::vector<cudaEvent_t> evpool;
+  size_t evused = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> rpairs;
+  std::vector<std::pair<cudaEvent_t, int>> fev;
   std::vector<std::vector<int>> polys;
   CGrid G{};
   int reg_seg = 0, reg_face = 0, reg_nv = 0;
@@ -1761,7 +1842,8 @@ struct gq_ctx {
 static double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
 static double g_prof[8];
 // fine stage timers (GQ_PROFILE=2): synchronise and charge the elapsed time
-static bool g_fine = false;
+static bool g_fine = false;      // GQ_PROFILE=2: host clock after a sync per stage
+static bool g_fine_ev = false;   // GQ_PROFILE=3: events per stage (device timeline, no syncs)
 static double g_fine_t[32];
 static const char* g_fine_names[32] = {"i.region", "i.big", "i.filter", "i.scan", "i.kill", "i.stars", "i.compact",
   "p.gridsync", "p.newverts", "p.check", "p.compact", "r.sorted", "r.make", "r.redirect", "r.append", "f.states",
@@ -1792,14 +1874,14 @@ static int grid_for(long long n, int bs = 128, int cap = 148 * 16) {
 
 static void ensure_cub(gq_ctx* c, size_t need) {
   if (need <= c->cub_cap) return;
-  if (c->cub_tmp) cudaFree(c->cub_tmp);
+  dfree(c->cub_tmp);
   c->cub_cap = need * 2;
-  CK(cudaMalloc(&c->cub_tmp, c->cub_cap));
+  c->cub_tmp = dmalloc<char>(c->cub_cap);
 }
 static void ensure_tmp(gq_ctx* c, size_t n) {
   if (n <= c->tmpcap) return;
   for (void* p : {(void*)c->tmpA, (void*)c->tmpB, (void*)c->tmpC, (void*)c->k64a, (void*)c->k64b, (void*)c->k32a, (void*)c->k32b})
-    if (p) cudaFree(p);
+    if (p) dfree(p);
   c->tmpcap = n * 2;
   c->tmpA = dmalloc<int>(c->tmpcap); c->tmpB = dmalloc<int>(c->tmpcap); c->tmpC = dmalloc<int>(c->tmpcap);
   c->k64a = dmalloc<unsigned long long>(c->tmpcap); c->k64b = dmalloc<unsigned long long>(c->tmpcap);
@@ -1878,7 +1960,7 @@ static void free_cands(Cand& C) {
                 C.state, C.vid, C.nt0, C.ntet, C.nbf, C.ncr, C.nbsub, C.nbseg, C.neseg, C.mind, C.tets, C.bf, C.cr,
                 C.crf, C.bsub, C.bseg, C.eseg, C.rseg, C.rface, C.nrseg, C.nrface, C.bigi, C.btets, C.bbf, C.bcr,
                 C.bcrf, C.bbsub, C.bbseg, C.beseg};
-  for (void* p : ps) if (p) cudaFree(p);
+  for (void* p : ps) if (p) dfree(p);
   C = Cand{};
 }
 static void ensure_cands(gq_ctx* c, int n) {
@@ -1921,7 +2003,7 @@ static void ensure_big(gq_ctx* c, int need) {
   auto grow = [&](int*& ptr, size_t w) {
     int* q = dmalloc<int>((size_t)cap * w);
     if (keep) CK(cudaMemcpy(q, ptr, 4 * keep * w, cudaMemcpyDeviceToDevice));
-    cudaFree(ptr);
+    dfree(ptr);
     ptr = q;
   };
   grow(C.btets, CTB); grow(C.bbf, CFB); grow(C.bcr, CCB); grow(C.bcrf, CCB);
@@ -2017,7 +2099,7 @@ static void free_all(gq_ctx* c) {
                 c->SB.stack, c->SB.in, c->SB.comp, c->tmpA, c->tmpB, c->tmpC, c->k64a, c->k64b, c->k32a, c->k32b,
                 c->cub_tmp, c->d_order, c->G.head, c->G.nodes, c->G.big, c->G.nnodes, c->Q.a, c->Q.b, c->Q.c,
                 c->Q.d, c->Q.e, c->Q.f, c->Q.g, c->Q.h, c->tv2, c->tn2, c->sub2, c->seg2, c->skip2, c->ratio2};
-  for (void* p : ps) if (p) cudaFree(p);
+  for (void* p : ps) if (p) dfree(p);
   free_cands(c->C);
   c->allocated = false;
   c->tmpcap = 0; c->cub_cap = 0; c->cub_tmp = nullptr;
@@ -2027,16 +2109,35 @@ static void free_all(gq_ctx* c) {
 }
 
 // regions for candidates [n0,n1): normal pass, then the overflow ones with big slabs
-static void time_region(gq_ctx* c) {
-  CK(cudaEventSynchronize(c->er1));
-  float ms = 0;
-  cudaEventElapsedTime(&ms, c->er0, c->er1);
-  c->region_ms += ms;
+static cudaEvent_t ev_next(gq_ctx* c) {
+  if (c->evused == c->evpool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    c->evpool.push_back(e);
+  }
+  return c->evpool[c->evused++];
+}
+static void region_begin(gq_ctx* c) { c->er0 = ev_next(c); CK(cudaEventRecord(c->er0, c->st)); }
+static void region_end(gq_ctx* c) {
+  c->er1 = ev_next(c);
+  CK(cudaEventRecord(c->er1, c->st));
+  c->rpairs.push_back({c->er0, c->er1});
+}
+// after the final sync of a refine: sum the region-kernel intervals, resolve the stage timeline
+static void resolve_events(gq_ctx* c) {
+  for (auto& pr : c->rpairs) { float ms = 0; cudaEventElapsedTime(&ms, pr.first, pr.second); c->region_ms += ms; }
+  for (size_t i = 1; i < c->fev.size(); ++i) {
+    if (c->fev[i].second < 0) continue;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->fev[i - 1].first, c->fev[i].first);
+    g_fine_t[c->fev[i].second] += ms * 1e-3;
+  }
+  c->rpairs.clear(); c->fev.clear(); c->evused = 0;
 }
 static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   if (n1 <= n0) return;
   fine(c, 31);
-  CK(cudaEventRecord(c->er0, c->st));
+  region_begin(c);
   if (!getenv("GQ_THREAD_REGIONS")) {   // debug switch: per-thread kernel
     long long nw = n1 - n0;
     int blocks = (int)std::min<long long>((nw + WR_WARPS - 1) / WR_WARPS, c->S.nthreads / WR_WARPS);
@@ -2046,8 +2147,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   } else {
     LAUNCH_S(k_region, n1 - n0, c->D, c->C, c->S, n0, n1, (const int*)nullptr, probe, 0);
   }
-  CK(cudaEventRecord(c->er1, c->st));
-  time_region(c);
+  region_end(c);
   fine(c, 24);
   // overflow pass
   ensure_tmp(c, n1 + 1);
@@ -2212,6 +2312,7 @@ static void compact_tets(gq_ctx* c) {
 }
 
 static void ensure_big(gq_ctx* c, int need);
+static bool g_trace = false;
 static void init_delaunay(gq_ctx* c, const int* order, int n) {
   CK(cudaMemcpyAsync(c->d_order, order, 4 * (size_t)n, cudaMemcpyHostToDevice, c->st));
   LAUNCH(k_init_first, 1, c->D, c->d_order, n, c->d_int + 8);
@@ -2240,7 +2341,18 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
   int* d_touched = dmalloc<int>(c->D.tcap);
   CK(cudaMemsetAsync(d_succ, 0xff, 4 * (size_t)c->D.tcap, c->st));
   CK(cudaMemsetAsync(d_touched, 0xff, 4 * (size_t)c->D.tcap, c->st));
-  CK(cudaMemsetAsync(d_hint, 0, 4 * (size_t)np, c->st));
+  CK(cudaMemsetAsync(d_hint, 0xff, 4 * (size_t)np, c->st));   // -1: no walk yet
+  CellHint H;
+  {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    std::vector<double> P(3 * (size_t)n);
+    CK(cudaMemcpy(P.data(), c->D.P, 24 * (size_t)n, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], P[3 * i + k]); hi[k] = std::max(hi[k], P[3 * i + k]); }
+    H.G = std::max(1, std::min(128, (int)std::cbrt(n / 2.0)));
+    for (int k = 0; k < 3; ++k) { H.lo[k] = lo[k]; H.inv[k] = hi[k] > lo[k] ? H.G / (hi[k] - lo[k]) : 0.0; }
+    H.cellv = dmalloc<int>((size_t)H.G * H.G * H.G);
+    CK(cudaMemsetAsync(H.cellv, 0xff, 4 * (size_t)H.G * H.G * H.G, c->st));
+  }
   CK(cudaMemsetAsync(C.status, 0, 4 * (size_t)np, c->st));          // CS_OK, not cached
   CK(cudaMemsetAsync(C.memb, 0xff, 4 * (size_t)np, c->st));
   CK(cudaMemsetAsync(C.bigi, 0xff, 4 * (size_t)np, c->st));
@@ -2251,12 +2363,14 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
   pull(c);
   int nt = c->hc.nt;
   int left = np, inserted = 4;
-  double wf = getenv("GQ_INIT_WINDOW") ? atof(getenv("GQ_INIT_WINDOW")) : 1.0;
+  // window = the next wf * inserted pending points; the number of rounds is set by the
+  // strict-order dependency chain, not the window, so a small window only saves work
+  double wf = getenv("GQ_INIT_WINDOW") ? atof(getenv("GQ_INIT_WINDOW")) : 0.0625;
   fine(c, -1);
   for (int round = 0; left > 0; ++round) {
     int W = (int)std::min<double>(left, std::max(64.0, wf * inserted));
     fine(c, 22);
-    CK(cudaEventRecord(c->er0, c->st));
+    region_begin(c);
     if (!getenv("GQ_THREAD_INIT")) {
       int blocks = std::min((W + WR_WARPS - 1) / WR_WARPS, c->S.nthreads / WR_WARPS);
       static int* h_wdbg = nullptr;
@@ -2267,7 +2381,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
       }
       if (h_wdbg) std::memset(h_wdbg, 0xff, 200000 * sizeof(int));
       k_init_region_warp<<<std::max(blocks, 1), 32 * WR_WARPS, WR_WARPS * sizeof(WarpShared), c->st>>>(
-          c->D, C, c->S, d_pend, d_plist, W, d_hint, d_succ, d_touched, round);
+          c->D, C, c->S, d_pend, d_plist, W, d_hint, d_succ, d_touched, round, H);
       c->launches++;
       CK(cudaGetLastError());
       if (h_wdbg) {
@@ -2289,8 +2403,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     } else {
       LAUNCH_S(k_init_region, W, c->D, C, c->S, d_pend, d_plist, W, d_hint, d_succ, d_touched, round, 0);
     }
-    CK(cudaEventRecord(c->er1, c->st));
-    time_region(c);
+    region_end(c);
     fine(c, 0);
     // big cavities (early rounds): resolve the lowest-order ones, truncate the window at the rest
     std::vector<int> bl;
@@ -2355,6 +2468,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
       CK(cudaGetLastError());
     }
     fine(c, 5);
+    LAUNCH(k_init_cellmark, W, c->D, H, d_pend, d_plist, d_acc, W);
     nt += add_t;
     // release big slabs (big regions are recomputed next round if still pending)
     LAUNCH(k_init_keep, W, d_acc, W, d_keep);
@@ -2362,6 +2476,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     LAUNCH(k_init_compact, left, d_plist, d_acc, d_scan, W, left, d_plist2);
     std::swap(d_plist, d_plist2);
     if (!bl.empty()) LAUNCH(k_release_big, bl.size(), C, c->tmpC, (int)bl.size());
+    if (g_trace) std::fprintf(stderr, "[init] round %d W %d big %d acc %d nt %d\n", round, W, (int)bl.size(), nacc, nt);
     left -= nacc;
     inserted += nacc;
     c->hc.nt = nt;
@@ -2372,8 +2487,8 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
   }
   // big-slab candidates must not keep stale bigi for the refinement rounds
   sync(c);
-  cudaFree(d_pend); cudaFree(d_hint); cudaFree(d_plist); cudaFree(d_plist2); cudaFree(d_acc);
-  cudaFree(d_scan); cudaFree(d_keep); cudaFree(d_succ); cudaFree(d_touched);
+  dfree(d_pend); dfree(d_hint); dfree(d_plist); dfree(d_plist2); dfree(d_acc);
+  dfree(d_scan); dfree(d_keep); dfree(d_succ); dfree(d_touched); dfree(H.cellv);
 }
 
 // ------------------------------------------------------------------ round
@@ -2529,13 +2644,18 @@ static void ensure_q(gq_ctx* c, size_t n) {
   if (n <= c->Q.cap) return;
   int** ps[] = {&c->Q.a, &c->Q.b, &c->Q.c, &c->Q.d, &c->Q.e, &c->Q.f, &c->Q.g, &c->Q.h};
   size_t cap = n + n / 2;
-  for (int** q : ps) { if (*q) cudaFree(*q); *q = dmalloc<int>(cap); }
+  for (int** q : ps) { if (*q) dfree(*q); *q = dmalloc<int>(cap); }
   c->Q.cap = cap;
 }
 
-static bool g_trace = false;
 static void fine(gq_ctx* c, int k) {
   if (g_trace) { CK(cudaStreamSynchronize(c->st)); std::fprintf(stderr, "[trace] stage %d ok\n", k); }
+  if (g_fine_ev) {
+    cudaEvent_t e = ev_next(c);
+    CK(cudaEventRecord(e, c->st));
+    c->fev.push_back({e, k});
+    return;
+  }
   if (!g_fine) return;
   CK(cudaStreamSynchronize(c->st));
   double t = now_s();
@@ -2674,7 +2794,9 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
                         const int* pidx, int f, const int* keep, const int* order, const gq_config* cfg,
                         gq_counts* out) {
   c->B = cfg->B; c->max_rounds = cfg->max_rounds; c->seed = cfg->seed; c->verbose = cfg->flags & 1;
-  g_fine = getenv("GQ_PROFILE") && atoi(getenv("GQ_PROFILE")) >= 2;
+  g_fine = getenv("GQ_PROFILE") && atoi(getenv("GQ_PROFILE")) == 2;
+  g_fine_ev = getenv("GQ_PROFILE") && atoi(getenv("GQ_PROFILE")) == 3;
+  c->rpairs.clear(); c->fev.clear(); c->evused = 0;
   g_trace = getenv("GQ_TRACE") != nullptr;
   { int ws = getenv("GQ_WSTOP") ? atoi(getenv("GQ_WSTOP")) : 0; CK(cudaMemcpyToSymbol(g_wstop, &ws, 4)); }
   c->n_input = n_input; c->npoly = f;
@@ -2754,7 +2876,7 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
     CK(cudaMemcpy(dseg, seg, 8 * (size_t)m, cudaMemcpyHostToDevice));
     LAUNCH(k_segs_init, m, D, dseg, m);
     sync(c);
-    cudaFree(dseg);
+    dfree(dseg);
   }
   pull(c);
   c->hc.nsegrec = m;
@@ -2768,7 +2890,7 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
     pull(c);
     LAUNCH(k_facets_records, c->hc.nt2, D, c->hc.nt2);
     sync(c);
-    cudaFree(dpo); cudaFree(dpi);
+    dfree(dpo); dfree(dpi);
   }
   LAUNCH(k_refresh_all, c->hc.nt, D);
   sync(c);
@@ -2806,7 +2928,8 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   CK(cudaEventRecord(c->ev1, c->st));
   sync(c);
   float ms = 0; cudaEventElapsedTime(&ms, c->ev0, c->ev1); c->dev_ms = ms;
-  if (g_fine) {
+  resolve_events(c);
+  if (g_fine || g_fine_ev) {
     std::fprintf(stderr, "[gq fine]");
     for (int k = 0; k < 32; ++k) if (g_fine_t[k] > 0) { std::fprintf(stderr, " %s %.1f;", g_fine_names[k], 1000 * g_fine_t[k]); g_fine_t[k] = 0; }
     std::fprintf(stderr, "\n");
@@ -2886,7 +3009,13 @@ int gq_create(int device, gq_ctx** out) {
 
 int gq_destroy(gq_ctx* c) {
   if (!c) return GQ_EINVAL;
-  try { cudaSetDevice(c->device); free_all(c); if (c->st) cudaStreamDestroy(c->st); } catch (...) {}
+  try {
+    cudaSetDevice(c->device);
+    free_all(c);
+    for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
+    { DevCache& C = dev_cache(); std::lock_guard<std::mutex> g(C.mu); cache_trim(C); }
+    if (c->st) cudaStreamDestroy(c->st);
+  } catch (...) {}
   delete c;
   return GQ_OK;
 }
@@ -2989,7 +3118,7 @@ int gq_quality(gq_ctx* c, double B, int64_t* bad_count, int64_t* hist36) {
     sync(c);
     unsigned long long h[37];
     CK(cudaMemcpy(h, d, 37 * 8, cudaMemcpyDeviceToHost));
-    cudaFree(d);
+    dfree(d);
     if (bad_count) *bad_count = (int64_t)h[0];
     if (hist36) for (int k = 0; k < 36; ++k) hist36[k] = (int64_t)h[1 + k];
   } catch (std::exception& e) { c->err = e.what(); return GQ_ECUDA; }
@@ -3009,7 +3138,7 @@ int gq_batch(int which, const double* in, int32_t n, int32_t width, int8_t* out8
     CK(cudaDeviceSynchronize());
     if (out8) CK(cudaMemcpy(out8, d8, n, cudaMemcpyDeviceToHost));
     if (outd) CK(cudaMemcpy(outd, dd, 32 * (size_t)n, cudaMemcpyDeviceToHost));
-    cudaFree(din); cudaFree(d8); cudaFree(dd);
+    dfree(din); dfree(d8); dfree(dd);
   } catch (std::exception&) { return GQ_ECUDA; }
   return GQ_OK;
 }
