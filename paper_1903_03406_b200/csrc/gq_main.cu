@@ -54,8 +54,8 @@ using namespace gq;
 #define CS_DROP 5      // redirected / skipped before the pool
 
 // slab capacities (normal pass); overflowing candidates rerun with big slabs
-#define CT 128
-#define CF 272
+#define CT 512
+#define CF 1088
 #define CC 96
 #define CRD 64
 #define CTB 4096
@@ -1842,6 +1842,7 @@ struct gq_ctx {
 static double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
 static double g_prof[8];
 // fine stage timers (GQ_PROFILE=2): synchronise and charge the elapsed time
+static bool g_trace = false;
 static bool g_fine = false;      // GQ_PROFILE=2: host clock after a sync per stage
 static bool g_fine_ev = false;   // GQ_PROFILE=3: events per stage (device timeline, no syncs)
 static double g_fine_t[32];
@@ -2165,7 +2166,17 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
     c->launches++;
     CK(cudaGetLastError());
     c->big_used += nb;
+    double tb = now_s();
     sync(c);
+    if (g_trace) {
+      std::vector<int> nts(nb);
+      int mx = 0; long long sm = 0;
+      for (int k = 0; k < nb; ++k) {
+        CK(cudaMemcpy(&nts[k], c->C.ntet + big[k], 4, cudaMemcpyDeviceToHost));
+        mx = std::max(mx, nts[k]); sm += nts[k];
+      }
+      std::fprintf(stderr, "[big] n %d of %d tets max %d mean %.0f block %.3f ms\n", nb, n1 - n0, mx, (double)sm / nb, 1e3 * (now_s() - tb));
+    }
   }
   fine(c, 26);
 }
@@ -2312,7 +2323,6 @@ static void compact_tets(gq_ctx* c) {
 }
 
 static void ensure_big(gq_ctx* c, int need);
-static bool g_trace = false;
 static void init_delaunay(gq_ctx* c, const int* order, int n) {
   CK(cudaMemcpyAsync(c->d_order, order, 4 * (size_t)n, cudaMemcpyHostToDevice, c->st));
   LAUNCH(k_init_first, 1, c->D, c->d_order, n, c->d_int + 8);

@@ -27,11 +27,11 @@ __device__ volatile int* g_wdbg;      // pinned host mirror: [warp][2] = candida
 #define WMARK(k) do {} while (0)
 #endif
 #define WSTOP(k) do { if (g_wstop == (k)) return RS_CNSS; } while (0)
-#define WR_MAXT 128
+#define WR_MAXT 512
 #ifndef CC_DBG
 #define CC_DBG 96
 #endif
-#define WR_HASH 512
+#define WR_HASH 2048
 #define WR_WARPS 8          // warps per block
 
 struct WarpShared {
