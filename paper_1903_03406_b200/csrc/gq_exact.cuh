@@ -253,6 +253,9 @@ __device__ inline int orient3d(const double* a, const double* b, const double* c
   double perm = fabs(adz) * (fabs(bdxcdy) + fabs(cdxbdy)) + fabs(bdz) * (fabs(cdxady) + fabs(adxcdy))
               + fabs(cdz) * (fabs(adxbdy) + fabs(bdxady));
   if (fabs(det) > GQ_O3D_BOUND * perm) return -fsign(det);
+  // four points on one axis-aligned plane (box and cube faces): exactly zero
+  for (int k = 0; k < 3; ++k)
+    if (a[k] == b[k] && a[k] == c[k] && a[k] == d[k]) return 0;
   atomicAdd(&g_exact_calls[2], 1ull);
   return orient3d_exact(a, b, c, d);
 }
@@ -498,6 +501,9 @@ __device__ __forceinline__ double dist2(const double* a, const double* b) {
 }
 
 // geometry.py:132-156: p strictly inside the diametral ball of (u,v)
+__device__ __forceinline__ bool same_point(const double* a, const double* b) {
+  return a[0] == b[0] && a[1] == b[1] && a[2] == b[2];
+}
 __device__ __noinline__ bool encroaches_segment(const double* u, const double* v, const double* p) {
   double f = 0.0, ssq = 0.0;
   for (int k = 0; k < 3; ++k) {
@@ -507,6 +513,7 @@ __device__ __noinline__ bool encroaches_segment(const double* u, const double* v
     ssq += t * t + e * e;
   }
   if (fabs(f) > 1e-12 * ssq) return f < 0.0;
+  if (same_point(p, u) || same_point(p, v)) return false;   // an endpoint is on the sphere: f == 0 exactly
   double xs[9] = {p[0], p[1], p[2], u[0], u[1], u[2], v[0], v[1], v[2]};
   BI s[9];
   scaled(xs, 9, s);
@@ -550,6 +557,8 @@ __device__ __noinline__ int equatorial_cmp(const double* a, const double* b, con
   double f = dist2(p, sph.c) - sph.r2;
   double scale = dist2(p, sph.c) + sph.r2;
   if (fabs(f) > 1e-9 * scale) return f > 0 ? 1 : -1;
+  // a vertex of the triangle lies exactly on its equatorial sphere
+  if (same_point(p, a) || same_point(p, b) || same_point(p, c)) return 0;
   return equatorial_cmp_exact(a, b, c, p);
 }
 __device__ inline bool encroaches_face(const double* a, const double* b, const double* c, const double* p) {

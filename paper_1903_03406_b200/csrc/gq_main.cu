@@ -563,15 +563,17 @@ __global__ void k_redirect(Dev D, Cand C, int n0, int n1) {
 // dead records are skipped at query time.
 struct CGrid {
   double lo[3], inv[3];
-  int G;
-  int* head;          // G^3
-  int2* nodes;        // {code = 2*rec + kind, next}
-  int* nnodes;
+  int G;              // level-0 cells per axis
+  int L;              // levels: level l has ceil(G / 2^l) cells per axis, the last has 1
+  int off[16];        // first cell of each level in start[]
+  int ncell;          // total cells over all levels
+  int* start;         // ncell + 1: CSR offsets of the cell lists (live balls only)
+  int* codes;         // 2*rec + kind
+  int* cnt;           // ncell + 1 counters / fill cursors
   int node_cap;
-  int* big;
-  int* nbig;
-  int big_cap;
+  int* nbig;          // [1] = CSR overflow flag
 };
+__device__ __host__ __forceinline__ int cg_gl(int G, int l) { return (G + (1 << l) - 1) >> l; }
 __device__ __forceinline__ int cg_ci(const CGrid& g, double x, int k) {
   double f = (x - g.lo[k]) * g.inv[k];
   if (!(f >= 0.0)) return 0;
@@ -592,8 +594,15 @@ __device__ inline bool cons_ball(const Dev& D, int kind, int r, double* c, doubl
   c[0] = s.c[0]; c[1] = s.c[1]; c[2] = s.c[2]; r2 = s.r2;
   return true;
 }
-__global__ void k_grid_register(Dev D, CGrid g, int kind, int r0, int r1) {
-  for (int r = r0 + blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += gridDim.x * blockDim.x) {
+// The grid is rebuilt from the live records whenever it is queried after a
+// change (count -> scan -> fill): cell lists are contiguous and hold no dead
+// records.  Levels halve the resolution; a ball is stored at the finest level
+// where it spans at most 3 cells per axis, so a query reads one short run per
+// level and there is no "big ball" list scanned by everyone.
+// pass 0 counts, pass 1 fills.
+__global__ void k_grid_build(Dev D, CGrid g, int nseg, int nface, int pass) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nseg + nface; x += gridDim.x * blockDim.x) {
+    int kind = x < nseg ? 0 : 1, r = x < nseg ? x : x - nseg;
     unsigned int fl = kind == 0 ? D.sg_fl[r] : D.sf_fl[r];
     if (!(fl & RF_LIVE)) continue;
     double c[3], r2;
@@ -602,26 +611,22 @@ __global__ void k_grid_register(Dev D, CGrid g, int kind, int r0, int r1) {
     int i0 = cg_ci(g, c[0] - rr, 0), i1 = cg_ci(g, c[0] + rr, 0);
     int j0 = cg_ci(g, c[1] - rr, 1), j1 = cg_ci(g, c[1] + rr, 1);
     int k0 = cg_ci(g, c[2] - rr, 2), k1 = cg_ci(g, c[2] + rr, 2);
-    long long nc = (long long)(i1 - i0 + 1) * (j1 - j0 + 1) * (k1 - k0 + 1);
+    int l = 0;
+    while (l < g.L - 1 && ((i1 >> l) - (i0 >> l) > 2 || (j1 >> l) - (j0 >> l) > 2 || (k1 >> l) - (k0 >> l) > 2)) ++l;
+    const int Gl = cg_gl(g.G, l), base = g.off[l];
     int code = 2 * r + kind;
-    if (nc > 64) {
-      int b = atomicAdd(g.nbig, 1);
-      if (b < g.big_cap) g.big[b] = code; else raise_err(GQ_ERR_CAP);
-      continue;
-    }
-    for (int i = i0; i <= i1; ++i) for (int j = j0; j <= j1; ++j) for (int k = k0; k <= k1; ++k) {
-      int nd = atomicAdd(g.nnodes, 1);
-      if (nd >= g.node_cap) { raise_err(GQ_ERR_CAP); return; }
-      int cell = (i * g.G + j) * g.G + k;
-      g.nodes[nd].x = code;
-      g.nodes[nd].y = atomicExch(g.head + cell, nd);
+    for (int i = i0 >> l; i <= i1 >> l; ++i) for (int j = j0 >> l; j <= j1 >> l; ++j) for (int k = k0 >> l; k <= k1 >> l; ++k) {
+      int cell = base + (i * Gl + j) * Gl + k;
+      if (pass == 0) { atomicAdd(g.cnt + cell, 1); continue; }
+      int pos = g.start[cell] + atomicAdd(g.cnt + cell, 1);
+      if (pos < g.node_cap) g.codes[pos] = code; else if (atomicExch(g.nbig + 1, 1) == 0) raise_err(GQ_ERR_CAP);
     }
   }
 }
 // visit every live constraint whose open ball strictly contains p
 template <class F>
 __device__ inline void grid_encroached(const Dev& D, const CGrid& g, const double* p, int kinds, F f) {
-  int cell = (cg_ci(g, p[0], 0) * g.G + cg_ci(g, p[1], 1)) * g.G + cg_ci(g, p[2], 2);
+  const int ci = cg_ci(g, p[0], 0), cj = cg_ci(g, p[1], 1), ck = cg_ci(g, p[2], 2);
   auto test = [&](int code) {
     int kind = code & 1, r = code >> 1;
     if (!((kinds >> kind) & 1)) return;
@@ -635,22 +640,12 @@ __device__ inline void grid_encroached(const Dev& D, const CGrid& g, const doubl
       if (encroaches_face(PT(D, q.x), PT(D, q.y), PT(D, q.z), p)) f(1, r);
     }
   };
-  for (int nd = g.head[cell]; nd >= 0; nd = g.nodes[nd].y) test(g.nodes[nd].x);
-  int nb = *g.nbig;
-  for (int b = 0; b < nb; ++b) test(g.big[b]);
-}
-__global__ void k_big_live(Dev D, CGrid g, int n, int* flags) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) {
-    int code = g.big[b], kind = code & 1, r = code >> 1;
-    flags[b] = kind == 0 ? (D.sg_fl[r] & RF_LIVE) != 0 : (D.sf_fl[r] & RF_LIVE) != 0;
+  for (int l = 0; l < g.L; ++l) {
+    const int Gl = cg_gl(g.G, l);
+    const int cell = g.off[l] + ((ci >> l) * Gl + (cj >> l)) * Gl + (ck >> l);
+    const int e = g.start[cell + 1];
+    for (int k = g.start[cell]; k < e; ++k) test(g.codes[k]);
   }
-}
-__global__ void k_big_gather(CGrid g, const int* pos, int n, int* out) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) out[b] = g.big[pos[b]];
-}
-__global__ void k_big_set(CGrid g, const int* src, int n) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) g.big[b] = src[b];
-  if (blockIdx.x == 0 && threadIdx.x == 0) *g.nbig = n;
 }
 // post_round part 1 (refine.py:818-828): new vertices against all balls
 __global__ void k_grid_newverts(Dev D, CGrid g, int v0, int v1) {
@@ -2074,15 +2069,21 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
     int g = (int)std::cbrt(std::max(1.0, n / 2.0));
     g = std::min(std::max(g, 4), 160);
     c->G.G = g;
-    c->G.head = dmalloc<int>((size_t)g * g * g);
-    CK(cudaMemset(c->G.head, 0xff, (size_t)g * g * g * 4));
-    c->G.node_cap = (int)std::min<size_t>(((size_t)sgcap + sfcap) * 8, (size_t)1 << 30);
-    c->G.nodes = dmalloc<int2>(c->G.node_cap);
-    c->G.big_cap = 1 << 20;
-    c->G.big = dmalloc<int>(c->G.big_cap);
-    c->G.nnodes = dmalloc<int>(2);
-    c->G.nbig = c->G.nnodes + 1;
-    CK(cudaMemset(c->G.nnodes, 0, 8));
+    size_t ncell = 0;
+    c->G.L = 0;
+    for (int l = 0;; ++l) {
+      int gl = cg_gl(g, l);
+      c->G.off[l] = (int)ncell;
+      ncell += (size_t)gl * gl * gl;
+      c->G.L = l + 1;
+      if (gl == 1) break;
+    }
+    c->G.ncell = (int)ncell;
+    c->G.start = dmalloc<int>(ncell + 1);
+    c->G.cnt = dmalloc<int>(ncell + 1);
+    c->G.node_cap = (int)std::min<size_t>(((size_t)sgcap + sfcap) * 27, (size_t)1 << 30);
+    c->G.codes = dmalloc<int>(c->G.node_cap);
+    c->G.nbig = dmalloc<int>(2);
     c->reg_seg = c->reg_face = 0;
   }
   c->allocated = true;
@@ -2098,7 +2099,7 @@ static void free_all(gq_ctx* c) {
                 c->S.tkey, c->S.tval, c->S.tep, c->S.fkey, c->S.fep, c->S.epoch, c->S.list, c->S.stack, c->S.in,
                 c->S.comp, c->SB.tkey, c->SB.tval, c->SB.tep, c->SB.fkey, c->SB.fep, c->SB.epoch, c->SB.list,
                 c->SB.stack, c->SB.in, c->SB.comp, c->tmpA, c->tmpB, c->tmpC, c->k64a, c->k64b, c->k32a, c->k32b,
-                c->cub_tmp, c->d_order, c->G.head, c->G.nodes, c->G.big, c->G.nnodes, c->Q.a, c->Q.b, c->Q.c,
+                c->cub_tmp, c->d_order, c->G.start, c->G.codes, c->G.cnt, c->G.nbig, c->Q.a, c->Q.b, c->Q.c,
                 c->Q.d, c->Q.e, c->Q.f, c->Q.g, c->Q.h, c->tv2, c->tn2, c->sub2, c->seg2, c->skip2, c->ratio2};
   for (void* p : ps) if (p) dfree(p);
   free_cands(c->C);
@@ -2269,19 +2270,16 @@ static int sorted_records(gq_ctx* c, int phase, unsigned int need, unsigned int 
 // register records created since the last call (ConstraintIndex.add_*)
 static void grid_sync(gq_ctx* c) {
   pull(c);
-  // drop dead entries from the big-ball list (scanned by every query)
-  if (++c->grid_calls % 4 == 0) {
-    int nb = read_int(c, c->G.nbig);
-    if (nb > 256) {
-      ensure_tmp(c, nb + 1);
-      LAUNCH(k_big_live, nb, c->D, c->G, nb, c->tmpB);
-      int live = select_flagged(c, c->tmpB, nb, c->tmpA);
-      LAUNCH(k_big_gather, std::max(live, 1), c->G, c->tmpA, live, c->tmpB);
-      LAUNCH(k_big_set, std::max(live, 1), c->G, c->tmpB, live);
-    }
-  }
-  if (c->hc.nsegrec > c->reg_seg) { LAUNCH(k_grid_register, c->hc.nsegrec - c->reg_seg, c->D, c->G, 0, c->reg_seg, c->hc.nsegrec); c->reg_seg = c->hc.nsegrec; }
-  if (c->hc.nfacerec > c->reg_face) { LAUNCH(k_grid_register, c->hc.nfacerec - c->reg_face, c->D, c->G, 1, c->reg_face, c->hc.nfacerec); c->reg_face = c->hc.nfacerec; }
+  int nseg = c->hc.nsegrec, nface = c->hc.nfacerec, ncell = c->G.ncell;
+  CK(cudaMemsetAsync(c->G.cnt, 0, 4 * (size_t)(ncell + 1), c->st));   // slot ncell stays 0: start[ncell] = total
+  CK(cudaMemsetAsync(c->G.nbig, 0, 8, c->st));
+  if (nseg + nface > 0) LAUNCH(k_grid_build, nseg + nface, c->D, c->G, nseg, nface, 0);
+  size_t need = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need, c->G.cnt, c->G.start, ncell + 1, c->st);
+  ensure_cub(c, need);
+  cub::DeviceScan::ExclusiveSum(c->cub_tmp, need, c->G.cnt, c->G.start, ncell + 1, c->st);
+  CK(cudaMemsetAsync(c->G.cnt, 0, 4 * (size_t)ncell, c->st));
+  if (nseg + nface > 0) LAUNCH(k_grid_build, nseg + nface, c->D, c->G, nseg, nface, 1);
 }
 
 static bool full_verify(gq_ctx* c) {
