@@ -406,6 +406,10 @@ __global__ void __launch_bounds__(32 * WR_WARPS) k_init_region_warp(Dev D, Cand 
         h = cv >= 0 ? D.vert_tet[cv] : 0;
       }
       while (h >= 0 && !D.alive[h]) h = succ[h];
+      // a ghost hint (last seen outside the hull) restarts at the hull tet behind
+      // it: walk() would otherwise rescan the tet array for a real tet.  The
+      // unconstrained cavity does not depend on the seed.
+      if (h >= 0 && D.tv[h].w == GHOST) h = tnk(D, h, 3) >> 2;
       int t = walk(D, p, h);
       hint[c] = t;
       W.seeds[0] = t;
@@ -473,6 +477,7 @@ __global__ void __launch_bounds__(BR_THREADS) k_init_region_block(Dev D, Cand C,
       int h = hint[c];
       if (h < 0) h = 0;
       while (h >= 0 && !D.alive[h]) h = succ[h];
+      if (h >= 0 && D.tv[h].w == GHOST) h = tnk(D, h, 3) >> 2;
       s_t = walk(D, p, h);
       hint[c] = s_t;
     }
@@ -1296,6 +1301,7 @@ __global__ void k_init_stars(Dev D, Cand C, const int* pend, const int* plist, c
 __global__ void k_count_ovf(const Cand C, const int* plist, int W, int* out) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x)
     if (C.status[plist[w]] == CS_OVF) atomicAdd(out, 1);
+    else if (C.status[plist[w]] == CS_OK) atomicMax(out + 1, C.ntet[plist[w]]);
 }
 __global__ void k_gather_status(const Cand C, const int* plist, int W, int* out) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) out[w] = C.status[plist[w]];
@@ -2416,7 +2422,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     // big cavities (early rounds): resolve the lowest-order ones, truncate the window at the rest
     std::vector<int> bl;
     {
-      CK(cudaMemsetAsync(c->d_int + 40, 0, 4, c->st));
+      CK(cudaMemsetAsync(c->d_int + 40, 0, 8, c->st));
       LAUNCH(k_count_ovf, W, C, d_plist, W, c->d_int + 40);
       int novf = read_int(c, c->d_int + 40);
       if (novf > 0) {
@@ -2484,7 +2490,15 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     LAUNCH(k_init_compact, left, d_plist, d_acc, d_scan, W, left, d_plist2);
     std::swap(d_plist, d_plist2);
     if (!bl.empty()) LAUNCH(k_release_big, bl.size(), C, c->tmpC, (int)bl.size());
-    if (g_trace) std::fprintf(stderr, "[init] round %d W %d big %d acc %d nt %d\n", round, W, (int)bl.size(), nacc, nt);
+    if (g_trace) {
+      sync(c);
+      float rms = 0; cudaEventElapsedTime(&rms, c->rpairs.back().first, c->rpairs.back().second);
+      unsigned long long rc = 0; CK(cudaMemcpyFromSymbol(&rc, g_region_calls, 8));
+      static unsigned long long rc_last = 0;
+      std::fprintf(stderr, "[init] round %d W %d big %d acc %d nt %d region_ms %.3f computed %llu maxtet %d\n", round, W,
+                   (int)bl.size(), nacc, nt, rms, rc - rc_last, read_int(c, c->d_int + 41));
+      rc_last = rc;
+    }
     left -= nacc;
     inserted += nacc;
     c->hc.nt = nt;

@@ -270,6 +270,7 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
   int off = incl - mycnt;
   for (int a = lo; a < hi; ++a) {
     int t = W.f0[a];
+    W.f1[a] = off;                   // first boundary face of sorted tet a
     for (int i = 0; i < 4; ++i) {
       int u = tnk(D, t, i) >> 2;
       bool blk = blocked(D, A, t, i);
@@ -321,76 +322,107 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
   WMARK(16);
   O.ntet = m; O.nbf = nbf; O.mind = mymin;
   O.ncr = 0; O.nbsub = 0; O.nbseg = 0; O.neseg = 0;
-  // ---- constraint classification (first-met order): lane 0, serial
+  // ---- constraint classification, warp-parallel.  Same lists and order as the
+  // reference's first-met loop (_kernels.py:560-635): occurrences are listed in
+  // (sorted tet, face / edge slot) order, a constraint counts at its first
+  // occurrence, and a subsegment is "boundary" iff one of the boundary faces of
+  // the tets up to its first one contains it (the numba partial-bedges rule).
   bool cons = false;
   for (int a = lane; a < m; a += 32) if (D.sub[W.f0[a]] || D.seg[W.f0[a]]) cons = true;
   WMARK(50);
   if (!__any_sync(FULL, cons)) return RS_OK;
   WSTOP(7);
-  int st = RS_OK;
-  if (lane == 0) {
-    S.fset.clear();
-    const unsigned long long TE = 2ull << 60, TSF = 3ull << 60, TSG = 4ull << 60;
-    auto member = [&](int u) {   // binary search in the sorted cavity
-      int l = 0, h = m - 1;
-      while (l <= h) { int mid = (l + h) >> 1; int v = W.f0[mid]; if (v == u) return true; if (v < u) l = mid + 1; else h = mid - 1; }
-      return false;
-    };
-    for (int a = 0; a < m && st == RS_OK; ++a) {
-      int t = W.f0[a];
-      int4 q = D.tv[t];
-      for (int i = 0; i < 4; ++i) {
-        int u = tnk(D, t, i) >> 2;
-        bool blk = blocked(D, A, t, i);
-        if (member(u) && !blk) continue;
-        int f[3]; face_verts(q, i, f);
-        for (int k = 0; k < 3; ++k) {
-          int x = f[k], y = f[(k + 1) % 3];
-          if (x == GHOST || y == GHOST) continue;
-          if (x > y) { int tt = x; x = y; y = tt; }
-          if (S.fset.add(TE | ((unsigned long long)x << 30) | (unsigned long long)y) < 0) st = RS_OVERFLOW;
-        }
-      }
-      int sm = D.sub[t];
-      for (int i = 0; sm && i < 4 && st == RS_OK; ++i) {
-        if (!(sm & (1 << i))) continue;
-        int f[3]; face_verts(q, i, f);
-        int a0 = f[0], b0 = f[1], c0 = f[2];
-        sort3(a0, b0, c0);
-        int ins = S.fset.add(TSF | (key3(a0, b0, c0) & ((1ull << 60) - 1)));
-        if (ins < 0) { st = RS_OVERFLOW; break; }
-        if (ins == 0) continue;
-        bool uin = member(tnk(D, t, i) >> 2);
-        int rec = face_lookup(D, a0, b0, c0);
-        DCHK(rec < D.sfcap);
-        bool crossed = uin && rec >= 0 && A.n > 0 && allowed_face(D, A, a0, b0, c0);
-        DCHK(O.ncr >= 0 && O.nbsub >= 0 && O.ccon == CC_DBG);
-        if (crossed) {
-          if (O.ncr >= O.ccon) { st = RS_OVERFLOW; break; }
-          O.cr[O.ncr] = rec; O.crf[O.ncr] = min(4 * t + i, tnk(D, t, i)); O.ncr++;
-        } else {
-          if (O.nbsub >= O.ccon) { st = RS_OVERFLOW; break; }
-          O.bsub[O.nbsub++] = rec;
-        }
-      }
-      int em = D.seg[t];
-      for (int i = 0; em && i < 6 && st == RS_OK; ++i) {
-        if (!(em & (1 << i))) continue;
-        int x = tvk(q, c_edges[i][0]), y = tvk(q, c_edges[i][1]);
-        if (x > y) { int tt = x; x = y; y = tt; }
-        int ins = S.fset.add(TSG | ((unsigned long long)x << 30) | (unsigned long long)y);
-        if (ins < 0) { st = RS_OVERFLOW; break; }
-        if (ins == 0) continue;
-        int rec = seg_lookup(D, x, y);
-        bool bound = S.fset.has(TE | ((unsigned long long)x << 30) | (unsigned long long)y);
-        if (O.nbseg + O.neseg >= O.ccon) { st = RS_OVERFLOW; break; }
-        if (bound) O.bseg[O.nbseg++] = rec; else O.eseg[O.neseg++] = rec;
-      }
+  // occurrences: code = a << 4 | slot (slot 0-3 subface face, 4-9 subsegment edge)
+  int* oc = W.hkey;                  // hkey / hval / cav / comp / in are free after the swallow check
+  int* k0 = W.cav; int* k1 = W.comp; int* k2 = W.hval;
+  unsigned char* ofirst = W.in;
+  const int OCAP = WR_MAXT;
+  int myocc = 0;
+  for (int a = lo; a < hi; ++a) {
+    int t = W.f0[a];
+    myocc += __popc((unsigned)D.sub[t] & 15u) + __popc((unsigned)D.seg[t] & 63u);
+  }
+  int oincl = myocc;
+  for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(FULL, oincl, o); if (lane >= o) oincl += v; }
+  const int K = __shfl_sync(FULL, oincl, 31);
+  if (K > OCAP) return RS_OVERFLOW;   // rare: the block kernel handles it
+  int op = oincl - myocc;
+  for (int a = lo; a < hi; ++a) {
+    int t = W.f0[a];
+    int4 q = D.tv[t];
+    int sm = D.sub[t], em = D.seg[t];
+    for (int i = 0; i < 4; ++i) {
+      if (!(sm & (1 << i))) continue;
+      int f[3]; face_verts(q, i, f);
+      int a0 = f[0], b0 = f[1], c0 = f[2];
+      sort3(a0, b0, c0);
+      oc[op] = a << 4 | i; k0[op] = a0; k1[op] = b0; k2[op] = c0; ++op;
+    }
+    for (int i = 0; i < 6; ++i) {
+      if (!(em & (1 << i))) continue;
+      int x = tvk(q, c_edges[i][0]), y = tvk(q, c_edges[i][1]);
+      if (x > y) { int tt = x; x = y; y = tt; }
+      oc[op] = a << 4 | (4 + i); k0[op] = x; k1[op] = y; k2[op] = -1; ++op;
     }
   }
-  st = __shfl_sync(FULL, st, 0);
-  O.ncr = __shfl_sync(FULL, O.ncr, 0); O.nbsub = __shfl_sync(FULL, O.nbsub, 0);
-  O.nbseg = __shfl_sync(FULL, O.nbseg, 0); O.neseg = __shfl_sync(FULL, O.neseg, 0);
+  __syncwarp();
+  for (int j = lane; j < K; j += 32) {
+    bool first = true;
+    const bool isf = (oc[j] & 15) < 4;
+    for (int i = 0; i < j && first; ++i)
+      if (((oc[i] & 15) < 4) == isf && k0[i] == k0[j] && k1[i] == k1[j] && k2[i] == k2[j]) first = false;
+    ofirst[j] = first;
+  }
+  __syncwarp();
+  // subfaces: crossed (allowed and interior) or boundary, appended in order
+  int st = RS_OK;
+  int ncr = 0, nbs = 0;
+  for (int base = 0; base < K; base += 32) {
+    const int j = base + lane;
+    bool isc = false, isb = false;
+    int rec = -1, crf = 0;
+    if (j < K && ofirst[j] && (oc[j] & 15) < 4) {
+      int a = oc[j] >> 4, i = oc[j] & 15, t = W.f0[a];
+      int nb = tnk(D, t, i);
+      int u = nb >> 2;
+      int l = 0, h = m - 1;
+      bool uin = false;
+      while (l <= h) { int mid = (l + h) >> 1; int v = W.f0[mid]; if (v == u) { uin = true; break; } if (v < u) l = mid + 1; else h = mid - 1; }
+      rec = face_lookup(D, k0[j], k1[j], k2[j]);
+      isc = uin && rec >= 0 && A.n > 0 && allowed_face(D, A, k0[j], k1[j], k2[j]);
+      isb = !isc;
+      crf = min(4 * t + i, nb);
+    }
+    unsigned bc = __ballot_sync(FULL, isc), bb = __ballot_sync(FULL, isb);
+    const unsigned below = (1u << lane) - 1u;
+    if (isc) { int k = ncr + __popc(bc & below); if (k < O.ccon) { O.cr[k] = rec; O.crf[k] = crf; } }
+    if (isb) { int k = nbs + __popc(bb & below); if (k < O.ccon) O.bsub[k] = rec; }
+    ncr += __popc(bc); nbs += __popc(bb);
+  }
+  if (ncr > O.ccon || nbs > O.ccon) st = RS_OVERFLOW;
+  // subsegments: boundary iff an edge of the boundary faces met so far
+  int nbg = 0, neg = 0;
+  for (int j0 = 0; j0 < K && st == RS_OK; ++j0) {
+    if (!ofirst[j0] || (oc[j0] & 15) < 4) continue;
+    const int a = oc[j0] >> 4, x = k0[j0], y = k1[j0];
+    const int fend = a + 1 < m ? W.f1[a + 1] : nbf;   // boundary faces of sorted tets 0..a
+    bool hit = false;
+    for (int k = lane; k < fend && !hit; k += 32) {
+      int t = O.bf[k] >> 2, i = O.bf[k] & 3;
+      int f[3]; face_verts(D.tv[t], i, f);
+      bool hx = f[0] == x || f[1] == x || f[2] == x, hy = f[0] == y || f[1] == y || f[2] == y;
+      hit = hx && hy;
+    }
+    const bool bound = __any_sync(FULL, hit);
+    if (nbg + neg >= O.ccon) { st = RS_OVERFLOW; break; }
+    if (lane == 0) {
+      int rec = seg_lookup(D, x, y);
+      if (bound) O.bseg[nbg] = rec; else O.eseg[neg] = rec;
+    }
+    if (bound) ++nbg; else ++neg;
+  }
+  O.ncr = ncr; O.nbsub = nbs; O.nbseg = nbg; O.neseg = neg;
+  __syncwarp();
   WMARK(60);
   return st;
 }
