@@ -19,6 +19,8 @@
 // on the device.
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 #include <algorithm>
 #include <array>
@@ -728,6 +730,84 @@ __global__ void k_reject(Dev D, Cand C, Owners W, int n, int* undecided) {
     for_claims(D, C, W, c, [&](int k) { if (W.own[k] == -1) hit = true; });
     if (hit) C.state[c] = 2;
     else atomicAdd(undecided, 1);
+  }
+}
+// The same iterations as one persistent cooperative kernel: a warp per
+// candidate walks its claim keys lane-parallel (contiguous slab reads), the five
+// passes of an iteration are separated by grid-wide barriers, and the loop ends
+// on the device when nothing is undecided -- no launches or host syncs per
+// iteration.  States: 0 undecided, 1 accepted, 2 rejected, 4 rejected in the
+// current iteration (claims still to release), 10+it accepted in iteration it.
+template <class F>
+__device__ __forceinline__ void warp_claims(const Dev& D, const Cand& C, const Owners& W, int c, int lane, F f) {
+  SlabView v = slab(C, c);
+  const int nt = C.ntet[c], nb = C.nbf[c], ncr = C.ncr[c], nbs = C.nbseg[c], nes = C.neseg[c];
+  const int ex = C.extra[c];
+  const int e1 = nt, e2 = e1 + nb, e3 = e2 + ncr, e4 = e3 + nbs, e5 = e4 + nes, tot = e5 + (ex >= 0);
+  for (int j = lane; j < tot; j += 32) {
+    int key;
+    if (j < e1) key = W.toff + v.tets[j];
+    else if (j < e2) { int b = v.bf[j - e1]; key = W.foff + min(b, tnk(D, b >> 2, b & 3)); }
+    else if (j < e3) key = W.foff + v.crf[j - e2];
+    else if (j < e4) { int r = v.bseg[j - e3]; if (r < 0) continue; key = W.soff + r; }
+    else if (j < e5) { int r = v.eseg[j - e4]; if (r < 0) continue; key = W.soff + r; }
+    else key = (C.kind[c] == K_SEG ? W.soff : W.foff) + ex;
+    f(key);
+  }
+}
+__global__ void __launch_bounds__(256) k_filter_coop(Dev D, Cand C, Owners W, int n, int* ctr) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const unsigned FULL = 0xffffffffu;
+  for (int it = 0;; ++it) {
+    if (gw == 0 && lane == 0) ctr[(it + 1) % 3] = 0;
+    for (int c = gw; c < n; c += nw) {                       // claim
+      if (C.state[c] != 0) continue;
+      const int r = C.rank[c];
+      warp_claims(D, C, W, c, lane, [&](int k) { atomicMin(W.own + k, r); });
+    }
+    grid.sync();
+    for (int c = gw; c < n; c += nw) {                       // decide
+      if (C.state[c] != 0) continue;
+      const int r = C.rank[c];
+      bool win = true;
+      warp_claims(D, C, W, c, lane, [&](int k) { if (W.own[k] != r) win = false; });
+      win = __all_sync(FULL, win);
+      if (win && lane == 0) C.state[c] = 10 + it;
+    }
+    grid.sync();
+    for (int c = gw; c < n; c += nw) {                       // mark
+      if (C.state[c] != 10 + it) continue;
+      warp_claims(D, C, W, c, lane, [&](int k) { W.own[k] = -1; });
+      __syncwarp();
+      if (lane == 0) C.state[c] = 1;
+    }
+    grid.sync();
+    int und = 0;
+    for (int c = gw; c < n; c += nw) {                       // reject
+      if (C.state[c] != 0) continue;
+      bool hit = false;
+      warp_claims(D, C, W, c, lane, [&](int k) { if (W.own[k] == -1) hit = true; });
+      hit = __any_sync(FULL, hit);
+      if (lane == 0) { if (hit) C.state[c] = 4; else ++und; }
+    }
+    if (lane == 0 && und) atomicAdd(ctr + it % 3, und);
+    grid.sync();
+    for (int c = gw; c < n; c += nw) {                       // release the claims of losers
+      const int st = C.state[c];
+      if (st != 0 && st != 4) continue;
+      warp_claims(D, C, W, c, lane, [&](int k) { if (W.own[k] >= 0) W.own[k] = INT_MAX; });
+      __syncwarp();
+      if (st == 4 && lane == 0) C.state[c] = 2;
+    }
+    grid.sync();
+    if (*(volatile int*)(ctr + it % 3) == 0) break;
+  }
+  for (int c = gw; c < n; c += nw) {                         // clear all owner slots touched
+    const int st = C.state[c];
+    if (st < 0 || st == 3) continue;
+    warp_claims(D, C, W, c, lane, [&](int k) { W.own[k] = INT_MAX; });
   }
 }
 __global__ void k_strict_state(Cand C, int n) {
@@ -2217,7 +2297,23 @@ static void rank_candidates(gq_ctx* c, int n) {
 
 // LFMIS filter over candidates [0,n): state 0 for ok ones, 3 for the rest.
 static void run_filter(gq_ctx* c, int n, int* nacc_out) {
-  // iterations are idempotent once nothing is undecided: check every 3rd
+  if (n <= 0) return;
+  if (!getenv("GQ_FILTER_LAUNCHES")) {
+    static int blocks_per_sm = 0, nsm = 0;
+    if (!blocks_per_sm) {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_filter_coop, 256, 0));
+      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+      if (blocks_per_sm < 1) throw std::runtime_error("filter kernel cannot be resident");
+    }
+    int blocks = std::min(blocks_per_sm * nsm, (n + 7) / 8);
+    int* ctr = c->d_int + 48;
+    CK(cudaMemsetAsync(ctr, 0, 12, c->st));
+    void* args[] = {&c->D, &c->C, &c->W, &n, &ctr};
+    CK(cudaLaunchCooperativeKernel((void*)k_filter_coop, dim3(std::max(blocks, 1)), dim3(256), args, 0, c->st));
+    c->launches++;
+    return;
+  }
+  // debug path: one launch per pass, iterations are idempotent once nothing is undecided: check every 3rd
   for (int it = 0;; ++it) {
     CK(cudaMemsetAsync(c->d_int, 0, 4, c->st));
     LAUNCH(k_claim, n, c->D, c->C, c->W, n);
