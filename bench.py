@@ -227,6 +227,15 @@ def main():
         peaks = _peaks()
         peak = float(peaks.get("hbm_gbs", 6650.0))
         achieved = (region_bytes / (region_ms / 1000.0) / 1e9) if region_ms > 0 else 0.0
+        traffic, traffic_note = None, None
+        try:   # dram bytes of one captured region launch (ncu --set full), committed under profiles/
+            with open(os.path.join(ROOT, "profiles", "region_traffic.json")) as f:
+                tr = json.load(f)
+            traffic = tr["dram_bytes"]
+            traffic_note = (f"{tr['kernel']} launch {tr['launch']} of a C2 refine: dram read+write {tr['dram_bytes']} B "
+                            f"vs {tr['bytes_alg']} algorithmic B in {tr['duration_ms']} ms ({tr['source']})")
+        except Exception:
+            pass
         line = {
             "metric": "steiner_points_per_second", "value": tot_steiner / t_dev, "unit": "steiner_points/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -241,8 +250,8 @@ def main():
                     "d2h_bytes_per_step": int(d2h), "s_per_refine": e2e_wall / args.steps},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if peak else None, "traffic": None,
-                         "kernel": "k_region (Delaunay region growth/peel/finish)",
+                         "frac": achieved / peak if peak else None, "traffic": traffic, "traffic_note": traffic_note,
+                         "kernel": "k_region_warp + k_init_region_warp (Delaunay regions; all launches, CUDA events)",
                          "peak_source": "measured" if not peaks.get("_fallback") else "fallback"},
             "clocks": clk.summary(),
         }

@@ -1347,6 +1347,76 @@ __global__ void k_init_unclaim(Dev D, Cand C, Owners W, const int* plist, int nw
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x)
     for_claims(D, C, W, plist[w], [&](int k) { W.own[k] = INT_MAX; });
 }
+// The window filter, tet-id assignment and cavity removal of one bulk round as
+// one cooperative kernel: a warp per window point walks its claims
+// lane-parallel; block 0 scans acceptance and boundary-face counts between the
+// barriers; totals go to tot[0] (accepted) and tot[1] (new tets).
+__global__ void __launch_bounds__(256) k_init_filter_coop(Dev D, Cand C, Owners W, const int* plist, int nw, int nt,
+                                                          int* acc, int* accscan, int* nbfscan, int* tot, int* succ) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
+  const unsigned FULL = 0xffffffffu;
+  for (int w = gw; w < nw; w += nwarp) {                    // claim: lowest order wins
+    const int c = plist[w];
+    warp_claims(D, C, W, c, lane, [&](int k) { atomicMin(W.own + k, c); });
+  }
+  grid.sync();
+  for (int w = gw; w < nw; w += nwarp) {                    // decide
+    const int c = plist[w];
+    bool win = true;
+    warp_claims(D, C, W, c, lane, [&](int k) { if (W.own[k] != c) win = false; });
+    win = __all_sync(FULL, win);
+    if (lane == 0) acc[w] = win;
+  }
+  grid.sync();
+  for (int w = gw; w < nw; w += nwarp)                      // release
+    warp_claims(D, C, W, plist[w], lane, [&](int k) { W.own[k] = INT_MAX; });
+  if (blockIdx.x == 0) {                                    // scans in insertion order
+    typedef cub::BlockScan<int, 256> BS;
+    __shared__ typename BS::TempStorage ts;
+    __shared__ int carry[2];
+    if (threadIdx.x == 0) carry[0] = carry[1] = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < nw; b0 += 256) {
+      const int w = b0 + threadIdx.x;
+      const int a = w < nw ? acc[w] : 0;
+      const int f = a ? C.nbf[plist[w]] : 0;
+      int sa, sf, ta, tf;
+      BS(ts).ExclusiveSum(a, sa, ta);
+      __syncthreads();
+      BS(ts).ExclusiveSum(f, sf, tf);
+      if (w < nw) { accscan[w] = carry[0] + sa; nbfscan[w] = carry[1] + sf; }
+      __syncthreads();
+      if (threadIdx.x == 0) { carry[0] += ta; carry[1] += tf; }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      tot[0] = carry[0]; tot[1] = carry[1];
+      if (nt + carry[1] > D.tcap) raise_err(GQ_ERR_CAP);
+    }
+  }
+  grid.sync();
+  for (int w = gw; w < nw; w += nwarp) {                    // new tet ids, cavities die
+    if (!acc[w]) continue;
+    const int c = plist[w];
+    const int nt0 = nt + nbfscan[w];
+    if (nt0 + C.nbf[c] > D.tcap) continue;
+    if (lane == 0) {
+      C.nt0[c] = nt0;
+      if (C.mind[c] <= D.too_close_sq) raise_err(GQ_ERR_DEGEN);
+    }
+    SlabView v = slab(C, c);
+    for (int j = lane; j < C.ntet[c]; j += 32) { D.alive[v.tets[j]] = 0; succ[v.tets[j]] = nt0; }
+  }
+}
+// pending list minus the accepted window points (order kept)
+__global__ void k_init_compact2(const int* plist, const int* acc, const int* accscan, int nw, int ntot, int nacc, int* out) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < ntot; w += gridDim.x * blockDim.x) {
+    if (w < nw && acc[w]) continue;
+    out[w < nw ? w - accscan[w] : w - nacc] = plist[w];
+  }
+}
 // accepted window points: new tet ids (scan of nbf in insertion order)
 __global__ void k_init_nbf(Cand C, const int* plist, const int* acc, int nw, int* nbfv) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x)
@@ -2236,6 +2306,18 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
     LAUNCH_S(k_region, n1 - n0, c->D, c->C, c->S, n0, n1, (const int*)nullptr, probe, 0);
   }
   region_end(c);
+  if (g_trace) {   // per-launch algorithmic bytes for matching an ncu capture
+    static long long launch_no = 0;
+    static unsigned long long t_last = 0, r_last = 0;
+    sync(c);
+    unsigned long long rc = 0, tested = 0;
+    CK(cudaMemcpyFromSymbol(&rc, g_region_calls, 8));
+    CK(cudaMemcpyFromSymbol(&tested, g_tested, 8));
+    float ms = 0; cudaEventElapsedTime(&ms, c->er0, c->er1);
+    std::fprintf(stderr, "[region] launch %lld cands %d bytes_alg %llu ms %.3f\n", launch_no++, n1 - n0,
+                 58ull * (tested - t_last) + 24ull * (rc - r_last), ms);
+    t_last = tested; r_last = rc;
+  }
   fine(c, 24);
   // overflow pass
   ensure_tmp(c, n1 + 1);
@@ -2550,26 +2632,46 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
       }
     }
     fine(c, 1);
-    LAUNCH(k_init_claim, W, c->D, C, c->W, d_plist, W);
-    LAUNCH(k_init_decide, W, c->D, C, c->W, d_plist, W, d_acc);
-    LAUNCH(k_init_unclaim, W, c->D, C, c->W, d_plist, W);
-    fine(c, 2);
-    LAUNCH(k_init_nbf, W, C, d_plist, d_acc, W, d_keep);
-    exclusive_scan(c, d_keep, d_scan, W);
-    int lastn = 0, lasts = 0, lasta = 0;
-    CK(cudaMemcpyAsync(&lastn, d_keep + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(&lasts, d_scan + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
-    // number accepted
-    exclusive_scan(c, d_acc, d_plist2, W);
-    int lastacc_scan = 0;
-    CK(cudaMemcpyAsync(&lastacc_scan, d_plist2 + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(&lasta, d_acc + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
-    sync(c);
-    int nacc = lastacc_scan + lasta;
-    int add_t = lasts + lastn;
-    if (nt + add_t > c->D.tcap) throw std::runtime_error("tet capacity exceeded in init");
-    fine(c, 3);
-    LAUNCH(k_init_kill, W, c->D, C, d_plist, d_acc, d_scan, W, nt, d_succ);
+    int nacc = 0, add_t = 0;
+    if (!getenv("GQ_INIT_LAUNCHES")) {
+      static int bps = 0, nsm = 0;
+      if (!bps) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_init_filter_coop, 256, 0));
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+        if (bps < 1) throw std::runtime_error("init filter kernel cannot be resident");
+      }
+      int blocks = std::max(1, std::min(bps * nsm, (W + 7) / 8));
+      int* tot = c->d_int + 52;
+      void* args[] = {&c->D, &C, &c->W, &d_plist, &W, &nt, &d_acc, &d_plist2, &d_scan, &tot, &d_succ};
+      CK(cudaLaunchCooperativeKernel((void*)k_init_filter_coop, dim3(blocks), dim3(256), args, 0, c->st));
+      c->launches++;
+      int h2[2];
+      CK(cudaMemcpyAsync(h2, tot, 8, cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+      nacc = h2[0]; add_t = h2[1];
+      if (nt + add_t > c->D.tcap) throw std::runtime_error("tet capacity exceeded in init");
+      fine(c, 3);
+    } else {   // debug path: one launch per pass
+      LAUNCH(k_init_claim, W, c->D, C, c->W, d_plist, W);
+      LAUNCH(k_init_decide, W, c->D, C, c->W, d_plist, W, d_acc);
+      LAUNCH(k_init_unclaim, W, c->D, C, c->W, d_plist, W);
+      fine(c, 2);
+      LAUNCH(k_init_nbf, W, C, d_plist, d_acc, W, d_keep);
+      exclusive_scan(c, d_keep, d_scan, W);
+      int lastn = 0, lasts = 0, lasta = 0;
+      CK(cudaMemcpyAsync(&lastn, d_keep + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(&lasts, d_scan + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
+      exclusive_scan(c, d_acc, d_plist2, W);
+      int lastacc_scan = 0;
+      CK(cudaMemcpyAsync(&lastacc_scan, d_plist2 + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(&lasta, d_acc + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+      nacc = lastacc_scan + lasta;
+      add_t = lasts + lastn;
+      if (nt + add_t > c->D.tcap) throw std::runtime_error("tet capacity exceeded in init");
+      fine(c, 3);
+      LAUNCH(k_init_kill, W, c->D, C, d_plist, d_acc, d_scan, W, nt, d_succ);
+    }
     fine(c, 4);
     {
       int blocks = std::max(1, std::min((W + WS_WARPS - 1) / WS_WARPS, c->SB.nthreads / WS_WARPS));
@@ -2581,10 +2683,11 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     LAUNCH(k_init_cellmark, W, c->D, H, d_pend, d_plist, d_acc, W);
     nt += add_t;
     // release big slabs (big regions are recomputed next round if still pending)
-    LAUNCH(k_init_keep, W, d_acc, W, d_keep);
-    exclusive_scan(c, d_keep, d_scan, W);
-    LAUNCH(k_init_compact, left, d_plist, d_acc, d_scan, W, left, d_plist2);
-    std::swap(d_plist, d_plist2);
+    {
+      int* d_out = d_keep;   // the acceptance scan lives in d_plist2 (accscan)
+      LAUNCH(k_init_compact2, left, d_plist, d_acc, d_plist2, W, left, nacc, d_out);
+      std::swap(d_plist, d_keep);
+    }
     if (!bl.empty()) LAUNCH(k_release_big, bl.size(), C, c->tmpC, (int)bl.size());
     if (g_trace) {
       sync(c);
