@@ -343,14 +343,29 @@ __global__ void k_init_cellmark(Dev D, CellHint H, const int* pend, const int* p
 }
 // one warp per candidate (the common case); overflowing cavities are marked
 // CS_OVF for the block kernel
-__global__ void __launch_bounds__(32 * WR_WARPS) k_region_warp(Dev D, Cand C, Scr SC, int n0, int n1) {
+// tiers of the warp region kernel.  Measured on C2: a 128-tet tier at 16 warps
+// / SM plus the 512-tet tier for its overflows is no faster than the 512-tet
+// tier alone (the 4% large cavities cost what the occupancy gains), so both
+// tiers are the large one and the second pass is skipped.
+#define WT1_MAXT 512
+#define WT1_HASH 2048
+#define WT1_MINB 1
+#define WT2_MAXT 512
+#define WT2_HASH 2048
+typedef WarpSharedT<WT1_MAXT, WT1_HASH> WarpShared1;
+typedef WarpSharedT<WT2_MAXT, WT2_HASH> WarpShared2;
+// candidates [n0,n1) (list == nullptr) or list[n0..n1) (the small tier's overflows)
+template <int MAXT, int HASH, int MINB>
+__global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_region_warp(Dev D, Cand C, Scr SC, int n0, int n1, const int* list) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  typedef WarpSharedT<MAXT, HASH> WS;
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpShared& W = reinterpret_cast<WarpShared*>(smem_raw)[wib];
+  WS& W = reinterpret_cast<WS*>(smem_raw)[wib];
   const int gw = blockIdx.x * WR_WARPS + wib, nw = gridDim.x * WR_WARPS;
   Scratch S = scratch_for(SC, gw);
-  for (int c = n0 + gw; c < n1; c += nw) {
-    if (C.status[c] != CS_OK) continue;
+  for (int k = n0 + gw; k < n1; k += nw) {
+    const int c = list ? list[k] : k;
+    if (C.status[c] != (list ? CS_OVF : CS_OK)) continue;
     DCHK(C.bigi[c] == -1);
     if (lane == 0) W.nseeds = cand_seeds(D, C, c, W.seeds, S);
     __syncwarp();
@@ -372,13 +387,16 @@ __global__ void __launch_bounds__(32 * WR_WARPS) k_region_warp(Dev D, Cand C, Sc
     __syncwarp();
   }
 }
-// bulk construction, warp per pending point (cached cavities re-validated)
-__global__ void __launch_bounds__(32 * WR_WARPS) k_init_region_warp(Dev D, Cand C, Scr SC, const int* pend, const int* plist,
+// bulk construction, warp per pending point (cached cavities re-validated);
+// redo_ovf: the large tier, run on the small tier's overflows
+template <int MAXT, int HASH, int MINB>
+__global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_init_region_warp(Dev D, Cand C, Scr SC, const int* pend, const int* plist,
                                                                     int Wn, int* hint, const int* succ, const int* touched, int round,
-                                                                    CellHint H) {
+                                                                    CellHint H, int redo_ovf) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  typedef WarpSharedT<MAXT, HASH> WS;
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpShared& W = reinterpret_cast<WarpShared*>(smem_raw)[wib];
+  WS& W = reinterpret_cast<WS*>(smem_raw)[wib];
   const int gw = blockIdx.x * WR_WARPS + wib, nw = gridDim.x * WR_WARPS;
   Scratch S = scratch_for(SC, gw);
   for (int w = gw; w < Wn; w += nw) {
@@ -386,7 +404,7 @@ __global__ void __launch_bounds__(32 * WR_WARPS) k_init_region_warp(Dev D, Cand 
     if (lane == 0 && g_wdbg) { g_wdbg[2 * gw] = c; g_wdbg[2 * gw + 1] = 0; }
     DCHK(c >= 0 && c < C.cap);
     int st0 = C.status[c];
-    if (st0 == CS_OVF) continue;
+    if ((st0 == CS_OVF) != (redo_ovf != 0)) continue;
     if (st0 == CS_OK && C.memb[c] >= 0) {
       SlabView v = slab(C, c);
       bool bad = false;
@@ -2292,16 +2310,20 @@ static void resolve_events(gq_ctx* c) {
   }
   c->rpairs.clear(); c->fev.clear(); c->evused = 0;
 }
+template <class K>
+static void launch_warp_regions(gq_ctx* c, K kern, size_t shm, int nwork, int n0, int n1, const int* list) {
+  int blocks = (int)std::min<long long>(((long long)nwork + WR_WARPS - 1) / WR_WARPS, c->S.nthreads / WR_WARPS);
+  kern<<<std::max(blocks, 1), 32 * WR_WARPS, shm, c->st>>>(c->D, c->C, c->S, n0, n1, list);
+  c->launches++;
+  CK(cudaGetLastError());
+}
 static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   if (n1 <= n0) return;
   fine(c, 31);
   region_begin(c);
   if (!getenv("GQ_THREAD_REGIONS")) {   // debug switch: per-thread kernel
-    long long nw = n1 - n0;
-    int blocks = (int)std::min<long long>((nw + WR_WARPS - 1) / WR_WARPS, c->S.nthreads / WR_WARPS);
-    k_region_warp<<<std::max(blocks, 1), 32 * WR_WARPS, WR_WARPS * sizeof(WarpShared), c->st>>>(c->D, c->C, c->S, n0, n1);
-    c->launches++;
-    CK(cudaGetLastError());
+    launch_warp_regions(c, k_region_warp<WT1_MAXT, WT1_HASH, WT1_MINB>, WR_WARPS * sizeof(WarpShared1), n1 - n0, n0, n1,
+                        (const int*)nullptr);
   } else {
     LAUNCH_S(k_region, n1 - n0, c->D, c->C, c->S, n0, n1, (const int*)nullptr, probe, 0);
   }
@@ -2319,13 +2341,27 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
     t_last = tested; r_last = rc;
   }
   fine(c, 24);
-  // overflow pass
+  // overflow passes: the large warp tier, then one block per cavity
   ensure_tmp(c, n1 + 1);
   std::vector<int> hs(n1 - n0);
   CK(cudaMemcpyAsync(hs.data(), c->C.status + n0, sizeof(int) * (n1 - n0), cudaMemcpyDeviceToHost, c->st));
   sync(c);
+  std::vector<int> ovf;
+  for (int k = 0; k < n1 - n0; ++k) if (hs[k] == CS_OVF) ovf.push_back(n0 + k);
   std::vector<int> big;
-  for (int k = 0; k < n1 - n0; ++k) if (hs[k] == CS_OVF) big.push_back(n0 + k);
+  if (!ovf.empty() && WT1_MAXT != WT2_MAXT && !getenv("GQ_THREAD_REGIONS")) {
+    int no = (int)ovf.size();
+    CK(cudaMemcpyAsync(c->tmpB, ovf.data(), sizeof(int) * no, cudaMemcpyHostToDevice, c->st));
+    region_begin(c);
+    launch_warp_regions(c, k_region_warp<WT2_MAXT, WT2_HASH, 1>, WR_WARPS * sizeof(WarpShared2), no, 0, no, c->tmpB);
+    region_end(c);
+    LAUNCH(k_gather_status, no, c->C, c->tmpB, no, c->tmpA);
+    CK(cudaMemcpyAsync(hs.data(), c->tmpA, sizeof(int) * no, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    for (int k = 0; k < no; ++k) if (hs[k] == CS_OVF) big.push_back(ovf[k]);
+  } else {
+    big.swap(ovf);
+  }
   fine(c, 25);
   if (!big.empty()) {
     int nb = (int)big.size();
@@ -2572,8 +2608,8 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
         CK(cudaMemcpyToSymbol(g_wdbg, &dptr, sizeof(dptr)));
       }
       if (h_wdbg) std::memset(h_wdbg, 0xff, 200000 * sizeof(int));
-      k_init_region_warp<<<std::max(blocks, 1), 32 * WR_WARPS, WR_WARPS * sizeof(WarpShared), c->st>>>(
-          c->D, C, c->S, d_pend, d_plist, W, d_hint, d_succ, d_touched, round, H);
+      k_init_region_warp<WT1_MAXT, WT1_HASH, WT1_MINB><<<std::max(blocks, 1), 32 * WR_WARPS, WR_WARPS * sizeof(WarpShared1), c->st>>>(
+          c->D, C, c->S, d_pend, d_plist, W, d_hint, d_succ, d_touched, round, H, 0);
       c->launches++;
       CK(cudaGetLastError());
       if (h_wdbg) {
@@ -2610,8 +2646,25 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
         CK(cudaMemcpyAsync(sw.data(), d_scan, 4 * (size_t)W, cudaMemcpyDeviceToHost, c->st));
         sync(c);
         for (int w = 0; w < W; ++w) if (sw[w] == CS_OVF) bl.push_back(pl[w]);
+        if (WT1_MAXT != WT2_MAXT && !getenv("GQ_THREAD_INIT")) {   // the large warp tier first
+          int no = (int)bl.size();
+          CK(cudaMemcpyAsync(d_keep, bl.data(), 4 * (size_t)no, cudaMemcpyHostToDevice, c->st));
+          int blocks = std::min((no + WR_WARPS - 1) / WR_WARPS, c->S.nthreads / WR_WARPS);
+          k_init_region_warp<WT2_MAXT, WT2_HASH, 1><<<std::max(blocks, 1), 32 * WR_WARPS, WR_WARPS * sizeof(WarpShared2), c->st>>>(
+              c->D, C, c->S, d_pend, d_keep, no, d_hint, d_succ, d_touched, round, H, 1);
+          c->launches++;
+          CK(cudaGetLastError());
+          LAUNCH(k_gather_status, no, C, d_keep, no, d_scan);
+          std::vector<int> s2(no);
+          CK(cudaMemcpyAsync(s2.data(), d_scan, 4 * (size_t)no, cudaMemcpyDeviceToHost, c->st));
+          sync(c);
+          std::vector<int> rest;
+          for (int k = 0; k < no; ++k) if (s2[k] == CS_OVF) rest.push_back(bl[k]);
+          bl.swap(rest);
+        }
         int nb = (int)std::min<size_t>(bl.size(), 4096);
         bl.resize(nb);
+        if (nb > 0) {
         ensure_big(c, nb);
         ensure_tmp(c, nb + 1);
         std::vector<int> bis(nb);
@@ -2629,6 +2682,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
         for (int w = 0; w < W; ++w) if (sw[w] == CS_OVF) { W = w; break; }
         if (W == 0) throw std::runtime_error("init: cavity overflow");
         CK(cudaMemcpyAsync(c->tmpC, bl.data(), 4 * (size_t)nb, cudaMemcpyHostToDevice, c->st));
+        }
       }
     }
     fine(c, 1);
@@ -3214,10 +3268,14 @@ int gq_create(int device, gq_ctx** out) {
     CK(cudaEventCreate(&c->er0)); CK(cudaEventCreate(&c->er1));
     CK(cudaDeviceSetLimit(cudaLimitStackSize, 16384));
     CK(cudaFuncSetAttribute(k_region_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BlockShared)));
-    CK(cudaFuncSetAttribute(k_region_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared))));
+    CK(cudaFuncSetAttribute(k_region_warp<WT1_MAXT, WT1_HASH, WT1_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared1))));
+    if (WT1_MAXT != WT2_MAXT)
+      CK(cudaFuncSetAttribute(k_region_warp<WT2_MAXT, WT2_HASH, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared2))));
     CK(cudaFuncSetAttribute(k_star_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WS_WARPS * sizeof(StarShared))));
     CK(cudaFuncSetAttribute(k_init_stars_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WS_WARPS * sizeof(StarShared))));
-    CK(cudaFuncSetAttribute(k_init_region_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared))));
+    CK(cudaFuncSetAttribute(k_init_region_warp<WT1_MAXT, WT1_HASH, WT1_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared1))));
+    if (WT1_MAXT != WT2_MAXT)
+      CK(cudaFuncSetAttribute(k_init_region_warp<WT2_MAXT, WT2_HASH, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared2))));
     CK(cudaFuncSetAttribute(k_init_region_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BlockShared)));
   } catch (std::exception& e) {
     c->err = e.what();

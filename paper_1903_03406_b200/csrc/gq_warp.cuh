@@ -27,31 +27,36 @@ __device__ volatile int* g_wdbg;      // pinned host mirror: [warp][2] = candida
 #define WMARK(k) do {} while (0)
 #endif
 #define WSTOP(k) do { if (g_wstop == (k)) return RS_CNSS; } while (0)
-#define WR_MAXT 512
 #ifndef CC_DBG
 #define CC_DBG 96
 #endif
-#define WR_HASH 2048
 #define WR_WARPS 8          // warps per block
 
-struct WarpShared {
-  int hkey[WR_HASH];
-  int hval[WR_HASH];
-  int cav[WR_MAXT];
-  int f0[WR_MAXT];
-  int f1[WR_MAXT];
-  int comp[WR_MAXT];
-  unsigned char in[WR_MAXT];
+// Two instantiations: a small tier (128 tets, 6.5 KB per warp) that runs at
+// 16 warps / SM for the common cavities, and a large tier (512 tets, 25 KB per
+// warp) for the few percent that overflow the small one.
+template <int MAXT, int HASH>
+struct WarpSharedT {
+  int hkey[HASH];
+  int hval[HASH];
+  int cav[MAXT];
+  int f0[MAXT];
+  int f1[MAXT];
+  int comp[MAXT];
+  unsigned char in[MAXT];
   int n, nf, cnt, flag, memb, seed;
   unsigned long long mind;
   int seeds[32];
   int nseeds;
 };
 
-__device__ __forceinline__ unsigned int wh(int k) { return ((unsigned int)k * 2654435761u) & (WR_HASH - 1); }
-__device__ inline int wh_claim(WarpShared& W, int k) {
-  unsigned int i = wh(k);
-  for (int p = 0; p < WR_HASH; ++p) {
+template <int HASH>
+__device__ __forceinline__ unsigned int wh(int k) { return ((unsigned int)k * 2654435761u) & (HASH - 1); }
+template <class WS>
+__device__ inline int wh_claim(WS& W, int k) {
+  constexpr int HASH = sizeof(W.hkey) / sizeof(int);
+  unsigned int i = wh<HASH>(k);
+  for (int p = 0; p < HASH; ++p) {
     int cur = W.hkey[i];
     if (cur == k) return -1;
     if (cur == INT_MIN) {
@@ -59,25 +64,29 @@ __device__ inline int wh_claim(WarpShared& W, int k) {
       if (old == INT_MIN) return (int)i;
       if (old == k) return -1;
     }
-    i = (i + 1) & (WR_HASH - 1);
+    i = (i + 1) & (HASH - 1);
   }
   return -2;
 }
-__device__ inline int wh_find(const WarpShared& W, int k) {
-  unsigned int i = wh(k);
-  for (int p = 0; p < WR_HASH; ++p) {
+template <class WS>
+__device__ inline int wh_find(const WS& W, int k) {
+  constexpr int HASH = sizeof(W.hkey) / sizeof(int);
+  unsigned int i = wh<HASH>(k);
+  for (int p = 0; p < HASH; ++p) {
     int cur = W.hkey[i];
     if (cur == k) return W.hval[i];
     if (cur == INT_MIN) return -1;
-    i = (i + 1) & (WR_HASH - 1);
+    i = (i + 1) & (HASH - 1);
   }
   return -1;
 }
 
 // All 32 lanes of the warp call this with the same arguments.  S is the
 // warp's global scratch (lane 0 only: walks and the constraint pass).
+template <int MAXT, int HASH>
 __device__ inline int region_warp(const Dev& D, const double* p, const int* seeds, int nseeds, const Allow& A,
-                                  WarpShared& W, Scratch& S, RegionOut& O, bool walk_on_miss = true) {
+                                  WarpSharedT<MAXT, HASH>& W, Scratch& S, RegionOut& O, bool walk_on_miss = true) {
+  constexpr int WR_MAXT = MAXT, WR_HASH = HASH;
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
   for (int i = lane; i < WR_HASH; i += 32) W.hkey[i] = INT_MIN;
