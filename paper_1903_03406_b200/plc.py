@@ -203,9 +203,32 @@ def _overlapping_pairs(boxes):
         active.append(k)
 
 
-def validate(plc: PLC) -> list:
+FAST_MIN_FEATURES = 2000   # below this the exact path is fast enough
+
+
+def _exact_pair(plc: PLC, u: int, v: int) -> bool:
+    """The exact pair test of the final validate loop (features numbered
+    segments first, then polygons)."""
+    nseg = len(plc.segments)
+    if v < nseg:
+        (i, j), (k, l) = plc.segments[u], plc.segments[v]
+        return _segs_conflict(plc.points[i], plc.points[j], plc.points[k], plc.points[l])
+    if u < nseg:
+        return _seg_poly_conflict(plc.points, plc.segments[u], plc.polygons[v - nseg])
+    return False
+
+
+def validate(plc: PLC, fast: bool = None) -> list:
     """Every invariant violation as (code, detail); [] means valid.
-    Same checks and codes as plc.py:267-383."""
+    Same checks and codes as plc.py:267-383.  Large inputs are first offered
+    to the vectorised certifier (setup_fast.py); anything it cannot certify
+    valid goes through the exact path below."""
+    if fast is None:
+        fast = len(plc.segments) + len(plc.polygons) >= FAST_MIN_FEATURES
+    if fast and plc.points:
+        from .setup_fast import certify_valid
+        if certify_valid(plc, lambda u, v: _exact_pair(plc, u, v)):
+            return []
     out = []
     npts = len(plc.points)
     first = {}
@@ -316,6 +339,9 @@ def hull_covered(plc: PLC) -> bool:
         hull = ConvexHull(np.asarray(plc.points))
     except QhullError:
         return False
+    from .setup_fast import certify_hull_covered
+    if certify_hull_covered(plc, hull.simplices):
+        return True
     by_vertex = {}
     for pid, poly in enumerate(plc.polygons):
         for v in poly:

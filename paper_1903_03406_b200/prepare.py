@@ -68,9 +68,13 @@ def facet_keep(plc: PLC) -> np.ndarray:
 
     from .plc import _proj_axis
 
-    out = np.zeros((len(plc.polygons), 2), dtype=np.int32)
+    from .setup_fast import facet_axes
+
+    out = facet_axes(plc)          # triangles with a certified normal (vectorised)
     cache = {}
     for pid, poly in enumerate(plc.polygons):
+        if out[pid, 0] >= 0:
+            continue
         pts = [plc.points[v] for v in poly]
         axis = _proj_axis(pts)
         i, j = [k for k in range(3) if k != axis]
