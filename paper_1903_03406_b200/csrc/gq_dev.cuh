@@ -79,6 +79,8 @@ struct Dev {
   int* t2count;        // alive triangles per polygon
   // static PLC info
   int2* poly_keep;     // projection axes per polygon
+  int* t2last;         // per polygon: most recently added real 2D triangle (walk start)
+  uint8_t* poly_obl;   // 1: polygon not parallel to a coordinate plane (in-plane circle test in 3D)
   int* segpoly_off;    // sid -> polygons (CSR)
   int* segpoly;
   int2* sid_uv;        // original segment endpoints
@@ -825,6 +827,16 @@ __device__ inline bool tri_in_region(const Tri2Ctx& C, int tid) {
     if (s != 0) return s > 0;
     return between2d_exact(pa, pb, C.p);
   }
+  if (C.D->poly_obl[C.pid]) {
+    // Oblique polygon: the projection to the kept axes is affine but not a
+    // similarity, so the projected incircle test would build a triangulation
+    // that disagrees with the 3D mesh's subfaces (whose Delaunay property is
+    // the equatorial-ball one) -- the reference breaks down on such facets
+    // (SURVEY F1).  Decide membership by the exact equatorial-ball test of
+    // the 3D points instead; on axis-parallel polygons both tests coincide.
+    const Dev& D = *C.D;
+    return equatorial_cmp_robust(PT(D, t.x), PT(D, t.y), PT(D, t.z), PT(D, C.vid)) < 0;
+  }
   double pc[2];
   C.pos(t.x, pa); C.pos(t.y, pb); C.pos(t.z, pc);
   return incircle2d(pa, pb, pc, C.p) > 0;
@@ -839,6 +851,7 @@ __device__ inline int t2_add(const Dev& D, int a, int b, int c, int pid) {
   if (tid >= D.t2cap) { raise_err(GQ_ERR_CAP); return -1; }
   D.t2v[tid] = make_int4(a, b, c, pid);
   D.t2alive[tid] = 1;
+  if (c != GHOST) D.t2last[pid] = tid;
   ht_put(D.he_hk, D.he_hv, D.he_hmask, keyhe(a, b, pid), tid);
   ht_put(D.he_hk, D.he_hv, D.he_hmask, keyhe(b, c, pid), tid);
   ht_put(D.he_hk, D.he_hv, D.he_hmask, keyhe(c, a, pid), tid);
@@ -858,9 +871,17 @@ __device__ __noinline__ int tri2_cavity(const Tri2Ctx& C, const int* forced, int
   int seed = -1;
   for (int k = 0; k < nseeds && seed < 0; ++k)
     if (seeds[k] >= 0 && D.t2alive[seeds[k]] && D.t2v[seeds[k]].w == C.pid && tri_in_region(C, seeds[k])) seed = seeds[k];
-  if (seed < 0 && nseeds > 0 && seeds[0] >= 0 && D.t2alive[seeds[0]]) {
+  int start = (nseeds > 0 && seeds[0] >= 0 && D.t2alive[seeds[0]]) ? seeds[0] : -1;
+  if (seed < 0 && start < 0 && nforced == 0) {
+    // no hint from the 3D side (the target's triangle was retiled earlier in
+    // the round): walk from the polygon's most recent triangle, like the
+    // reference walks from its last touched triangle (facets.py:107-123)
+    int t = D.t2last[C.pid];
+    if (t >= 0 && D.t2alive[t] && D.t2v[t].w == C.pid) start = t;
+  }
+  if (seed < 0 && start >= 0) {
     // facets.py:107-123: walk toward p
-    int tid = seeds[0];
+    int tid = start;
     int n_alive = D.t2count[C.pid];
     for (int s = 0; s < 4 * n_alive + 16; ++s) {
       int4 t = D.t2v[tid];
@@ -874,6 +895,11 @@ __device__ __noinline__ int tri2_cavity(const Tri2Ctx& C, const int* forced, int
       if (!moved) break;
     }
     if (tri_in_region(C, tid)) seed = tid;
+    if (seed < 0 && nforced == 0) {   // exhaustive fallback (facets.py:121-123)
+      const int nt2 = D.ctr->nt2;
+      for (int t = 0; t < nt2 && seed < 0; ++t)
+        if (D.t2alive[t] && D.t2v[t].w == C.pid && tri_in_region(C, t)) seed = t;
+    }
   }
   int own_seed = seed;
   if (seed >= 0) {
@@ -894,6 +920,10 @@ __device__ __noinline__ int tri2_cavity(const Tri2Ctx& C, const int* forced, int
       }
     }
   } else if (nforced == 0) {
+#ifdef GQ_DEBUG2D
+    printf("[2d] no seed pid %d vid %d nseeds %d seed0 %d alive %d count %d p %.17g %.17g\n", C.pid, C.vid, nseeds,
+           nseeds > 0 ? seeds[0] : -9, nseeds > 0 && seeds[0] >= 0 ? (int)D.t2alive[seeds[0]] : -1, D.t2count[C.pid], C.p[0], C.p[1]);
+#endif
     raise_err(GQ_ERR_2D);
     return -1;
   }
@@ -925,7 +955,12 @@ __device__ __noinline__ int tri2_cavity(const Tri2Ctx& C, const int* forced, int
           }
         }
       }
-      if (n == D.t2count[C.pid]) { raise_err(GQ_ERR_2D); return -1; }
+      if (n == D.t2count[C.pid]) {
+#ifdef GQ_DEBUG2D
+        printf("[2d] consumed pid %d vid %d n %d nforced %d own %d\n", C.pid, C.vid, n, nforced, own_seed);
+#endif
+        raise_err(GQ_ERR_2D); return -1;
+      }
     }
     // component of the seed (facets.py:172-183)
     int s0 = own_seed;

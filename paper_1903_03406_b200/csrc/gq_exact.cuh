@@ -31,7 +31,12 @@ __device__ unsigned int g_err;
 #define GQ_ERR_STAR 16u
 #define GQ_ERR_WALK 32u
 #define GQ_ERR_2D 64u
-__device__ __forceinline__ void raise_err(unsigned int e) { atomicOr(&g_err, e); }
+__device__ __forceinline__ void raise_err_(unsigned int e) { atomicOr(&g_err, e); }
+#ifdef GQ_DEBUG2D
+#define raise_err(e) do { printf("[err] %u at %s:%d\n", (unsigned)(e), __FILE__, __LINE__); raise_err_(e); } while (0)
+#else
+#define raise_err(e) raise_err_(e)
+#endif
 
 // exact-call counters (instrumentation for the roofline / report)
 __device__ unsigned long long g_exact_calls[4];
@@ -559,6 +564,19 @@ __device__ __noinline__ int equatorial_cmp(const double* a, const double* b, con
   if (fabs(f) > 1e-9 * scale) return f > 0 ? 1 : -1;
   // a vertex of the triangle lies exactly on its equatorial sphere
   if (same_point(p, a) || same_point(p, b) || same_point(p, c)) return 0;
+  return equatorial_cmp_exact(a, b, c, p);
+}
+// The same comparison for the in-plane Delaunay test of oblique polygons:
+// sliver triangles (split points along one subsegment) can make the float
+// circumcircle degenerate; the exact evaluation decides them.
+__device__ __noinline__ int equatorial_cmp_robust(const double* a, const double* b, const double* c, const double* p) {
+  if (same_point(p, a) || same_point(p, b) || same_point(p, c)) return 0;
+  Sphere sph;
+  if (circumcircle_tri(a, b, c, sph)) {
+    double f = dist2(p, sph.c) - sph.r2;
+    double scale = dist2(p, sph.c) + sph.r2;
+    if (isfinite(f) && fabs(f) > 1e-9 * scale) return f > 0 ? 1 : -1;
+  }
   return equatorial_cmp_exact(a, b, c, p);
 }
 __device__ inline bool encroaches_face(const double* a, const double* b, const double* c, const double* p) {

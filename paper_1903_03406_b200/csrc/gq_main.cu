@@ -917,6 +917,7 @@ struct T2Items {
   int* cav; int* ncav; int cap;             // per item cavity tids
   int* own;                                 // per 2D triangle owner rank
   int* rem; int* nrem; int rcap;            // removed subface records per item
+  int icap;                                 // items allocated
 };
 
 __device__ __noinline__ void t2_forced(const Dev& D, const Cand& C, int c, int pid, int* forced, int& nf, int cap) {
@@ -964,7 +965,12 @@ __global__ void k_t2_compute(Dev D, Cand C, T2Items T, Scr SC) {
     int ts = t2_seed_of(D, C, c, pid);
     if (ts >= 0) seeds[ns++] = ts;
     int n = tri2_cavity(X, forced, nf, seeds, ns, S.tset, T.cav + (size_t)w * T.cap, S.stack, T.cap);
-    if (n < 0) { raise_err(GQ_ERR_2D); n = 0; }
+    if (n < 0) {
+#ifdef GQ_DEBUG2D
+      printf("[2d] cavity fail pid %d vid %d\n", pid, X.vid);
+#endif
+      raise_err(GQ_ERR_2D); n = 0;
+    }
     T.ncav[w] = n;
   }
 }
@@ -1618,7 +1624,12 @@ __device__ __noinline__ void insert_one(const Dev& D, const Cand& C, int c, Scra
       if (ts >= 0) seeds[ns++] = ts;
       int* cav = T.cav + (size_t)w * T.cap;
       int n = tri2_cavity(X, forced, nf, seeds, ns, S.tset, cav, S.stack, T.cap);
-      if (n < 0) { raise_err(GQ_ERR_2D); n = 0; }
+      if (n < 0) {
+#ifdef GQ_DEBUG2D
+      printf("[2d] cavity fail pid %d vid %d\n", pid, X.vid);
+#endif
+      raise_err(GQ_ERR_2D); n = 0;
+    }
       S.tset.clear();
       for (int a = 0; a < n; ++a) S.tset.put(cav[a], a);
       int* rem = T.rem + (size_t)w * T.rcap;
@@ -2180,6 +2191,15 @@ static void ensure_big(gq_ctx* c, int need) {
   grow(C.bbsub, CCB); grow(C.bbseg, CCB); grow(C.beseg, CCB);
   C.nbigcap = cap;
 }
+// 2D retiling work items (candidate, polygon): grown on demand (facet-heavy rounds)
+static void ensure_items(gq_ctx* c, int n) {
+  if (n <= c->T.icap) return;
+  int icap = std::max(n, 2 * c->T.icap);
+  for (int** q : {&c->T.cand, &c->T.pid, &c->T.state, &c->T.ncav, &c->T.nrem}) { dfree(*q); *q = dmalloc<int>(icap); }
+  dfree(c->T.cav); c->T.cav = dmalloc<int>((size_t)icap * c->T.cap);
+  dfree(c->T.rem); c->T.rem = dmalloc<int>((size_t)icap * c->T.rcap);
+  c->T.icap = icap;
+}
 static unsigned int pow2_at_least(size_t n) { unsigned int p = 1024; while (p < n) p <<= 1; return p; }
 
 static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
@@ -2216,6 +2236,9 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   D.t2count = dmalloc<int>(std::max(f, 1));
   CK(cudaMemset(D.t2count, 0, std::max(f, 1) * 4));
   D.poly_keep = dmalloc<int2>(std::max(f, 1));
+  D.poly_obl = dmalloc<uint8_t>(std::max(f, 1));
+  D.t2last = dmalloc<int>(std::max(f, 1));
+  CK(cudaMemset(D.t2last, 0xff, 4 * (size_t)std::max(f, 1)));
   D.segpoly_off = dmalloc<int>(m + 1);
   D.segpoly = dmalloc<int>(std::max(npidx, 1));
   D.sid_uv = dmalloc<int2>(std::max(m, 1));
@@ -2228,10 +2251,9 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   CK(cudaMemset(c->W.own, 0x7f, (5 * tcap + sgcap) * 4));
   // 2D items
   c->T.cap = 256; c->T.rcap = 128;
-  int icap = 1 << 16;
-  c->T.cand = dmalloc<int>(icap); c->T.pid = dmalloc<int>(icap); c->T.state = dmalloc<int>(icap);
-  c->T.cav = dmalloc<int>((size_t)icap * c->T.cap); c->T.ncav = dmalloc<int>(icap);
-  c->T.rem = dmalloc<int>((size_t)icap * c->T.rcap); c->T.nrem = dmalloc<int>(icap);
+  c->T.icap = 0;
+  c->T.cand = c->T.pid = c->T.state = c->T.ncav = c->T.nrem = c->T.cav = c->T.rem = nullptr;   // freed by free_all
+  ensure_items(c, 1 << 16);
   c->T.own = dmalloc<int>(t2cap);
   CK(cudaMemset(c->T.own, 0x7f, t2cap * 4));
   c->L.cap = 1 << 20; c->L.rows = dmalloc<int>((size_t)8 * c->L.cap);
@@ -2268,7 +2290,7 @@ static void free_all(gq_ctx* c) {
   Dev& D = c->D;
   void* ps[] = {D.P, D.vorigin, D.vert_tet, D.vsid, D.tv, D.tn, D.alive, D.sub, D.seg, D.skip, D.ratio, D.sg_uv,
                 D.sg_sid, D.sg_fl, D.sg_hk, D.sg_hv, D.sf_v, D.sf_fl, D.sf_hk, D.sf_hv, D.t2v, D.t2alive, D.he_hk,
-                D.he_hv, D.t2count, D.poly_keep, D.segpoly_off, D.segpoly, D.sid_uv, c->dctr, c->W.own, c->T.cand,
+                D.he_hv, D.t2count, D.poly_keep, D.poly_obl, D.t2last, D.segpoly_off, D.segpoly, D.sid_uv, c->dctr, c->W.own, c->T.cand,
                 c->T.pid, c->T.state, c->T.cav, c->T.ncav, c->T.rem, c->T.nrem, c->T.own, c->L.rows, c->d_int,
                 c->S.tkey, c->S.tval, c->S.tep, c->S.fkey, c->S.fep, c->S.epoch, c->S.list, c->S.stack, c->S.in,
                 c->S.comp, c->SB.tkey, c->SB.tval, c->SB.tep, c->SB.fkey, c->SB.fep, c->SB.epoch, c->SB.list,
@@ -2862,7 +2884,7 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
   if (c->npoly > 0) {
     LAUNCH(k_item_count, ni, c->D, C, ins, ni, flags);
     nit = scan_total(c, flags, pos, ni);
-    if (nit > (1 << 16)) throw std::runtime_error("too many 2D items");
+    ensure_items(c, nit);
     item_of = c->Q.f;
     if (nit > 0) LAUNCH(k_item_fill, ni, c->D, C, ins, ni, pos, flags, c->T, item_of);
   }
@@ -3137,6 +3159,14 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
     for (int s = 0; s < m; ++s) { spo[s + 1] = spo[s] + (int)c->polys[s].size(); for (int p : c->polys[s]) sp.push_back(p); }
     for (int s = 0; s < m; ++s) if (c->polys[s].size() > 4) throw std::runtime_error("segment shared by more than 4 polygons");
     CK(cudaMemcpy(D.poly_keep, keep, 8 * (size_t)f, cudaMemcpyHostToDevice));
+    std::vector<uint8_t> obl(f, 1);
+    for (int pid = 0; pid < f; ++pid)
+      for (int k = 0; k < 3 && obl[pid]; ++k) {
+        bool same = true;
+        for (int q = poff[pid] + 1; q < poff[pid + 1] && same; ++q) same = xyz[3 * pidx[q] + k] == xyz[3 * pidx[poff[pid]] + k];
+        if (same) obl[pid] = 0;
+      }
+    CK(cudaMemcpy(D.poly_obl, obl.data(), f, cudaMemcpyHostToDevice));
     if (!sp.empty()) CK(cudaMemcpy(D.segpoly, sp.data(), 4 * sp.size(), cudaMemcpyHostToDevice));
   }
   CK(cudaMemcpy(D.segpoly_off, spo.data(), 4 * (size_t)(m + 1), cudaMemcpyHostToDevice));
