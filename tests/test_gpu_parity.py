@@ -103,6 +103,31 @@ def test_refine_c2_scaled_vs_oracle(gq):
     assert rep.bad_tet_count == int(((ref["alive"] == 1) & (ref["tv"][:, 3] >= 0) & (ref["ratio"] > 1.6)).sum())
 
 
+@pytest.mark.parametrize("cfg,scale,B", [("C3", 0.02, 1.4), ("C5", 0.05, 1.5), ("C1", 1.0, 2.0)])
+def test_refine_other_configs_vs_oracle(gq, cfg, scale, B):
+    """C3 (axis-plane triangles on a 2^-16 grid, the reference-robust parity
+    variant), C5 (cube + random points) and C1 at test scale: bit-identical
+    point sets and the same per-round statistics as the oracle."""
+    import oracle
+    from paper_1903_03406_b200 import synth
+    plc = synth.config_plc(cfg, scale=scale)
+    mesh, rep = _refine(plc, B)
+    ref = oracle.refine(plc, B=B)
+    assert np.array_equal(mesh.points, ref["points"])
+    assert len(rep.per_round) == len(ref["per_round"])
+    mesh.audit()
+
+
+def test_refine_c3_oblique_stress(gq):
+    """C3 stress variant (oblique triangles): the reference crashes on it
+    (SURVEY F1); the GPU path must finish with a conforming mesh."""
+    from paper_1903_03406_b200 import synth
+    plc = synth.triangles_cloud(2000, 20, 0, snapped=False)
+    mesh, rep = _refine(plc, 1.4)
+    mesh.audit()
+    assert rep.steiner_points > 0
+
+
 def test_refine_c2_full_matches_published_reference_counts(gq):
     """Full BASELINE configs[1]: the reference's measured run (SURVEY.md
     Appendix A / BASELINE.md section 2) gave 135,443 Steiner points,
