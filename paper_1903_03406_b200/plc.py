@@ -33,11 +33,28 @@ class PLC:
         self.segments = [tuple(int(i) for i in s) for s in self.segments]
         self.polygons = [tuple(int(i) for i in poly) for poly in self.polygons]
 
+    @classmethod
+    def _normalised(cls, points, segments, polygons):
+        """Build from lists that are already in normal form (no re-conversion)."""
+        obj = cls.__new__(cls)
+        obj.points, obj.segments, obj.polygons = points, segments, polygons
+        return obj
+
+
+def points_array(plc: PLC) -> np.ndarray:
+    """(n, 3) float64 view of plc.points, converted once per PLC object (the
+    list is the public, reference-compatible representation)."""
+    cache = plc.__dict__.get("_points_np")
+    if cache is None or cache[0] is not plc.points or len(cache[1]) != len(plc.points):
+        arr = np.asarray(plc.points, dtype=np.float64).reshape(-1, 3)
+        plc.__dict__["_points_np"] = cache = (plc.points, arr)
+    return cache[1]
+
 
 def bounding_box(plc: PLC):
     if not plc.points:
         raise EmptyPLC("PLC has no points")
-    arr = np.asarray(plc.points, dtype=np.float64)
+    arr = points_array(plc)
     return tuple(float(x) for x in arr.min(axis=0)), tuple(float(x) for x in arr.max(axis=0))
 
 
@@ -203,7 +220,7 @@ def _overlapping_pairs(boxes):
         active.append(k)
 
 
-FAST_MIN_FEATURES = 2000   # below this the exact path is fast enough
+FAST_MIN_FEATURES = 256    # below this the exact path is fast enough
 
 
 def _exact_pair(plc: PLC, u: int, v: int) -> bool:
@@ -287,7 +304,7 @@ def validate(plc: PLC, fast: bool = None) -> list:
                 out.append(("polygon-not-simple", pidx))
     if out or not plc.points:
         return out
-    pts = np.asarray(plc.points, dtype=np.float64)
+    pts = points_array(plc)
     boxes = []
     for (i, j) in plc.segments:
         boxes.append((np.minimum(pts[i], pts[j]), np.maximum(pts[i], pts[j])))
@@ -336,7 +353,7 @@ def hull_covered(plc: PLC) -> bool:
     from scipy.spatial import ConvexHull, QhullError
 
     try:
-        hull = ConvexHull(np.asarray(plc.points))
+        hull = ConvexHull(points_array(plc))
     except QhullError:
         return False
     from .setup_fast import certify_hull_covered
@@ -393,5 +410,6 @@ def augment_with_box(plc: PLC) -> PLC:
                 quad.append(n + 4 * bits[0] + 2 * bits[1] + bits[2])
             faces.append(tuple(quad))
     edges = sorted({(min(q[k], q[(k + 1) % 4]), max(q[k], q[(k + 1) % 4])) for q in faces for k in range(4)})
-    return PLC(points=list(plc.points) + corners, segments=list(plc.segments) + edges,
-               polygons=list(plc.polygons) + faces)
+    return PLC._normalised(list(plc.points) + [tuple(float(x) for x in q) for q in corners],
+                           list(plc.segments) + [tuple(int(i) for i in e) for e in edges],
+                           list(plc.polygons) + [tuple(int(i) for i in f) for f in faces])

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .errors import AllCoplanar, DuplicatePoint, InvalidPLC
-from .plc import PLC, augment_with_box, validate
+from .plc import PLC, augment_with_box, points_array, validate
 
 
 @dataclass
@@ -45,10 +45,15 @@ def prepare(plc: PLC, seed: int = 0, check: bool = True) -> Prepared:
         if violations:
             raise InvalidPLC(violations)
     aug = augment_with_box(plc)
-    pts = np.ascontiguousarray(np.asarray(aug.points, dtype=np.float64).reshape(-1, 3))
+    if aug is plc:
+        pts = np.ascontiguousarray(points_array(plc))
+    else:   # input points (converted once already) + the 8 box corners
+        pts = np.ascontiguousarray(np.concatenate([points_array(plc),
+                                                   np.asarray(aug.points[len(plc.points):], dtype=np.float64).reshape(-1, 3)]))
     if len(pts) < 4:
         raise AllCoplanar("need at least 4 points")
-    if len({tuple(p) for p in aug.points}) != len(aug.points):
+    q = pts[np.lexsort((pts[:, 2], pts[:, 1], pts[:, 0]))]
+    if len(q) > 1 and np.any(np.all(q[1:] == q[:-1], axis=1)):
         raise DuplicatePoint("duplicate input points")
     segs = np.ascontiguousarray(np.asarray(aug.segments, dtype=np.int32).reshape(-1, 2))
     off = [0]

@@ -53,6 +53,7 @@ def refine(plc: PLC, cfg: RefineConfig = None, device: int = None):
     ctx = _context(default_device() if device is None else device)
     cnt = ctx.refine(prep, keep, cfg.B, cfg.max_rounds, cfg.seed, cfg.verbose)
     t_dev = time.perf_counter() - t0 - t_prep
+    t1 = time.perf_counter()
     arrays = ctx.export_mesh(cnt)
     segs, faces = ctx.export_constraints(cnt)
     rows, secs = ctx.export_rounds(cnt)
@@ -73,8 +74,10 @@ def refine(plc: PLC, cfg: RefineConfig = None, device: int = None):
                       "accepted": int(r[3]), "blasted": int(r[4]), "failed": int(r[5]), "inserted": int(r[6]),
                       "pending_segments": int(r[7]), "pending_faces": int(r[8]), "workers": cfg.workers,
                       "time": float(t)} for r, t in zip(rows, secs)]
+    t_exp = time.perf_counter() - t1
     rep.total_time = time.perf_counter() - t0
     rep.device = {"device_ms": cnt.device_ms, "init_ms": cnt.init_ms, "prepare_s": t_prep, "gq_refine_s": t_dev,
+                  "export_s": t_exp,
                   "kernel_launches": int(cnt.kernel_launches), "region_calls": int(cnt.region_calls),
                   "region_ms": cnt.region_ms, "bytes_alg": int(cnt.bytes_alg),
                   "exact_calls": [int(x) for x in cnt.exact_calls]}

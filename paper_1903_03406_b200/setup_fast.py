@@ -137,7 +137,8 @@ def certify_valid(plc, exact_pair) -> bool | None:
     (seg-seg or seg-polygon, indices in the combined feature numbering)."""
     from .plc import _F, _collinear
 
-    P = np.asarray(plc.points, dtype=np.float64).reshape(-1, 3)
+    from .plc import points_array
+    P = points_array(plc)
     npts = len(P)
     if npts == 0 or not np.all(np.isfinite(P)):
         return None
@@ -273,7 +274,8 @@ def facet_axes(plc):
     idx = np.array([k for k, p in enumerate(polys) if len(p) == 3], dtype=np.int64)
     if len(idx) == 0:
         return out
-    P = np.asarray(plc.points, dtype=np.float64).reshape(-1, 3)
+    from .plc import points_array
+    P = points_array(plc)
     T = np.asarray([polys[k] for k in idx], dtype=np.int64)
     nrm, err = _cross_with_bound(P[T[:, 1]] - P[T[:, 0]], P[T[:, 2]] - P[T[:, 0]])
     mag = np.abs(nrm)
