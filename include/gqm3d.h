@@ -84,6 +84,14 @@ int gq_export_skipped(gq_ctx* ctx, int32_t* rows);
  * tets (stats.py:26-99), computed on the device */
 int gq_quality(gq_ctx* ctx, double B, int64_t* bad_count, int64_t* hist36);
 
+/* .node / .ele / .face files of a refined mesh (host only; formats.py:210-263 of
+ * the reference: 1-based ids, "%.17g" coordinates, origin attribute, alive
+ * non-ghost tets in slot order, subface rows (a<b<c, pid) sorted by the caller).
+ * face_path may be NULL. */
+int gq_write_mesh(const char* node_path, const char* ele_path, const char* face_path, const double* points,
+                  const uint8_t* origins, int32_t nv, const int32_t* tv, const uint8_t* alive, int32_t nt,
+                  const int32_t* faces, int32_t nf);
+
 /* batched exact predicates / constructions on the device, for parity tests:
  * which 0 orient3d(12) 1 insphere(15) 2 orient2d(6) 3 incircle2d(8)
  * 4 incircle3d(12) 5 encroaches_segment(9) 6 encroaches_face(12) -> out8;

@@ -33,7 +33,7 @@ class GqCounts(ctypes.Structure):
 
 
 EXPORTS = ("gq_create", "gq_destroy", "gq_last_error", "gq_refine", "gq_export_mesh", "gq_export_constraints",
-           "gq_export_rounds", "gq_export_skipped", "gq_quality", "gq_batch")
+           "gq_export_rounds", "gq_export_skipped", "gq_quality", "gq_batch", "gq_write_mesh")
 
 
 def lib_path() -> str:
@@ -60,6 +60,7 @@ def lib():
         L.gq_export_skipped.argtypes = [vp, vp]
         L.gq_quality.argtypes = [vp, ctypes.c_double, vp, vp]
         L.gq_batch.argtypes = [ctypes.c_int, vp, i32, i32, vp, vp]
+        L.gq_write_mesh.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, vp, vp, i32, vp, vp, i32, vp, i32]
         for name in EXPORTS:
             if name not in ("gq_last_error",):
                 getattr(L, name).restype = ctypes.c_int

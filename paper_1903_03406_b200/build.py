@@ -9,7 +9,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "libgqm3d.so")
 SRC = os.path.join(HERE, "csrc", "gq_main.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("gq_main.cu", "gq_dev.cuh", "gq_exact.cuh", "gq_block.cuh", "gq_warp.cuh")] + \
+SRC_IO = os.path.join(HERE, "csrc", "gq_io.cpp")
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("gq_main.cu", "gq_dev.cuh", "gq_exact.cuh", "gq_block.cuh", "gq_warp.cuh", "gq_io.cpp")] + \
        [os.path.join(os.path.dirname(HERE), "include", "gqm3d.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -29,7 +30,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
     if not force and up_to_date():
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", SO + ".tmp", SRC]
+    cmd = [nvcc, *NVCC_FLAGS, "-o", SO + ".tmp", SRC, SRC_IO]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
