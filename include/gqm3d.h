@@ -36,7 +36,8 @@ enum {
 typedef struct {
   double B;
   int32_t max_rounds;
-  int32_t flags;     /* bit 0: verbose per-round lines on stderr */
+  int32_t flags;     /* bit 0: verbose per-round lines on stderr; bit 1: paper-literal
+                        grow-and-blast filter (one claim round, no resurrection) */
   uint64_t seed;
 } gq_config;
 

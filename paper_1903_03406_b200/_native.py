@@ -100,8 +100,10 @@ class Context:
         except Exception:
             pass
 
-    def refine(self, prep, keep: np.ndarray, B: float, max_rounds: int, seed: int, verbose: bool = False) -> GqCounts:
-        cfg = GqConfig(float(B), int(max_rounds), 1 if verbose else 0, int(seed) & 0xFFFFFFFFFFFFFFFF)
+    def refine(self, prep, keep: np.ndarray, B: float, max_rounds: int, seed: int, verbose: bool = False,
+               blast: bool = False) -> GqCounts:
+        cfg = GqConfig(float(B), int(max_rounds), (1 if verbose else 0) | (2 if blast else 0),
+                       int(seed) & 0xFFFFFFFFFFFFFFFF)
         cnt = GqCounts()
         keep = np.ascontiguousarray(keep, dtype=np.int32)
         self._check(self._L.gq_refine(self._h, _p(prep.points), len(prep.points), prep.n_input, _p(prep.segments),

@@ -20,8 +20,16 @@ class RefineConfig:
     sequential_until: int = 50000
     seed: int = 0
     verbose: bool = False
+    # extension (not in the reference): "greedy" = the reference's filter
+    # (growblast.py:123-207, result-identical); "blast" = the paper's literal
+    # grow-and-blast, one claim round per refinement round and no
+    # resurrection of candidates whose blocker was itself blasted
+    # (SURVEY 8(f) row 4).  Not result-identical.
+    filter: str = "greedy"
 
     def __post_init__(self):
+        if self.filter not in ("greedy", "blast"):
+            raise ValueError("filter must be 'greedy' or 'blast'")
         if self.B <= 0:
             raise ValueError("B must be positive")
         if self.max_rounds < 1:

@@ -830,7 +830,8 @@ __global__ void __launch_bounds__(256) k_filter_coop(Dev D, Cand C, Owners W, in
 }
 __global__ void k_strict_state(Cand C, int n) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
-    C.state[c] = C.state[c] == 10 ? 1 : 2;
+    if (C.state[c] == 10) C.state[c] = 1;
+    else if (C.state[c] == 0) C.state[c] = 2;
 }
 __global__ void k_reset_claims(Dev D, Cand C, Owners W, int n, int all) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
@@ -1995,7 +1996,7 @@ struct gq_ctx {
   unsigned long long* k64a = nullptr; unsigned long long* k64b = nullptr; unsigned int* k32a = nullptr; unsigned int* k32b = nullptr;
   void* cub_tmp = nullptr; size_t cub_cap = 0;
   // config / state
-  double B = 2.0; int max_rounds = 500; unsigned long long seed = 0; bool verbose = false;
+  double B = 2.0; int max_rounds = 500; unsigned long long seed = 0; bool verbose = false; bool blast = false;   // blast: paper-literal grow-and-blast filter (flags bit 1)
   int n_input = 0, npoly = 0;
   std::vector<std::array<long long, 9>> rounds;
   std::vector<double> rtimes;
@@ -3039,7 +3040,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   fine(c, 15);
   rank_candidates(c, n);
   fine(c, 16);
-  run_filter(c, n, nullptr);
+  if (c->blast) run_filter_strict(c, n); else run_filter(c, n, nullptr);
   fine(c, 17);
   g_prof[2] += now_s() - t1;
   R.failed = nfail;
@@ -3091,6 +3092,7 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
                         const int* pidx, int f, const int* keep, const int* order, const gq_config* cfg,
                         gq_counts* out) {
   c->B = cfg->B; c->max_rounds = cfg->max_rounds; c->seed = cfg->seed; c->verbose = cfg->flags & 1;
+  c->blast = (cfg->flags & 2) != 0;
   g_fine = getenv("GQ_PROFILE") && atoi(getenv("GQ_PROFILE")) == 2;
   g_fine_ev = getenv("GQ_PROFILE") && atoi(getenv("GQ_PROFILE")) == 3;
   c->rpairs.clear(); c->fev.clear(); c->evused = 0;

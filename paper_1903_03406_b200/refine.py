@@ -51,7 +51,7 @@ def refine(plc: PLC, cfg: RefineConfig = None, device: int = None):
     keep = facet_keep(prep.plc)
     t_prep = time.perf_counter() - t0
     ctx = _context(default_device() if device is None else device)
-    cnt = ctx.refine(prep, keep, cfg.B, cfg.max_rounds, cfg.seed, cfg.verbose)
+    cnt = ctx.refine(prep, keep, cfg.B, cfg.max_rounds, cfg.seed, cfg.verbose, blast=cfg.filter == "blast")
     t_dev = time.perf_counter() - t0 - t_prep
     t1 = time.perf_counter()
     arrays = ctx.export_mesh(cnt)

@@ -15,6 +15,7 @@ ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--audit", action="store_true")
 ap.add_argument("--max-rounds", type=int, default=500)
 ap.add_argument("--verbose", action="store_true")
+ap.add_argument("--filter", default="greedy")
 a = ap.parse_args()
 Bdef = {"C1": 2.0, "C2": 1.6, "C3": 1.4, "C4": 1.5, "C5": 1.5}[a.config]
 B = a.B or Bdef
@@ -26,7 +27,7 @@ else:
 print(f"{a.config}: {len(plc.points)} points {len(plc.segments)} segments {len(plc.polygons)} polygons, gen {time.time()-t:.1f}s", flush=True)
 for r in range(a.reps):
     t = time.time()
-    mesh, rep = refine(plc, RefineConfig(B=B, max_rounds=a.max_rounds, verbose=a.verbose))
+    mesh, rep = refine(plc, RefineConfig(B=B, max_rounds=a.max_rounds, verbose=a.verbose, filter=a.filter))
     dt = time.time() - t
     ph = {}
     for row in rep.per_round:

@@ -128,6 +128,19 @@ def test_refine_c3_oblique_stress(gq):
     assert rep.steiner_points > 0
 
 
+def test_paper_literal_blast_mode_within_two_percent(gq, golden_dir):
+    """RefineConfig(filter="blast"): the paper's one-shot grow-and-blast
+    filter (no resurrection).  Not result-identical, but the Steiner count
+    stays within the 2% bar of the reference."""
+    g = np.load(os.path.join(golden_dir, "refine_c1.npz"))
+    build, B = CASES["c1"]
+    mesh, rep = _refine(build(), float(g["B"]), filter="blast")
+    mesh.audit()
+    steiner = int(g["steiner"])
+    assert abs(rep.steiner_points - steiner) <= 0.02 * steiner
+    assert rep.bad_tet_count <= max(2, int(g["bad_tet_count"]) * 1.02)
+
+
 def test_refine_c2_full_matches_published_reference_counts(gq):
     """Full BASELINE configs[1]: the reference's measured run (SURVEY.md
     Appendix A / BASELINE.md section 2) gave 135,443 Steiner points,
