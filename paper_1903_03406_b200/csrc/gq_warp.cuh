@@ -524,9 +524,20 @@ __device__ inline bool star_warp(const Dev& D, int vid, const int* bf, int nbf, 
       int h = star_slot(X, inner_key(g, vid), true);
       if (h < 0) { *X.flag = 1; continue; }
       int mine = 4 * nt + m;
-      if (atomicCAS(&X.v0[h], -1, mine) != -1 && atomicCAS(&X.v1[h], -1, mine) != -1) *X.flag = 1;
+      if (atomicCAS(&X.v0[h], -1, mine) != -1 && atomicCAS(&X.v1[h], -1, mine) != -1) {
+#ifdef GQ_DEBUG2D
+        int x = g[0] == vid ? g[1] : g[0], y = g[2] == vid ? g[1] : g[2];
+        printf("[star] vid %d nbf %d: edge (%d,%d) on more than two boundary faces\n", vid, nbf, x, y);
+#endif
+        *X.flag = 1;
+      }
     }
-    if (om < 0) { *X.flag = 1; continue; }
+    if (om < 0) {
+#ifdef GQ_DEBUG2D
+      printf("[star] vid %d nbf %d: boundary face not reproduced\n", vid, nbf);
+#endif
+      *X.flag = 1; continue;
+    }
     set_tn(D, nt, om, 4 * u + j);
     set_tn(D, u, j, 4 * nt + om);
     for (int m = 0; m < 4; ++m) {
@@ -547,7 +558,12 @@ __device__ inline bool star_warp(const Dev& D, int vid, const int* bf, int nbf, 
       int h = star_slot(X, inner_key(g, vid), false);
       int mine = 4 * nt + m;
       int other = h < 0 ? -1 : (X.v0[h] == mine ? X.v1[h] : X.v0[h]);
-      if (other < 0) { *X.flag = 1; continue; }
+      if (other < 0) {
+#ifdef GQ_DEBUG2D
+        printf("[star] vid %d nbf %d: inner face without partner\n", vid, nbf);
+#endif
+        *X.flag = 1; continue;
+      }
       set_tn(D, nt, m, other);
     }
   }
