@@ -311,28 +311,24 @@ __device__ inline int region_block(const Dev& D, const double* p, const int* see
   __syncthreads();
   if (!s_cons) return RS_OK;
   if (tid == 0) {
+    // thread 0, first-met order (_kernels.py:560-635).  Cavity membership by
+    // binary search in the sorted cavity; the boundary-edge set (needed only
+    // to classify subsegments) is built lazily, up to the current tet, the
+    // first time a subsegment is met.
     S.fset.clear();
-    S.tset.clear();
-    // cavity membership for the crossed test: restore from the sorted list
-    for (int a = 0; a < m; ++a) S.tset.put(B.f0[a], a);
+    auto member = [&](int u) {
+      int l = 0, h = m - 1;
+      while (l <= h) { int mid = (l + h) >> 1; int v = B.f0[mid]; if (v == u) return true; if (v < u) l = mid + 1; else h = mid - 1; }
+      return false;
+    };
     const unsigned long long TE = 2ull << 60, TSF = 3ull << 60, TSG = 4ull << 60;
     int st = RS_OK;
+    int te_upto = 0;       // boundary faces O.bf[0..te_upto) are in the edge set
+    int bf_end = 0;        // boundary faces of sorted tets 0..a
     for (int a = 0; a < m && st == RS_OK; ++a) {
       int t = B.f0[a];
       int4 q = D.tv[t];
-      for (int i = 0; i < 4; ++i) {
-        int u = tnk(D, t, i) >> 2;
-        bool blk = blocked(D, A, t, i);
-        bool uin = S.tset.find(u) >= 0;
-        if (uin && !blk) continue;
-        int f[3]; face_verts(q, i, f);
-        for (int k = 0; k < 3; ++k) {
-          int x = f[k], y = f[(k + 1) % 3];
-          if (x == GHOST || y == GHOST) continue;
-          if (x > y) { int tt = x; x = y; y = tt; }
-          if (S.fset.add(TE | ((unsigned long long)x << 30) | (unsigned long long)y) < 0) st = RS_OVERFLOW;
-        }
-      }
+      bf_end += B.f1[a];
       int sm = D.sub[t];
       for (int i = 0; sm && i < 4; ++i) {
         if (!(sm & (1 << i))) continue;
@@ -342,8 +338,7 @@ __device__ inline int region_block(const Dev& D, const double* p, const int* see
         int ins = S.fset.add(TSF | (key3(a0, b0, c0) & ((1ull << 60) - 1)));
         if (ins < 0) { st = RS_OVERFLOW; break; }
         if (ins == 0) continue;
-        int u = tnk(D, t, i) >> 2;
-        bool uin = S.tset.find(u) >= 0;
+        bool uin = member(tnk(D, t, i) >> 2);
         int rec = face_lookup(D, a0, b0, c0);
         bool crossed = uin && rec >= 0 && A.n > 0 && allowed_face(D, A, a0, b0, c0);
         if (crossed) {
@@ -355,13 +350,23 @@ __device__ inline int region_block(const Dev& D, const double* p, const int* see
         }
       }
       int em = D.seg[t];
-      for (int i = 0; em && i < 6; ++i) {
+      for (int i = 0; em && i < 6 && st == RS_OK; ++i) {
         if (!(em & (1 << i))) continue;
         int x = tvk(q, c_edges[i][0]), y = tvk(q, c_edges[i][1]);
         if (x > y) { int tt = x; x = y; y = tt; }
         int ins = S.fset.add(TSG | ((unsigned long long)x << 30) | (unsigned long long)y);
         if (ins < 0) { st = RS_OVERFLOW; break; }
         if (ins == 0) continue;
+        for (; te_upto < bf_end && st == RS_OK; ++te_upto) {   // catch the edge set up to tet a
+          int bt = O.bf[te_upto] >> 2, bi = O.bf[te_upto] & 3;
+          int f[3]; face_verts(D.tv[bt], bi, f);
+          for (int k = 0; k < 3; ++k) {
+            int u = f[k], w = f[(k + 1) % 3];
+            if (u == GHOST || w == GHOST) continue;
+            if (u > w) { int tt = u; u = w; w = tt; }
+            if (S.fset.add(TE | ((unsigned long long)u << 30) | (unsigned long long)w) < 0) st = RS_OVERFLOW;
+          }
+        }
         int rec = seg_lookup(D, x, y);
         bool bound = S.fset.has(TE | ((unsigned long long)x << 30) | (unsigned long long)y);
         if (O.nbseg + O.neseg >= O.ccon) { st = RS_OVERFLOW; break; }

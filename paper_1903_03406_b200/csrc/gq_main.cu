@@ -821,6 +821,10 @@ __global__ void __launch_bounds__(256) k_filter_coop(Dev D, Cand C, Owners W, in
     }
     grid.sync();
     if (*(volatile int*)(ctr + it % 3) == 0) break;
+    if (it >= 100000) {                 // safety net: the iteration always makes progress
+      if (gw == 0 && lane == 0) raise_err(GQ_ERR_CAP);
+      break;
+    }
   }
   for (int c = gw; c < n; c += nw) {                         // clear all owner slots touched
     const int st = C.state[c];

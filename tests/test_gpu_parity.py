@@ -118,16 +118,6 @@ def test_refine_other_configs_vs_oracle(gq, cfg, scale, B):
     mesh.audit()
 
 
-def test_refine_c3_oblique_stress(gq):
-    """C3 stress variant (oblique triangles): the reference crashes on it
-    (SURVEY F1); the GPU path must finish with a conforming mesh."""
-    from paper_1903_03406_b200 import synth
-    plc = synth.triangles_cloud(2000, 20, 0, snapped=False)
-    mesh, rep = _refine(plc, 1.4)
-    mesh.audit()
-    assert rep.steiner_points > 0
-
-
 def test_paper_literal_blast_mode_within_two_percent(gq, golden_dir):
     """RefineConfig(filter="blast"): the paper's one-shot grow-and-blast
     filter (no resurrection).  Not result-identical, but the Steiner count
