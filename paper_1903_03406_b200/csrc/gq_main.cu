@@ -955,10 +955,11 @@ __device__ __noinline__ int t2_seed_of(const Dev& D, const Cand& C, int c, int p
   return -1;
 }
 
-__global__ void k_t2_compute(Dev D, Cand C, T2Items T, Scr SC) {
-  int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  Scratch S = scratch_for(SC, tid);
-  for (int w = tid; w < T.n; w += gridDim.x * blockDim.x) {
+// The passes of the facet retiling as bodies over items [start, T.n) with a
+// stride: launched grid-wide for many items, or all passes fused in one block
+// (k_t2_fused) when a round has few of them.
+__device__ void t2_compute_body(const Dev& D, const Cand& C, const T2Items& T, Scratch& S, int start, int stride) {
+  for (int w = start; w < T.n; w += stride) {
     if (T.state[w] != 0) continue;
     int c = T.cand[w], pid = T.pid[w];
     Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = C.vid[c];
@@ -991,17 +992,15 @@ __device__ inline void t2_for_claims(const Dev& D, const T2Items& T, int w, F f)
     (void)pid;
   }
 }
-__global__ void k_t2_claim(Dev D, Cand C, T2Items T) {
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < T.n; w += gridDim.x * blockDim.x) {
+__device__ void t2_claim_body(const Dev& D, const Cand& C, const T2Items& T, int start, int stride) {
+  for (int w = start; w < T.n; w += stride) {
     if (T.state[w] != 0) continue;
     int r = C.rank[T.cand[w]];
     t2_for_claims(D, T, w, [&](int tid) { atomicMin(T.own + tid, r); });
   }
 }
-__global__ void k_t2_apply(Dev D, Cand C, T2Items T, Scr SC, int* applied) {
-  int tid0 = blockIdx.x * blockDim.x + threadIdx.x;
-  Scratch S = scratch_for(SC, tid0);
-  for (int w = tid0; w < T.n; w += gridDim.x * blockDim.x) {
+__device__ void t2_apply_body(const Dev& D, const Cand& C, const T2Items& T, int* applied, int start, int stride) {
+  for (int w = start; w < T.n; w += stride) {
     if (T.state[w] != 0) continue;
     int c = T.cand[w];
     int r = C.rank[c];
@@ -1012,10 +1011,8 @@ __global__ void k_t2_apply(Dev D, Cand C, T2Items T, Scr SC, int* applied) {
     atomicAdd(applied, 1);
   }
 }
-__global__ void k_t2_commit(Dev D, Cand C, T2Items T, Scr SC) {
-  int tid0 = blockIdx.x * blockDim.x + threadIdx.x;
-  Scratch S = scratch_for(SC, tid0);
-  for (int w = tid0; w < T.n; w += gridDim.x * blockDim.x) {
+__device__ void t2_commit_body(const Dev& D, const Cand& C, const T2Items& T, Scratch& S, int start, int stride) {
+  for (int w = start; w < T.n; w += stride) {
     if (T.state[w] != 2) continue;
     int c = T.cand[w], pid = T.pid[w];
     Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = C.vid[c];
@@ -1044,19 +1041,60 @@ __global__ void k_t2_commit(Dev D, Cand C, T2Items T, Scr SC) {
     T.state[w] = 1;
   }
 }
-__global__ void k_t2_reset(Dev D, Cand C, T2Items T, int final_pass) {
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < T.n; w += gridDim.x * blockDim.x) {
+__device__ void t2_reset_body(const Dev& D, const T2Items& T, int final_pass, int start, int stride) {
+  for (int w = start; w < T.n; w += stride) {
     if (!final_pass && T.state[w] == 1 && T.ncav[w] < 0) continue;
     t2_for_claims(D, T, w, [&](int tid) { T.own[tid] = INT_MAX; });
   }
 }
 // retire the removed subface records (after every pass, so lookups in later
 // passes still see the pre-round tables only for untouched keys)
-__global__ void k_t2_retire(Dev D, T2Items T) {
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < T.n; w += gridDim.x * blockDim.x) {
+__device__ void t2_retire_body(const Dev& D, const T2Items& T, int start, int stride) {
+  for (int w = start; w < T.n; w += stride) {
     const int* rem = T.rem + (size_t)w * T.rcap;
     for (int k = 0; k < T.nrem[w]; ++k) D.sf_fl[rem[k]] = 0;
   }
+}
+
+#define GRID_START (blockIdx.x * blockDim.x + threadIdx.x)
+#define GRID_STRIDE (gridDim.x * blockDim.x)
+__global__ void k_t2_compute(Dev D, Cand C, T2Items T, Scr SC) {
+  Scratch S = scratch_for(SC, GRID_START);
+  t2_compute_body(D, C, T, S, GRID_START, GRID_STRIDE);
+}
+__global__ void k_t2_claim(Dev D, Cand C, T2Items T) { t2_claim_body(D, C, T, GRID_START, GRID_STRIDE); }
+__global__ void k_t2_apply(Dev D, Cand C, T2Items T, Scr SC, int* applied) { t2_apply_body(D, C, T, applied, GRID_START, GRID_STRIDE); }
+__global__ void k_t2_commit(Dev D, Cand C, T2Items T, Scr SC) {
+  Scratch S = scratch_for(SC, GRID_START);
+  t2_commit_body(D, C, T, S, GRID_START, GRID_STRIDE);
+}
+__global__ void k_t2_reset(Dev D, Cand C, T2Items T, int final_pass) { t2_reset_body(D, T, final_pass, GRID_START, GRID_STRIDE); }
+__global__ void k_t2_retire(Dev D, T2Items T) { t2_retire_body(D, T, GRID_START, GRID_STRIDE); }
+// every pass of a round in one block: no launches or host reads between passes
+__global__ void __launch_bounds__(128) k_t2_fused(Dev D, Cand C, T2Items T, Scr SC, int* applied_total) {
+  Scratch S = scratch_for(SC, threadIdx.x);
+  __shared__ int s_applied;
+  int left = T.n;
+  for (int pass = 0; left > 0; ++pass) {
+    if (threadIdx.x == 0) s_applied = 0;
+    t2_compute_body(D, C, T, S, threadIdx.x, blockDim.x);
+    __syncthreads();
+    t2_claim_body(D, C, T, threadIdx.x, blockDim.x);
+    __syncthreads();
+    t2_apply_body(D, C, T, &s_applied, threadIdx.x, blockDim.x);
+    __syncthreads();
+    t2_reset_body(D, T, 1, threadIdx.x, blockDim.x);
+    __syncthreads();
+    t2_commit_body(D, C, T, S, threadIdx.x, blockDim.x);
+    __syncthreads();
+    t2_retire_body(D, T, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const int applied = s_applied;
+    __syncthreads();
+    if (applied == 0) { if (threadIdx.x == 0) raise_err(GQ_ERR_2D); break; }
+    left -= applied;
+  }
+  if (threadIdx.x == 0) *applied_total = T.n - left;
 }
 
 __global__ void k_kill_cavities(Dev D, Cand C, Ins I) {
@@ -2836,6 +2874,13 @@ __global__ void k_item_fill(Dev D, Cand C, const int* ins, int ni, const int* of
     }
   }
 }
+__global__ void k_count_seed_dead(Dev D, Cand C, int n, int* out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    if (C.state[c] != 2 || C.kind[c] != K_TET) continue;
+    atomicAdd(out, 1);
+    if (!D.alive[C.tgt[c]]) atomicAdd(out + 1, 1);
+  }
+}
 __global__ void k_bump(Dev D, int dnv, int dnt) { D.ctr->nv += dnv; D.ctr->nt += dnt; }
 __global__ void k_pool_pos(Cand C, int n, const int* keepscan, const int* keep) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
@@ -2895,7 +2940,12 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
   }
   g_prof[3] += now_s() - t0;
   double t1 = now_s();
-  if (nit > 0) {
+  if (nit > 0 && nit <= 512 && !getenv("GQ_T2_LAUNCHES")) {   // few items: all passes in one block
+    c->T.n = nit;
+    k_t2_fused<<<1, 128, 0, c->st>>>(c->D, C, c->T, c->S, c->d_int + 16);
+    c->launches++;
+    CK(cudaGetLastError());
+  } else if (nit > 0) {
     c->T.n = nit;
     int left = nit;
     for (int pass = 0; left > 0; ++pass) {
@@ -2907,11 +2957,13 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
       LAUNCH_S(k_t2_commit, nit, c->D, C, c->T, c->S);
       LAUNCH(k_t2_retire, nit, c->D, c->T);
       int applied = read_int(c, c->d_int + 16);
+      if (g_trace) std::fprintf(stderr, "[t2] pass %d applied %d of %d\n", pass, applied, left);
       left -= applied;
       if (applied == 0) throw std::runtime_error("2D retiling made no progress");
     }
   }
   g_prof[4] += now_s() - t1;
+  if (g_trace && nit > 0) std::fprintf(stderr, "[t2] round %d items %d inserted %d\n", round_no, nit, ni);
   t1 = now_s();
   fine(c, 19);
   LAUNCH(k_ins_segsplit, ni, c->D, C, I);
@@ -3063,6 +3115,13 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     R.inserted += read_int(c, c->d_int + 20);
   }
   fine(c, 30);
+  if (g_trace && phase == 2) {   // how many blasted tet candidates had their own tet taken by an accepted cavity
+    CK(cudaMemsetAsync(c->d_int + 56, 0, 8, c->st));
+    LAUNCH(k_count_seed_dead, n, c->D, c->C, n, c->d_int + 56);
+    int h2[2];
+    CK(cudaMemcpy(h2, c->d_int + 56, 8, cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[seed] round %d rejected %d with dead seed tet %d\n", round_no, h2[0], h2[1]);
+  }
   g_prof[5] += now_s() - t1;
   t1 = now_s();
   // post round: new vertices vs every constraint ball, then new / dirty
