@@ -520,16 +520,18 @@ __global__ void __launch_bounds__(BR_THREADS) k_init_region_block(Dev D, Cand C,
 }
 
 // redirect decision (refine.py:595-613, 615-662); marks records RF_REDIR
-__global__ void k_redirect(Dev D, Cand C, int n0, int n1) {
+__global__ void k_redirect(Dev D, Cand C, int n0, int n1, int* nredir) {
   for (int c = n0 + blockIdx.x * blockDim.x + threadIdx.x; c < n1; c += gridDim.x * blockDim.x) {
     int kind = C.kind[c];
     if (kind == K_SEG || C.status[c] == CS_DROP) continue;
     int ns = C.nrseg[c], nf = C.nrface[c];
     if (ns > 0) {
       for (int k = 0; k < ns; ++k) atomicOr(D.sg_fl + C.rseg[(size_t)c * CRD + k], RF_REDIR);
+      atomicAdd(nredir, 1);
       C.status[c] = CS_DROP;
     } else if (kind == K_TET && nf > 0) {
       for (int k = 0; k < nf; ++k) atomicOr(D.sf_fl + C.rface[(size_t)c * CRD + k], RF_REDIR);
+      atomicAdd(nredir + 1, 1);
       C.status[c] = CS_DROP;
     } else if (kind == K_TET) {
       // refine.py:378-413 hull-exit walk from the tet toward its circumcentre
@@ -572,6 +574,7 @@ __global__ void k_redirect(Dev D, Cand C, int n0, int n1) {
       }
       if (hull >= 0 && !(D.sf_fl[hull] & RF_SKIP)) {
         atomicOr(D.sf_fl + hull, RF_REDIR);
+        atomicAdd(nredir + 1, 1);
         C.status[c] = CS_DROP;
       }
     }
@@ -3028,7 +3031,6 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   CandCtx X; X.round_no = round_no; X.seed = c->seed; X.with_facets = c->npoly > 0;
   double lmin2 = c->D.lmin2;
   int phase = -1, nbase = 0;
-  pull(c);
   int ns = sorted_records(c, 0, RF_ENC, RF_BLOCK | RF_SKIP, c->Q.g);
   fine(c, 11);
   if (ns > 0) {
@@ -3068,15 +3070,19 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     grid_sync(c);
     LAUNCH(k_grid_cands, nbase, c->D, c->G, c->C, 0, nbase);
     fine(c, 28);
-    LAUNCH(k_redirect, nbase, c->D, c->C, 0, nbase);
+    CK(cudaMemsetAsync(c->d_int + 60, 0, 8, c->st));
+    LAUNCH(k_redirect, nbase, c->D, c->C, 0, nbase, c->d_int + 60);
     fine(c, 13);
     ensure_tmp(c, nbase + 1);
     LAUNCH(k_kept, nbase, c->C, nbase, c->Q.a);
+    int redir[2] = {0, 0};
+    CK(cudaMemcpyAsync(redir, c->d_int + 60, 8, cudaMemcpyDeviceToHost, c->st));   // read with the scan below
     int kept = scan_total(c, c->Q.a, c->Q.b, nbase);
     LAUNCH(k_pool_pos, nbase, c->C, nbase, c->Q.b, c->Q.a);
     fine(c, 29);
-    int nrs = append_redirects(c, 0, nbase, kept, X);
-    int nrf = phase == 2 ? append_redirects(c, 1, nbase + nrs, kept + nrs, X) : 0;
+    // only rounds with redirect hits pay for the flagged-record sorts
+    int nrs = redir[0] > 0 ? append_redirects(c, 0, nbase, kept, X) : 0;
+    int nrf = phase == 2 && redir[1] > 0 ? append_redirects(c, 1, nbase + nrs, kept + nrs, X) : 0;
     fine(c, 14);
     R.ncand = kept + nrs + nrf;
     g_prof[0] += now_s() - t0;
