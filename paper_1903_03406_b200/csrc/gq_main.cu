@@ -343,6 +343,7 @@ __global__ void k_init_cellmark(Dev D, CellHint H, const int* pend, const int* p
 }
 // one warp per candidate (the common case); overflowing cavities are marked
 // CS_OVF for the block kernel
+#define INIT_BLOCK_ROUTE 192   // bulk construction: cached cavities above this go to the block kernel
 // tiers of the warp region kernel.  Measured on C2: a 128-tet tier at 16 warps
 // / SM plus the 512-tet tier for its overflows is no faster than the 512-tet
 // tier alone (the 4% large cavities cost what the occupancy gains), so both
@@ -413,6 +414,14 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_init_region_warp(Dev D,
         if (!D.alive[t] || touched[t] >= C.memb[c]) bad = true;
       }
       if (!__any_sync(0xffffffffu, bad)) continue;
+    }
+    // a point whose last cavity was large (a box corner far outside the current
+    // hull, recomputed every round while it waits) goes straight to the block
+    // kernel, which grows it with 256 threads instead of 32
+    if (!redo_ovf && st0 == CS_OK && (C.memb[c] == -2 || (C.memb[c] >= 0 && C.ntet[c] > INIT_BLOCK_ROUTE))) {
+      if (lane == 0) { C.status[c] = CS_OVF; C.memb[c] = -1; }
+      __syncwarp();
+      continue;
     }
     int vtx = pend[c];
     if (lane == 0 && g_wdbg) { g_wdbg[2 * gw] = c; g_wdbg[2 * gw + 1] = 1; }
@@ -1529,7 +1538,7 @@ __global__ void k_gather_status(const Cand C, const int* plist, int W, int* out)
 __global__ void k_release_big(Cand C, const int* list, int n) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     int c = list[k];
-    if (C.status[c] != CS_DROP) { C.status[c] = CS_OK; C.memb[c] = -1; }
+    if (C.status[c] != CS_DROP) { C.status[c] = CS_OK; C.memb[c] = -2; }   // -2: was big, route to the block kernel
     C.bigi[c] = -1;
   }
 }
