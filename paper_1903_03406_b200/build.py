@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "libgqm3d.so")
 SRC = os.path.join(HERE, "csrc", "gq_main.cu")
 SRC_IO = os.path.join(HERE, "csrc", "gq_io.cpp")
-DEPS = [os.path.join(HERE, "csrc", f) for f in ("gq_main.cu", "gq_dev.cuh", "gq_exact.cuh", "gq_block.cuh", "gq_warp.cuh", "gq_io.cpp")] + \
+DEPS = [os.path.join(HERE, "csrc", f) for f in sorted(os.listdir(os.path.join(HERE, "csrc"))) if f.endswith((".cu", ".cuh", ".cpp"))] + \
        [os.path.join(os.path.dirname(HERE), "include", "gqm3d.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

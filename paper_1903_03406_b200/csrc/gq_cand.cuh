@@ -1,0 +1,220 @@
+// gq_cand.cuh -- candidate arrays, slabs, priorities, skip log and splitting points (refine.py:35-104, 338-375; mesh.py:416-433).
+// Part of the single translation unit gq_main.cu (included in order).
+#pragma once
+
+// candidate kinds / phases
+#define K_SEG 0
+#define K_FACE 1
+#define K_TET 2
+
+// candidate status
+#define CS_OK 0
+#define CS_CNSS 1
+#define CS_TOOCLOSE 2
+#define CS_MEMB 3
+#define CS_OVF 4
+#define CS_DROP 5      // redirected / skipped before the pool
+
+// slab capacities (normal pass); overflowing candidates rerun with big slabs
+#define CT 512
+#define CF 1088
+#define CC 96
+#define CRD 64
+#define CTB 4096
+#define CFB 8200
+#define CCB 2048
+
+struct Scr {           // per-thread scratch arenas
+  int* tkey; int* tval; unsigned int* tep; int tcap;
+  unsigned long long* fkey; unsigned int* fep; int fcap;
+  unsigned int* epoch;
+  int* list; int* stack; uint8_t* in; uint8_t* comp; int cap;
+  int nthreads;
+};
+__device__ inline Scratch scratch_for(const Scr& s, int tid) {
+  Scratch S;
+  S.tset.key = s.tkey + (size_t)tid * s.tcap; S.tset.val = s.tval + (size_t)tid * s.tcap;
+  S.tset.ep = s.tep + (size_t)tid * s.tcap; S.tset.cur = s.epoch + 2 * tid; S.tset.cap = s.tcap;
+  S.fset.key = s.fkey + (size_t)tid * s.fcap; S.fset.ep = s.fep + (size_t)tid * s.fcap;
+  S.fset.cur = s.epoch + 2 * tid + 1; S.fset.cap = s.fcap;
+  S.list = s.list + (size_t)tid * s.cap; S.stack = s.stack + (size_t)tid * 2 * s.cap;
+  S.in = s.in + (size_t)tid * s.cap; S.comp = s.comp + (size_t)tid * s.cap; S.cap = s.cap;
+  return S;
+}
+
+struct Cand {          // candidate arrays (capacity cap)
+  int cap;
+  int* kind; int* tgt; int* seed; int* status; int* memb; int* pool; int* rank;
+  int4* allow; int* nallow; int* extra;
+  double* p; unsigned long long* h; int4* canon;
+  int* state; int* vid; int* nt0;
+  // region slabs (normal); big slab index in bigi (-1 none)
+  int* ntet; int* nbf; int* ncr; int* nbsub; int* nbseg; int* neseg; double* mind;
+  int* tets; int* bf; int* cr; int* crf; int* bsub; int* bseg; int* eseg;
+  int* rseg; int* rface; int* nrseg; int* nrface;
+  int* bigi;
+  int* btets; int* bbf; int* bcr; int* bcrf; int* bbsub; int* bbseg; int* beseg;
+  int nbigcap;
+};
+struct SlabView { int* tets; int* bf; int* cr; int* crf; int* bsub; int* bseg; int* eseg; int ct, cf, cc; };
+__device__ __forceinline__ SlabView slab(const Cand& C, int c) {
+  SlabView v;
+  int b = C.bigi[c];
+  if (b < 0) {
+    v.tets = C.tets + (size_t)c * CT; v.bf = C.bf + (size_t)c * CF; v.cr = C.cr + (size_t)c * CC;
+    v.crf = C.crf + (size_t)c * CC; v.bsub = C.bsub + (size_t)c * CC; v.bseg = C.bseg + (size_t)c * CC;
+    v.eseg = C.eseg + (size_t)c * CC; v.ct = CT; v.cf = CF; v.cc = CC;
+  } else {
+    v.tets = C.btets + (size_t)b * CTB; v.bf = C.bbf + (size_t)b * CFB; v.cr = C.bcr + (size_t)b * CCB;
+    v.crf = C.bcrf + (size_t)b * CCB; v.bsub = C.bbsub + (size_t)b * CCB; v.bseg = C.bbseg + (size_t)b * CCB;
+    v.eseg = C.beseg + (size_t)b * CCB; v.ct = CTB; v.cf = CFB; v.cc = CCB;
+  }
+  return v;
+}
+
+__device__ unsigned long long g_region_calls;
+__device__ unsigned long long g_tested;       // tets tested for membership (algorithmic bytes)
+
+// ---------------------------------------------------------------------------
+// priorities (refine.py:35-52)
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+  x = x + 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ inline unsigned long long prio_hash(const int* canon, int n, int round_no, unsigned long long seed) {
+  unsigned long long h = splitmix64(seed ^ ((unsigned long long)round_no * 0x9E3779B97F4A7C15ull));
+  for (int k = 0; k < n; ++k) h = splitmix64(h ^ (unsigned long long)((long long)canon[k] + 2));
+  return h;
+}
+
+// ---------------------------------------------------------------------------
+// skipped-element log
+struct SkipLog { int* rows; int cap; };   // 8 ints: round, kind, reason, n, v0..v3
+__device__ __noinline__ void log_skip(const Dev& D, const SkipLog& L, int round_no, int kind, int reason, const int* v, int n) {
+  int k = atomicAdd(&D.ctr->nskip, 1);
+  if (k >= L.cap) { raise_err(GQ_ERR_CAP); return; }
+  int* r = L.rows + 8 * (size_t)k;
+  r[0] = round_no; r[1] = kind; r[2] = reason; r[3] = n;
+  for (int i = 0; i < 4; ++i) r[4 + i] = i < n ? v[i] : -1;
+}
+__device__ inline void tet_canon(const Dev& D, int t, int* c) {
+  int4 q = D.tv[t];
+  c[0] = q.x; c[1] = q.y; c[2] = q.z; c[3] = q.w;
+  for (int a = 1; a < 4; ++a) { int x = c[a], b = a - 1; while (b >= 0 && c[b] > x) { c[b + 1] = c[b]; --b; } c[b + 1] = x; }
+}
+
+// ---------------------------------------------------------------------------
+// candidate construction (refine.py:338-375)
+struct CandCtx { int round_no; unsigned long long seed; int with_facets; };
+
+__device__ __noinline__ int walk_seed(const Dev& D, const double* p, int near_vertex) {   // refine.py:416-418
+  int hint = D.vert_tet[near_vertex];
+  return walk(D, p, hint >= 0 ? hint : -1);
+}
+
+// fills point / priority / seed / allowed pids / claim extra for candidate c.
+// Returns false when the element is degenerate (DegenerateTet / DegenerateTri).
+__device__ __noinline__ bool make_cand(const Dev& D, const Cand& C, int c, const CandCtx& X, Scratch& S) {
+  int kind = C.kind[c], tgt = C.tgt[c];
+  double* p = C.p + 3 * (size_t)c;
+  int canon[4];
+  int nc = 0;
+  C.seed[c] = -1; C.nallow[c] = 0; C.extra[c] = -1;
+  if (kind == K_TET) {
+    tet_canon(D, tgt, canon); nc = 4;
+    int4 q = D.tv[tgt];
+    Sphere s;
+    if (circumsphere_tet(PT(D, q.x), PT(D, q.y), PT(D, q.z), PT(D, q.w), s) != 0) return false;
+    p[0] = s.c[0]; p[1] = s.c[1]; p[2] = s.c[2];
+  } else if (kind == K_SEG) {
+    int2 e = D.sg_uv[tgt];
+    canon[0] = e.x; canon[1] = e.y; nc = 2;
+    const double *pu = PT(D, e.x), *pv = PT(D, e.y);
+    for (int k = 0; k < 3; ++k) p[k] = (pu[k] + pv[k]) / 2.0;
+    if (!edge_exists(D, e.x, e.y, S.tset, S.stack, 2 * S.cap)) C.seed[c] = walk_seed(D, p, e.x);
+    if (X.with_facets) {
+      int sid = D.sg_sid[tgt];
+      int o0 = D.segpoly_off[sid], o1 = D.segpoly_off[sid + 1];
+      int na = 0;
+      int4 al = make_int4(-1, -1, -1, -1);
+      for (int o = o0; o < o1 && na < 4; ++o) {
+        int pid = D.segpoly[o];
+        if (na == 0) al.x = pid; else if (na == 1) al.y = pid; else if (na == 2) al.z = pid; else al.w = pid;
+        ++na;
+      }
+      if (o1 - o0 > 4) raise_err(GQ_ERR_CAP);
+      C.allow[c] = al; C.nallow[c] = na;
+      C.extra[c] = tgt;
+    }
+  } else {
+    int4 f = D.sf_v[tgt];
+    canon[0] = f.x; canon[1] = f.y; canon[2] = f.z; nc = 3;
+    Sphere s;
+    if (!circumcircle_tri(PT(D, f.x), PT(D, f.y), PT(D, f.z), s)) return false;
+    p[0] = s.c[0]; p[1] = s.c[1]; p[2] = s.c[2];
+    int slot = find_face(D, f.x, f.y, f.z, S.tset, S.stack, 2 * S.cap);
+    if (slot < 0) C.seed[c] = walk_seed(D, p, f.x);
+    C.allow[c] = make_int4(f.w, -1, -1, -1); C.nallow[c] = 1;
+    if (slot >= 0) C.extra[c] = min(slot, tnk(D, slot >> 2, slot & 3));
+  }
+  C.h[c] = prio_hash(canon, nc, X.round_no, X.seed);
+  int4 cn = make_int4(nc > 0 ? canon[0] : INT_MAX, nc > 1 ? canon[1] : INT_MAX, nc > 2 ? canon[2] : INT_MAX,
+                      nc > 3 ? canon[3] : INT_MAX);
+  C.canon[c] = cn;
+  return true;
+}
+
+__device__ inline Allow allow_of(const Cand& C, int c) {
+  Allow A;
+  A.n = C.nallow[c];
+  int4 a = C.allow[c];
+  A.pid[0] = a.x; A.pid[1] = a.y; A.pid[2] = a.z; A.pid[3] = a.w;
+  return A;
+}
+
+// seeds of a candidate (mesh.py:416-433): tet itself / sorted edge ring /
+// the two tets of the subface, or the walk seed of a missing constraint
+__device__ __noinline__ int cand_seeds(const Dev& D, const Cand& C, int c, int* out, Scratch& S) {
+  if (C.seed[c] >= 0) { out[0] = C.seed[c]; return 1; }
+  int kind = C.kind[c], tgt = C.tgt[c];
+  DCHK(kind >= 0 && kind <= 2);
+  if (kind == K_TET) { out[0] = tgt; return 1; }
+  if (kind == K_SEG) {
+    int2 e = D.sg_uv[tgt];
+    int n = 0;
+    around_vertex(D, e.x, S.tset, S.stack, 2 * S.cap, [&](int t) {
+      if (has_v(D.tv[t], e.y)) {
+        if (n < 32) out[n++] = t;
+        else { int mx = 0; for (int k = 1; k < 32; ++k) if (out[k] > out[mx]) mx = k; if (t < out[mx]) out[mx] = t; }
+      }
+      return false;
+    });
+    for (int a = 1; a < n; ++a) { int x = out[a], b = a - 1; while (b >= 0 && out[b] > x) { out[b + 1] = out[b]; --b; } out[b + 1] = x; }
+    return n;
+  }
+  int4 f = D.sf_v[tgt];
+  int slot = find_face(D, f.x, f.y, f.z, S.tset, S.stack, 2 * S.cap);
+  if (slot < 0) return 0;
+  int t = slot >> 2, u = tnk(D, t, slot & 3) >> 2;
+  if (u >= 0 && D.alive[u]) { out[0] = min(t, u); out[1] = max(t, u); return 2; }
+  out[0] = t;
+  return 1;
+}
+
+__device__ inline RegionOut region_view(const Cand& C, int c, const SlabView& v, int probe) {
+  RegionOut O;
+  O.tets = v.tets; O.bf = v.bf; O.cr = v.cr; O.crf = v.crf; O.bsub = v.bsub; O.bseg = v.bseg; O.eseg = v.eseg;
+  O.ctet = v.ct; O.cbf = v.cf; O.ccon = v.cc;
+  O.probe = probe;
+  O.rseg = C.rseg + (size_t)c * CRD; O.rface = C.rface + (size_t)c * CRD; O.crd = CRD;
+  O.nrseg = 0; O.nrface = 0;
+  O.memb = -1; O.seed = -1;
+  return O;
+}
+__device__ inline void store_region(const Cand& C, int c, const RegionOut& O) {
+  C.ntet[c] = O.ntet; C.nbf[c] = O.nbf; C.ncr[c] = O.ncr; C.nbsub[c] = O.nbsub; C.nbseg[c] = O.nbseg;
+  C.neseg[c] = O.neseg; C.mind[c] = O.mind; C.nrseg[c] = O.nrseg; C.nrface[c] = O.nrface;
+}
+

@@ -1,0 +1,352 @@
+// gq_fallback.cuh -- sequential fallback for failed candidates (refine.py:748-799).
+// Part of the single translation unit gq_main.cu (included in order).
+#pragma once
+
+// ---------------------------------------------------------------------------
+// sequential fallback for failed candidates (refine.py:748-799): one thread,
+// in pool order, on the updated mesh.  Uses the big scratch / slab 0.
+struct FallbackIO { const int* list; int n; int round_no; unsigned long long seed; int with_facets; double lmin2; int* inserted; };
+
+__device__ inline void mark_enc_face_key(const Dev& D, int a, int b, int c) {
+  sort3(a, b, c);
+  int r = face_lookup(D, a, b, c);
+  if (r >= 0 && !(D.sf_fl[r] & RF_SKIP)) D.sf_fl[r] |= RF_ENC;
+}
+__device__ __noinline__ void skip_cand(const Dev& D, const Cand& C, int c, int reason, int round_no, const SkipLog& L) {
+  int kind = C.kind[c], tgt = C.tgt[c];
+  if (kind == K_TET) {
+    if (tgt >= 0 && tgt < D.ctr->nt && D.alive[tgt]) {
+      D.skip[tgt] = 1;
+      int cv[4]; tet_canon(D, tgt, cv);
+      log_skip(D, L, round_no, K_TET, reason, cv, 4);
+    }
+  } else if (kind == K_SEG) {
+    D.sg_fl[tgt] = (D.sg_fl[tgt] | RF_SKIP) & ~RF_ENC;
+    int2 e = D.sg_uv[tgt]; int v[2] = {e.x, e.y};
+    log_skip(D, L, round_no, K_SEG, reason, v, 2);
+  } else {
+    D.sf_fl[tgt] = (D.sf_fl[tgt] | RF_SKIP) & ~RF_ENC;
+    int4 f = D.sf_v[tgt]; int v[3] = {f.x, f.y, f.z};
+    log_skip(D, L, round_no, K_FACE, reason, v, 3);
+  }
+}
+
+__device__ __noinline__ void insert_one(const Dev& D, const Cand& C, int c, Scratch& S, T2Items& T, int item0) {
+  // sequential insert_candidate: vid, 2D retile per polygon, split, star
+  int vid = atomicAdd(&D.ctr->nv, 1);
+  C.vid[c] = vid;
+  const double* p = C.p + 3 * (size_t)c;
+  double* q = D.P + 3 * (size_t)vid;
+  q[0] = p[0]; q[1] = p[1]; q[2] = p[2];
+  D.vorigin[vid] = 1; D.vert_tet[vid] = -1;
+  D.vsid[vid] = C.kind[c] == K_SEG ? D.sg_sid[C.tgt[c]] : -1;
+  int nitems = 0;
+  if (C.kind[c] != K_TET && D.npoly > 0) {
+    int pids[8]; int np = 0;
+    if (C.kind[c] == K_SEG) {
+      int sid = D.sg_sid[C.tgt[c]];
+      for (int o = D.segpoly_off[sid]; o < D.segpoly_off[sid + 1] && np < 8; ++o) pids[np++] = D.segpoly[o];
+    } else pids[np++] = D.sf_v[C.tgt[c]].w;
+    for (int k = 0; k < np; ++k) {
+      int w = item0 + k;
+      int pid = pids[k];
+      Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = vid;
+      proj2(D, pid, p, X.p);
+      int forced[CC + 2]; int nf;
+      t2_forced(D, C, c, pid, forced, nf, CC + 2);
+      int seeds[CC + 3]; int ns = 0;
+      for (int j = 0; j < nf; ++j) seeds[ns++] = forced[j];
+      int ts = t2_seed_of(D, C, c, pid);
+      if (ts >= 0) seeds[ns++] = ts;
+      int* cav = T.cav + (size_t)w * T.cap;
+      int n = tri2_cavity(X, forced, nf, seeds, ns, S.tset, cav, S.stack, T.cap);
+      if (n < 0) {
+#ifdef GQ_DEBUG2D
+      printf("[2d] cavity fail pid %d vid %d\n", pid, X.vid);
+#endif
+      raise_err(GQ_ERR_2D); n = 0;
+    }
+      S.tset.clear();
+      for (int a = 0; a < n; ++a) S.tset.put(cav[a], a);
+      int* rem = T.rem + (size_t)w * T.rcap;
+      int nrem = 0;
+      tri2_apply(X, cav, n, S.tset,
+        [&](int a, int b, int cc) {
+          sort3(a, b, cc);
+          int rec = face_lookup(D, a, b, cc);
+          if (rec >= 0 && D.sf_v[rec].w == pid) { if (nrem < T.rcap) rem[nrem++] = rec; }
+        },
+        [&](int a, int b, int cc, int) {
+          if (collinear_sliver(D, a, b, cc)) return;
+          int a0 = a, b0 = b, c0 = cc; sort3(a0, b0, c0);
+          if (face_lookup(D, a0, b0, c0) >= 0) return;
+          new_face_record(D, a0, b0, c0, pid, RF_LIVE | RF_CHECK);
+        });
+      T.nrem[w] = nrem;
+      for (int j = 0; j < nrem; ++j) D.sf_fl[rem[j]] = 0;
+      ++nitems;
+    }
+  }
+  if (C.kind[c] == K_SEG) {
+    int r = C.tgt[c];
+    int2 e = D.sg_uv[r];
+    int sid = D.sg_sid[r];
+    D.sg_fl[r] = 0;
+    new_seg_record(D, e.x, vid, sid, RF_LIVE | RF_CHECK);
+    new_seg_record(D, e.y, vid, sid, RF_LIVE | RF_CHECK);
+  }
+  SlabView v = slab(C, c);
+  for (int j = 0; j < C.ntet[c]; ++j) D.alive[v.tets[j]] = 0;
+  int nt0 = atomicAdd(&D.ctr->nt, C.nbf[c]);
+  if (nt0 + C.nbf[c] > D.tcap) { raise_err(GQ_ERR_CAP); return; }
+  C.nt0[c] = nt0;
+  star_insert(D, vid, v.bf, C.nbf[c], nt0, false);
+  for (int j = 0; j < C.nbsub[c]; ++j) { int r = v.bsub[j]; if (r >= 0 && (D.sf_fl[r] & RF_LIVE)) D.sf_fl[r] |= RF_CHECK; }
+  for (int j = 0; j < C.nbseg[c]; ++j) { int r = v.bseg[j]; if (r >= 0 && (D.sg_fl[r] & RF_LIVE)) D.sg_fl[r] |= RF_CHECK; }
+  for (int w = item0; w < item0 + nitems; ++w) {
+    const int* rem = T.rem + (size_t)w * T.rcap;
+    for (int j = 0; j < T.nrem[w]; ++j) {
+      int rec = rem[j];
+      bool crossed = false;
+      for (int qq = 0; qq < C.ncr[c]; ++qq) if (v.cr[qq] == rec) { crossed = true; break; }
+      if (crossed) continue;
+      int4 f = D.sf_v[rec];
+      int slot = find_face(D, f.x, f.y, f.z, S.tset, S.stack, 2 * S.cap);
+      if (slot >= 0) {
+        int t = slot >> 2;
+        refresh_masks(D, t);
+        int u = tnk(D, t, slot & 3) >> 2;
+        if (u >= 0 && D.alive[u]) refresh_masks(D, u);
+      }
+    }
+  }
+}
+
+__global__ void k_fallback(Dev D, Cand C, Scr SCB, FallbackIO F, T2Items T, SkipLog L) {
+  if (blockIdx.x || threadIdx.x) return;
+  Scratch S = scratch_for(SCB, 0);
+  CandCtx X; X.round_no = F.round_no; X.seed = F.seed; X.with_facets = F.with_facets;
+  for (int k = 0; k < F.n; ++k) {
+    int c = F.list[k];
+    int kind = C.kind[c], tgt = C.tgt[c];
+    if (C.status[c] == CS_TOOCLOSE) { skip_cand(D, C, c, 2, F.round_no, L); continue; }
+    if (kind == K_TET && !(tgt >= 0 && tgt < D.ctr->nt && D.alive[tgt])) continue;
+    if (kind == K_SEG && !(D.sg_fl[tgt] & RF_LIVE)) continue;
+    if (kind == K_FACE && !(D.sf_fl[tgt] & RF_LIVE)) continue;
+    if (!make_cand(D, C, c, X, S)) { raise_err(GQ_ERR_DEGEN); continue; }
+    const double* p = C.p + 3 * (size_t)c;
+    if (kind == K_TET) {
+      int cur = tgt, prev = -1, hull = -2;
+      int max_steps = walk_cap(D, 64);
+      bool done = false;
+      for (int step = 0; step < max_steps && !done; ++step) {
+        int4 q = D.tv[cur];
+        if (q.w == GHOST) { int a = q.x, b = q.y, cc = q.z; sort3(a, b, cc); hull = face_lookup(D, a, b, cc); if (hull < 0) hull = -1; done = true; break; }
+        bool moved = false;
+        for (int kk = 0; kk < 4; ++kk) {
+          int i = (kk + step) & 3;
+          int u = tnk(D, cur, i) >> 2;
+          if (u == prev) continue;
+          int f[3]; face_verts(q, i, f);
+          if (orient3d(PT(D, f[0]), PT(D, f[1]), PT(D, f[2]), p) > 0) {
+            if (D.tv[u].w == GHOST) { sort3(f[0], f[1], f[2]); hull = face_lookup(D, f[0], f[1], f[2]); if (hull < 0) hull = -1; done = true; break; }
+            prev = cur; cur = u; moved = true; break;
+          }
+        }
+        if (done) break;
+        if (!moved) { done = true; break; }
+      }
+      if (!done) {
+        int end = walk(D, p, tgt);
+        if (end >= 0 && D.tv[end].w == GHOST) { int4 q = D.tv[end]; int a = q.x, b = q.y, cc = q.z; sort3(a, b, cc); hull = face_lookup(D, a, b, cc); if (hull < 0) hull = -1; }
+      }
+      if (hull >= 0) {   // redirect the subface to the next round
+        if (!(D.sf_fl[hull] & RF_SKIP)) D.sf_fl[hull] |= RF_ENC;
+        continue;
+      }
+    }
+    C.bigi[c] = 0;
+    SlabView sv = slab(C, c);
+    RegionOut O = region_view(C, c, sv, 0);
+    int seeds[32];
+    int ns = cand_seeds(D, C, c, seeds, S);
+    atomicAdd(&g_region_calls, 1ull);
+    int st = ns == 0 ? RS_CNSS : region_compute(D, p, seeds, ns, allow_of(C, c), S, O);
+    store_region(C, c, O);
+    if (st == RS_OK) {
+      if (O.mind <= D.too_close_sq) { skip_cand(D, C, c, 2, F.round_no, L); continue; }
+      if (kind == K_TET && O.mind < F.lmin2) {
+        D.skip[tgt] = 1;
+        int cv[4]; tet_canon(D, tgt, cv);
+        log_skip(D, L, F.round_no, K_TET, 1, cv, 4);
+        continue;
+      }
+      if (D.ctr->nv >= D.vcap) { raise_err(GQ_ERR_CAP); return; }
+      insert_one(D, C, c, S, T, 0);
+      atomicAdd(F.inserted, 1);
+    } else if (st == RS_MEMBRANE) {
+      int t = O.memb >> 2, i = O.memb & 3;
+      int f[3]; face_verts(D.tv[t], i, f);
+      mark_enc_face_key(D, f[0], f[1], f[2]);
+      if (kind == K_SEG) D.sg_fl[tgt] |= RF_BLOCK;
+      else if (kind == K_FACE) D.sf_fl[tgt] |= RF_BLOCK;
+    } else {
+      if (st == RS_OVERFLOW) raise_err(GQ_ERR_CAP);
+      skip_cand(D, C, c, 3, F.round_no, L);
+    }
+  }
+}
+
+// accepted tets whose region has a too-short boundary edge (refine.py:891-894)
+__global__ void k_accept_flags(Dev D, Cand C, const int* acc, int nacc, int* insflag, SkipLog L, int round_no, double lmin2) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nacc; k += gridDim.x * blockDim.x) {
+    int c = acc[k];
+    if (C.kind[c] == K_TET && C.mind[c] < lmin2) {
+      insflag[k] = 0;
+      int t = C.tgt[c];
+      if (t >= 0 && D.alive[t]) {
+        D.skip[t] = 1;
+        int cv[4]; tet_canon(D, t, cv);
+        log_skip(D, L, round_no, K_TET, 1, cv, 4);
+      }
+    } else insflag[k] = 1;
+  }
+}
+__global__ void k_assign_ids(Cand C, const int* ins, int n, const int* nbfscan, int nv0, int nt0) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    int c = ins[k];
+    C.vid[c] = nv0 + k;
+    C.nt0[c] = nt0 + nbfscan[k];
+  }
+}
+__global__ void k_gather_nbf(Cand C, const int* ins, int n, int* out) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) out[k] = C.nbf[ins[k]];
+}
+__global__ void k_rank_scatter(Cand C, const int* order, int n) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) C.rank[order[k]] = k;
+}
+
+// compaction of dead tet slots (mesh.py:847-865), stable
+__global__ void k_compact_flags(Dev D, int* flags) {
+  int nt = D.ctr->nt;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) flags[t] = D.alive[t] == 1;
+}
+__global__ void k_compact_move(Dev D, const int* remap, int nt, int4* tv2, int4* tn2, uint8_t* sub2, uint8_t* seg2,
+                               double* ratio2, uint8_t* skip2) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    if (D.alive[t] != 1) continue;
+    int r = remap[t];
+    tv2[r] = D.tv[t];
+    int4 q = D.tn[t];
+    tn2[r] = make_int4(remap[q.x >> 2] * 4 + (q.x & 3), remap[q.y >> 2] * 4 + (q.y & 3),
+                       remap[q.z >> 2] * 4 + (q.z & 3), remap[q.w >> 2] * 4 + (q.w & 3));
+    sub2[r] = D.sub[t]; seg2[r] = D.seg[t]; ratio2[r] = D.ratio[t]; skip2[r] = D.skip[t];
+  }
+}
+__global__ void k_compact_vt(Dev D, const int* remap, const int* flags, int nv) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    int t = D.vert_tet[v];
+    D.vert_tet[v] = t >= 0 ? (flags[t] ? remap[t] : -1) : -1;
+  }
+}
+
+// quality (stats.py:35-99): bad count + dihedral histogram of real tets
+__global__ void k_quality(Dev D, double B, unsigned long long* bad, unsigned long long* hist) {
+  int nt = D.ctr->nt;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    if (!D.alive[t] || D.tv[t].w == GHOST) continue;
+    int4 q = D.tv[t];
+    const double* P4[4] = {PT(D, q.x), PT(D, q.y), PT(D, q.z), PT(D, q.w)};
+    double a[3], u[3], v[3], w[3];
+    for (int k = 0; k < 3; ++k) { a[k] = P4[0][k]; u[k] = P4[1][k] - a[k]; v[k] = P4[2][k] - a[k]; w[k] = P4[3][k] - a[k]; }
+    double vw[3] = {v[1] * w[2] - v[2] * w[1], v[2] * w[0] - v[0] * w[2], v[0] * w[1] - v[1] * w[0]};
+    double wu[3] = {w[1] * u[2] - w[2] * u[1], w[2] * u[0] - w[0] * u[2], w[0] * u[1] - w[1] * u[0]};
+    double uv[3] = {u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2], u[0] * v[1] - u[1] * v[0]};
+    double denom = 2.0 * (u[0] * vw[0] + u[1] * vw[1] + u[2] * vw[2]);
+    double lu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    double lv = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+    double lw = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
+    double off[3];
+    for (int k = 0; k < 3; ++k) off[k] = (lu * vw[k] + lv * wu[k] + lw * uv[k]) / denom;
+    double r2 = off[0] * off[0] + off[1] * off[1] + off[2] * off[2];
+    double sh = INFINITY;
+    const int pr[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+    for (int e = 0; e < 6; ++e) {
+      double d = dist2(P4[pr[e][0]], P4[pr[e][1]]);
+      sh = d < sh ? d : sh;
+    }
+    double ratio = sqrt(r2 / sh);
+    if (!isfinite(ratio)) ratio = INFINITY;
+    if (ratio > B) atomicAdd(bad, 1ull);
+    for (int e = 0; e < 6; ++e) {
+      int i = pr[e][0], j = pr[e][1];
+      int kk = -1, ll = -1;
+      for (int m = 0; m < 4; ++m) if (m != i && m != j) { if (kk < 0) kk = m; else ll = m; }
+      double ed[3], ek[3], el[3];
+      for (int k = 0; k < 3; ++k) { ed[k] = P4[j][k] - P4[i][k]; ek[k] = P4[kk][k] - P4[i][k]; el[k] = P4[ll][k] - P4[i][k]; }
+      double n1[3] = {ed[1] * ek[2] - ed[2] * ek[1], ed[2] * ek[0] - ed[0] * ek[2], ed[0] * ek[1] - ed[1] * ek[0]};
+      double n2[3] = {ed[1] * el[2] - ed[2] * el[1], ed[2] * el[0] - ed[0] * el[2], ed[0] * el[1] - ed[1] * el[0]};
+      double dot = n1[0] * n2[0] + n1[1] * n2[1] + n1[2] * n2[2];
+      double nrm = sqrt((n1[0] * n1[0] + n1[1] * n1[1] + n1[2] * n1[2]) * (n2[0] * n2[0] + n2[1] * n2[1] + n2[2] * n2[2]));
+      double ca = dot / nrm;
+      ca = ca < -1.0 ? -1.0 : (ca > 1.0 ? 1.0 : ca);
+      double ang = acos(ca) * (180.0 / 3.14159265358979323846);
+      int bin = (int)(ang / 5.0);
+      bin = bin < 0 ? 0 : (bin > 35 ? 35 : bin);
+      if (!(ang == ang)) bin = 0;
+      atomicAdd(hist + bin, 1ull);
+    }
+  }
+}
+
+// batched predicates / constructions for parity tests (gq_batch)
+__global__ void k_batch(int which, const double* in, int n, signed char* out8, double* outd) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double* x;
+    switch (which) {
+      case 0: x = in + 12 * (size_t)i; out8[i] = (signed char)orient3d(x, x + 3, x + 6, x + 9); break;
+      case 1: x = in + 15 * (size_t)i; out8[i] = (signed char)insphere(x, x + 3, x + 6, x + 9, x + 12); break;
+      case 2: x = in + 6 * (size_t)i; out8[i] = (signed char)orient2d(x, x + 2, x + 4); break;
+      case 3: x = in + 8 * (size_t)i; out8[i] = (signed char)incircle2d(x, x + 2, x + 4, x + 6); break;
+      case 4: {
+        x = in + 12 * (size_t)i;
+        unsigned int before = g_err;
+        int r = incircle3d(x, x + 3, x + 6, x + 9);
+        // degenerate triangle: the reference raises; report 99
+        double ux = x[3] - x[0], uy = x[4] - x[1], uz = x[5] - x[2], vx = x[6] - x[0], vy = x[7] - x[1], vz = x[8] - x[2];
+        double a2[2], b2[2], c2[2]; bool deg = true;
+        for (int axis = 0; axis < 3 && deg; ++axis) {
+          int p = axis == 0 ? 1 : 0, q = axis == 2 ? 1 : 2;
+          a2[0] = x[p]; a2[1] = x[q]; b2[0] = x[3 + p]; b2[1] = x[3 + q]; c2[0] = x[6 + p]; c2[1] = x[6 + q];
+          if (orient2d(a2, b2, c2) != 0) deg = false;
+        }
+        (void)before; (void)ux; (void)uy; (void)uz; (void)vx; (void)vy; (void)vz;
+        out8[i] = deg ? 99 : (signed char)r;
+        break;
+      }
+      case 5: x = in + 9 * (size_t)i; out8[i] = encroaches_segment(x, x + 3, x + 6) ? 1 : 0; break;
+      case 6: {
+        x = in + 12 * (size_t)i;
+        Sphere sp;
+        if (!circumcircle_tri(x, x + 3, x + 6, sp)) { out8[i] = 99; break; }
+        out8[i] = encroaches_face(x, x + 3, x + 6, x + 9) ? 1 : 0;
+        break;
+      }
+      case 7: {
+        x = in + 12 * (size_t)i;
+        Sphere sp;
+        if (circumsphere_tet(x, x + 3, x + 6, x + 9, sp) != 0) { for (int k = 0; k < 4; ++k) outd[4 * (size_t)i + k] = nan(""); }
+        else { outd[4 * (size_t)i] = sp.c[0]; outd[4 * (size_t)i + 1] = sp.c[1]; outd[4 * (size_t)i + 2] = sp.c[2]; outd[4 * (size_t)i + 3] = sp.r2; }
+        break;
+      }
+      case 8: {
+        x = in + 9 * (size_t)i;
+        Sphere sp;
+        if (!circumcircle_tri(x, x + 3, x + 6, sp)) { for (int k = 0; k < 4; ++k) outd[4 * (size_t)i + k] = nan(""); }
+        else { outd[4 * (size_t)i] = sp.c[0]; outd[4 * (size_t)i + 1] = sp.c[1]; outd[4 * (size_t)i + 2] = sp.c[2]; outd[4 * (size_t)i + 3] = sp.r2; }
+        break;
+      }
+    }
+  }
+}
+

@@ -1,0 +1,345 @@
+// gq_insert.cuh -- insertion of the accepted set: vertices, facet retiling, stars, bookkeeping (refine.py:677-736, facets.py, mesh.py:697-816).
+// Part of the single translation unit gq_main.cu (included in order).
+#pragma once
+
+// ---------------------------------------------------------------------------
+// insertion of the accepted set
+struct Ins {          // inserted candidates in priority order
+  int* list; int n;
+  int nv0, nt0base;
+};
+
+// vertex ids / points / subsegment splits (refine.py:688-708 bookkeeping)
+__global__ void k_ins_vertices(Dev D, Cand C, Ins I) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < I.n; k += gridDim.x * blockDim.x) {
+    int c = I.list[k];
+    int vid = C.vid[c];
+    const double* p = C.p + 3 * (size_t)c;
+    double* q = D.P + 3 * (size_t)vid;
+    q[0] = p[0]; q[1] = p[1]; q[2] = p[2];
+    D.vorigin[vid] = 1;
+    D.vert_tet[vid] = -1;
+    D.vsid[vid] = C.kind[c] == K_SEG ? D.sg_sid[C.tgt[c]] : -1;
+  }
+}
+
+__device__ inline int new_seg_record(const Dev& D, int u, int v, int sid, unsigned int fl) {
+  if (u > v) { int t = u; u = v; v = t; }
+  int r = atomicAdd(&D.ctr->nsegrec, 1);
+  if (r >= D.sgcap) { raise_err(GQ_ERR_CAP); return -1; }
+  D.sg_uv[r] = make_int2(u, v); D.sg_sid[r] = sid; D.sg_fl[r] = fl;
+  ht_put(D.sg_hk, D.sg_hv, D.sg_hmask, key2(u, v), r);
+  return r;
+}
+__device__ inline int new_face_record(const Dev& D, int a, int b, int c, int pid, unsigned int fl) {
+  sort3(a, b, c);
+  int r = atomicAdd(&D.ctr->nfacerec, 1);
+  if (r >= D.sfcap) { raise_err(GQ_ERR_CAP); return -1; }
+  D.sf_v[r] = make_int4(a, b, c, pid); D.sf_fl[r] = fl;
+  ht_put(D.sf_hk, D.sf_hv, D.sf_hmask, key3(a, b, c), r);
+  return r;
+}
+
+__global__ void k_ins_segsplit(Dev D, Cand C, Ins I) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < I.n; k += gridDim.x * blockDim.x) {
+    int c = I.list[k];
+    if (C.kind[c] != K_SEG) continue;
+    int r = C.tgt[c];
+    int2 e = D.sg_uv[r];
+    int sid = D.sg_sid[r];
+    D.sg_fl[r] = 0;   // removed (also leaves enc_segs)
+    int vid = C.vid[c];
+    new_seg_record(D, e.x, vid, sid, RF_LIVE | RF_CHECK);
+    new_seg_record(D, e.y, vid, sid, RF_LIVE | RF_CHECK);
+  }
+}
+
+// facets.py:377-386: triangle on one segment line
+__device__ __noinline__ bool collinear_sliver(const Dev& D, int a, int b, int c) {
+  int v3[3] = {a, b, c};
+  for (int k = 0; k < 3; ++k) {
+    int s = D.vsid[v3[k]];
+    if (s < 0) continue;
+    int2 e = D.sid_uv[s];
+    bool all = true;
+    for (int j = 0; j < 3 && all; ++j) {
+      int w = v3[j];
+      if (D.vsid[w] == s || w == e.x || w == e.y) continue;
+      all = false;
+    }
+    if (all) return true;
+  }
+  return false;
+}
+
+// 2D retiling work items: (candidate, polygon)
+struct T2Items {
+  int* cand; int* pid; int* state; int n;   // state 0 pending, 1 done
+  int* cav; int* ncav; int cap;             // per item cavity tids
+  int* own;                                 // per 2D triangle owner rank
+  int* rem; int* nrem; int rcap;            // removed subface records per item
+  int icap;                                 // items allocated
+};
+
+__device__ __noinline__ void t2_forced(const Dev& D, const Cand& C, int c, int pid, int* forced, int& nf, int cap) {
+  // crossed subfaces of this polygon (refine.py:677-683) -> their 2D triangles
+  SlabView v = slab(C, c);
+  nf = 0;
+  for (int k = 0; k < C.ncr[c]; ++k) {
+    int rec = v.cr[k];
+    if (rec < 0) continue;
+    int4 f = D.sf_v[rec];
+    if (f.w != pid) continue;
+    // triangle with directed edge a->b or b->a holding c
+    int t = he_lookup(D, f.x, f.y, pid);
+    if (t < 0 || !(D.t2v[t].x == f.z || D.t2v[t].y == f.z || D.t2v[t].z == f.z)) t = he_lookup(D, f.y, f.x, pid);
+    if (t >= 0 && nf < cap) forced[nf++] = t;
+  }
+  if (C.kind[c] == K_SEG) {   // split edge triangles (facets.py:310-315)
+    int2 e = D.sg_uv[C.tgt[c]];
+    int t1 = he_lookup(D, e.x, e.y, pid); if (t1 >= 0 && nf < cap) forced[nf++] = t1;
+    int t2 = he_lookup(D, e.y, e.x, pid); if (t2 >= 0 && nf < cap) forced[nf++] = t2;
+  }
+}
+__device__ __noinline__ int t2_seed_of(const Dev& D, const Cand& C, int c, int pid) {
+  if (C.kind[c] == K_FACE) {
+    int4 f = D.sf_v[C.tgt[c]];
+    int t = he_lookup(D, f.x, f.y, pid);
+    if (t < 0 || !(D.t2v[t].x == f.z || D.t2v[t].y == f.z || D.t2v[t].z == f.z)) t = he_lookup(D, f.y, f.x, pid);
+    return t;
+  }
+  return -1;
+}
+
+// The passes of the facet retiling as bodies over items [start, T.n) with a
+// stride: launched grid-wide for many items, or all passes fused in one block
+// (k_t2_fused) when a round has few of them.
+__device__ void t2_compute_body(const Dev& D, const Cand& C, const T2Items& T, Scratch& S, int start, int stride) {
+  for (int w = start; w < T.n; w += stride) {
+    if (T.state[w] != 0) continue;
+    int c = T.cand[w], pid = T.pid[w];
+    Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = C.vid[c];
+    proj2(D, pid, C.p + 3 * (size_t)c, X.p);
+    int forced[CC + 2]; int nf;
+    t2_forced(D, C, c, pid, forced, nf, CC + 2);
+    int seeds[CC + 3]; int ns = 0;
+    for (int k = 0; k < nf; ++k) seeds[ns++] = forced[k];
+    int ts = t2_seed_of(D, C, c, pid);
+    if (ts >= 0) seeds[ns++] = ts;
+    int n = tri2_cavity(X, forced, nf, seeds, ns, S.tset, T.cav + (size_t)w * T.cap, S.stack, T.cap);
+    if (n < 0) {
+#ifdef GQ_DEBUG2D
+      printf("[2d] cavity fail pid %d vid %d\n", pid, X.vid);
+#endif
+      raise_err(GQ_ERR_2D); n = 0;
+    }
+    T.ncav[w] = n;
+  }
+}
+template <class F>
+__device__ inline void t2_for_claims(const Dev& D, const T2Items& T, int w, F f) {
+  const int* cav = T.cav + (size_t)w * T.cap;
+  int pid = T.pid[w];
+  for (int k = 0; k < T.ncav[w]; ++k) {
+    int tid = cav[k];
+    f(tid);
+    int4 t = D.t2v[tid];
+    for (int e = 0; e < 3; ++e) { int nb = t2_nb(D, t, e); if (nb >= 0) f(nb); }
+    (void)pid;
+  }
+}
+__device__ void t2_claim_body(const Dev& D, const Cand& C, const T2Items& T, int start, int stride) {
+  for (int w = start; w < T.n; w += stride) {
+    if (T.state[w] != 0) continue;
+    int r = C.rank[T.cand[w]];
+    t2_for_claims(D, T, w, [&](int tid) { atomicMin(T.own + tid, r); });
+  }
+}
+__device__ void t2_apply_body(const Dev& D, const Cand& C, const T2Items& T, int* applied, int start, int stride) {
+  for (int w = start; w < T.n; w += stride) {
+    if (T.state[w] != 0) continue;
+    int c = T.cand[w];
+    int r = C.rank[c];
+    bool win = true;
+    t2_for_claims(D, T, w, [&](int tid) { if (T.own[tid] != r) win = false; });
+    if (!win) continue;
+    T.state[w] = 2;   // apply (owners reset next)
+    atomicAdd(applied, 1);
+  }
+}
+__device__ void t2_commit_body(const Dev& D, const Cand& C, const T2Items& T, Scratch& S, int start, int stride) {
+  for (int w = start; w < T.n; w += stride) {
+    if (T.state[w] != 2) continue;
+    int c = T.cand[w], pid = T.pid[w];
+    Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = C.vid[c];
+    proj2(D, pid, C.p + 3 * (size_t)c, X.p);
+    int n = T.ncav[w];
+    int* cav = T.cav + (size_t)w * T.cap;
+    S.tset.clear();
+    for (int k = 0; k < n; ++k) S.tset.put(cav[k], k);
+    int* rem = T.rem + (size_t)w * T.rcap;
+    int nrem = 0;
+    tri2_apply(X, cav, n, S.tset,
+      [&](int a, int b, int cc) {          // removed: rem &= keys_by_pid
+        sort3(a, b, cc);
+        int rec = face_lookup(D, a, b, cc);
+        if (rec >= 0 && D.sf_v[rec].w == pid) {
+          if (nrem < T.rcap) rem[nrem++] = rec; else raise_err(GQ_ERR_CAP);
+        }
+      },
+      [&](int a, int b, int cc, int t2) {  // added, unless a collinear sliver
+        if (collinear_sliver(D, a, b, cc)) return;
+        int a0 = a, b0 = b, c0 = cc; sort3(a0, b0, c0);
+        if (face_lookup(D, a0, b0, c0) >= 0) return;   // never add a key twice
+        new_face_record(D, a0, b0, c0, pid, RF_LIVE | RF_CHECK);
+      });
+    T.nrem[w] = nrem;
+    T.state[w] = 1;
+  }
+}
+__device__ void t2_reset_body(const Dev& D, const T2Items& T, int final_pass, int start, int stride) {
+  for (int w = start; w < T.n; w += stride) {
+    if (!final_pass && T.state[w] == 1 && T.ncav[w] < 0) continue;
+    t2_for_claims(D, T, w, [&](int tid) { T.own[tid] = INT_MAX; });
+  }
+}
+// retire the removed subface records (after every pass, so lookups in later
+// passes still see the pre-round tables only for untouched keys)
+__device__ void t2_retire_body(const Dev& D, const T2Items& T, int start, int stride) {
+  for (int w = start; w < T.n; w += stride) {
+    const int* rem = T.rem + (size_t)w * T.rcap;
+    for (int k = 0; k < T.nrem[w]; ++k) D.sf_fl[rem[k]] = 0;
+  }
+}
+
+#define GRID_START (blockIdx.x * blockDim.x + threadIdx.x)
+#define GRID_STRIDE (gridDim.x * blockDim.x)
+__global__ void k_t2_compute(Dev D, Cand C, T2Items T, Scr SC) {
+  Scratch S = scratch_for(SC, GRID_START);
+  t2_compute_body(D, C, T, S, GRID_START, GRID_STRIDE);
+}
+__global__ void k_t2_claim(Dev D, Cand C, T2Items T) { t2_claim_body(D, C, T, GRID_START, GRID_STRIDE); }
+__global__ void k_t2_apply(Dev D, Cand C, T2Items T, Scr SC, int* applied) { t2_apply_body(D, C, T, applied, GRID_START, GRID_STRIDE); }
+__global__ void k_t2_commit(Dev D, Cand C, T2Items T, Scr SC) {
+  Scratch S = scratch_for(SC, GRID_START);
+  t2_commit_body(D, C, T, S, GRID_START, GRID_STRIDE);
+}
+__global__ void k_t2_reset(Dev D, Cand C, T2Items T, int final_pass) { t2_reset_body(D, T, final_pass, GRID_START, GRID_STRIDE); }
+__global__ void k_t2_retire(Dev D, T2Items T) { t2_retire_body(D, T, GRID_START, GRID_STRIDE); }
+// every pass of a round in one block: no launches or host reads between passes
+__global__ void __launch_bounds__(128) k_t2_fused(Dev D, Cand C, T2Items T, Scr SC, int* applied_total) {
+  Scratch S = scratch_for(SC, threadIdx.x);
+  __shared__ int s_applied;
+  int left = T.n;
+  for (int pass = 0; left > 0; ++pass) {
+    if (threadIdx.x == 0) s_applied = 0;
+    t2_compute_body(D, C, T, S, threadIdx.x, blockDim.x);
+    __syncthreads();
+    t2_claim_body(D, C, T, threadIdx.x, blockDim.x);
+    __syncthreads();
+    t2_apply_body(D, C, T, &s_applied, threadIdx.x, blockDim.x);
+    __syncthreads();
+    t2_reset_body(D, T, 1, threadIdx.x, blockDim.x);
+    __syncthreads();
+    t2_commit_body(D, C, T, S, threadIdx.x, blockDim.x);
+    __syncthreads();
+    t2_retire_body(D, T, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const int applied = s_applied;
+    __syncthreads();
+    if (applied == 0) { if (threadIdx.x == 0) raise_err(GQ_ERR_2D); break; }
+    left -= applied;
+  }
+  if (threadIdx.x == 0) *applied_total = T.n - left;
+}
+
+__global__ void k_kill_cavities(Dev D, Cand C, Ins I) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < I.n; k += gridDim.x * blockDim.x) {
+    int c = I.list[k];
+    SlabView v = slab(C, c);
+    for (int j = 0; j < C.ntet[c]; ++j) D.alive[v.tets[j]] = 0;
+  }
+}
+__global__ void k_star(Dev D, Cand C, Ins I) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < I.n; k += gridDim.x * blockDim.x) {
+    int c = I.list[k];
+    SlabView v = slab(C, c);
+    star_insert(D, C.vid[c], v.bf, C.nbf[c], C.nt0[c], true);
+  }
+}
+// warp per inserted cavity (serial star for oversized boundaries)
+// global-memory pairing hash for stars of oversized cavities: the big
+// scratch arena of warp gw % SB.nthreads (keys: fkey, partners: tkey/tval)
+__device__ inline StarHash big_star_hash(const Scr& SB, int gw, int* flag) {
+  int slot = gw % SB.nthreads;
+  StarHash h;
+  h.key = SB.fkey + (size_t)slot * SB.fcap;
+  h.v0 = SB.tkey + (size_t)slot * SB.tcap;
+  h.v1 = SB.tval + (size_t)slot * SB.tcap;
+  h.cap = SB.tcap < SB.fcap ? SB.tcap : SB.fcap;
+  h.flag = flag;
+  return h;
+}
+__global__ void __launch_bounds__(32 * WS_WARPS) k_star_warp(Dev D, Cand C, Ins I, Scr SB) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  StarShared& X = reinterpret_cast<StarShared*>(smem_raw)[wib];
+  const int gw = blockIdx.x * WS_WARPS + wib, nw = gridDim.x * WS_WARPS;
+  for (int k = gw; k < I.n; k += nw) {
+    int c = I.list[k];
+    SlabView v = slab(C, c);
+    int nbf = C.nbf[c];
+    if (nbf <= WS_MAXF) star_warp(D, C.vid[c], v.bf, nbf, C.nt0[c], true, star_hash_shared(X), nullptr, 0);
+    else star_warp(D, C.vid[c], v.bf, nbf, C.nt0[c], true, big_star_hash(SB, gw, &X.flag), nullptr, 0);
+    __syncwarp();
+  }
+}
+__global__ void __launch_bounds__(32 * WS_WARPS) k_init_stars_warp(Dev D, Cand C, const int* pend, const int* plist,
+                                                                   const int* acc, int nw_, int* touched, int round, Scr SB) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  StarShared& X = reinterpret_cast<StarShared*>(smem_raw)[wib];
+  const int gw = blockIdx.x * WS_WARPS + wib, nw = gridDim.x * WS_WARPS;
+  for (int w = gw; w < nw_; w += nw) {
+    if (!acc[w]) continue;
+    int c = plist[w];
+    SlabView v = slab(C, c);
+    int nbf = C.nbf[c];
+    if (nbf <= WS_MAXF) star_warp(D, pend[c], v.bf, nbf, C.nt0[c], true, star_hash_shared(X), touched, round);
+    else star_warp(D, pend[c], v.bf, nbf, C.nt0[c], true, big_star_hash(SB, gw, &X.flag), touched, round);
+    __syncwarp();
+    if (lane == 0) C.status[c] = CS_DROP;
+  }
+}
+
+// dirty constraints + survivor mask refresh for subfaces retiled in 2D but
+// not crossed by the 3D cavity (refine.py:720-736)
+__global__ void k_post_insert(Dev D, Cand C, Ins I, T2Items T, Scr SC, const int* item_of) {
+  int tid0 = blockIdx.x * blockDim.x + threadIdx.x;
+  Scratch S = scratch_for(SC, tid0);
+  for (int k = tid0; k < I.n; k += gridDim.x * blockDim.x) {
+    int c = I.list[k];
+    SlabView v = slab(C, c);
+    for (int j = 0; j < C.nbsub[c]; ++j) { int r = v.bsub[j]; if (r >= 0) atomicOr(D.sf_fl + r, D.sf_fl[r] & RF_LIVE ? RF_CHECK : 0u); }
+    for (int j = 0; j < C.nbseg[c]; ++j) { int r = v.bseg[j]; if (r >= 0) atomicOr(D.sg_fl + r, D.sg_fl[r] & RF_LIVE ? RF_CHECK : 0u); }
+    if (C.kind[c] == K_TET || !item_of) continue;
+    for (int w = item_of[2 * k]; w < item_of[2 * k + 1]; ++w) {
+      const int* rem = T.rem + (size_t)w * T.rcap;
+      for (int j = 0; j < T.nrem[w]; ++j) {
+        int rec = rem[j];
+        bool crossed = false;
+        for (int q = 0; q < C.ncr[c]; ++q) if (v.cr[q] == rec) { crossed = true; break; }
+        if (crossed) continue;
+        int4 f = D.sf_v[rec];
+        int slot = find_face(D, f.x, f.y, f.z, S.tset, S.stack, 2 * S.cap);
+        if (slot >= 0) {
+          int t = slot >> 2;
+          refresh_masks(D, t);
+          int u = tnk(D, t, slot & 3) >> 2;
+          if (u >= 0 && D.alive[u]) refresh_masks(D, u);
+        }
+      }
+    }
+  }
+}
+

@@ -1,0 +1,337 @@
+// gq_regions.cuh -- region kernels: candidates, bulk-construction points, oversized cavities, redirects (mesh.py:450-521, refine.py:378-413, 595-662).
+// Part of the single translation unit gq_main.cu (included in order).
+#pragma once
+
+// ===========================================================================
+// kernels
+// ===========================================================================
+
+__global__ void k_make_cands(Dev D, Cand C, Scr SC, int n0, int n1, CandCtx X, SkipLog L, double lmin2) {
+  int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  Scratch S = scratch_for(SC, tid);
+  for (int c = n0 + tid; c < n1; c += gridDim.x * blockDim.x) {
+    C.status[c] = CS_OK;
+    C.bigi[c] = -1;
+    bool ok = make_cand(D, C, c, X, S);
+    if (C.kind[c] == K_TET) {
+      int t = C.tgt[c];
+      if (!ok) {
+        D.skip[t] = 1;
+        int cv[4]; tet_canon(D, t, cv);
+        log_skip(D, L, X.round_no, K_TET, 0, cv, 4);
+        C.status[c] = CS_DROP;
+        continue;
+      }
+      int4 q = D.tv[t];
+      Sphere s;
+      circumsphere_tet(PT(D, q.x), PT(D, q.y), PT(D, q.z), PT(D, q.w), s);
+      if (s.r2 < lmin2) {
+        D.skip[t] = 1;
+        int cv[4]; tet_canon(D, t, cv);
+        log_skip(D, L, X.round_no, K_TET, 1, cv, 4);
+        C.status[c] = CS_DROP;
+      }
+    } else if (!ok) {
+      raise_err(GQ_ERR_DEGEN);
+      C.status[c] = CS_DROP;
+    }
+  }
+}
+
+// region of every candidate in [n0,n1) with status OK (or the listed ones)
+__global__ void k_region(Dev D, Cand C, Scr SC, int n0, int n1, const int* list, int probe, int big) {
+  int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  Scratch S = scratch_for(SC, tid);
+  int n = list ? n1 : n1 - n0;
+  for (int w = tid; w < n; w += gridDim.x * blockDim.x) {
+    int c = list ? list[w] : n0 + w;   // with a list, n0 is the first big slab
+    if (C.status[c] != CS_OK && !(big && C.status[c] == CS_OVF)) continue;
+    if (big) C.bigi[c] = n0 + w;
+    SlabView v = slab(C, c);
+    int seeds[32];
+    int ns = cand_seeds(D, C, c, seeds, S);
+    int pr = probe;
+    if (pr == 3) pr = C.kind[c] == K_TET ? 2 : (C.kind[c] == K_FACE ? 1 : 0);
+    RegionOut O = region_view(C, c, v, pr);
+    atomicAdd(&g_region_calls, 1ull);
+    int st = ns == 0 ? RS_CNSS : region_compute(D, C.p + 3 * (size_t)c, seeds, ns, allow_of(C, c), S, O);
+    store_region(C, c, O);
+    if (st == RS_OK) atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf));
+    if (st == RS_OK) {
+      C.status[c] = (O.mind <= D.too_close_sq) ? CS_TOOCLOSE : CS_OK;
+    } else if (st == RS_OVERFLOW) {
+      C.status[c] = big ? CS_CNSS : CS_OVF;
+      if (big) raise_err(GQ_ERR_CAP);
+    } else if (st == RS_MEMBRANE) {
+      C.status[c] = CS_MEMB; C.memb[c] = O.memb;
+    } else {
+      C.status[c] = CS_CNSS;
+    }
+  }
+}
+
+// coarse grid of inserted vertices: a pending point's first walk starts next
+// to an already inserted vertex instead of at the initial tet
+struct CellHint { double lo[3], inv[3]; int G; int* cellv; };
+__device__ __forceinline__ int cell_of(const CellHint& H, const double* p) {
+  int c[3];
+  for (int k = 0; k < 3; ++k) {
+    double f = (p[k] - H.lo[k]) * H.inv[k];
+    c[k] = f >= 0.0 ? (f < (double)H.G ? (int)f : H.G - 1) : 0;
+  }
+  return (c[0] * H.G + c[1]) * H.G + c[2];
+}
+__global__ void k_init_cellmark(Dev D, CellHint H, const int* pend, const int* plist, const int* acc, int nw) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x)
+    if (acc[w]) { int v = pend[plist[w]]; H.cellv[cell_of(H, PT(D, v))] = v; }
+}
+// one warp per candidate (the common case); overflowing cavities are marked
+// CS_OVF for the block kernel
+#define INIT_BLOCK_ROUTE 192   // bulk construction: cached cavities above this go to the block kernel
+// tiers of the warp region kernel.  Measured on C2: a 128-tet tier at 16 warps
+// / SM plus the 512-tet tier for its overflows is no faster than the 512-tet
+// tier alone (the 4% large cavities cost what the occupancy gains), so both
+// tiers are the large one and the second pass is skipped.
+#define WT1_MAXT 512
+#define WT1_HASH 2048
+#define WT1_MINB 1
+#define WT2_MAXT 512
+#define WT2_HASH 2048
+typedef WarpSharedT<WT1_MAXT, WT1_HASH> WarpShared1;
+typedef WarpSharedT<WT2_MAXT, WT2_HASH> WarpShared2;
+// candidates [n0,n1) (list == nullptr) or list[n0..n1) (the small tier's overflows)
+template <int MAXT, int HASH, int MINB>
+__global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_region_warp(Dev D, Cand C, Scr SC, int n0, int n1, const int* list) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  typedef WarpSharedT<MAXT, HASH> WS;
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WS& W = reinterpret_cast<WS*>(smem_raw)[wib];
+  const int gw = blockIdx.x * WR_WARPS + wib, nw = gridDim.x * WR_WARPS;
+  Scratch S = scratch_for(SC, gw);
+  for (int k = n0 + gw; k < n1; k += nw) {
+    const int c = list ? list[k] : k;
+    if (C.status[c] != (list ? CS_OVF : CS_OK)) continue;
+    DCHK(C.bigi[c] == -1);
+    if (lane == 0) W.nseeds = cand_seeds(D, C, c, W.seeds, S);
+    __syncwarp();
+    int ns = W.nseeds;
+    DCHK(ns >= 0 && ns <= 32);
+    SlabView v = slab(C, c);
+    RegionOut O = region_view(C, c, v, 0);
+    int st = ns == 0 ? RS_CNSS : region_warp(D, C.p + 3 * (size_t)c, W.seeds, ns, allow_of(C, c), W, S, O);
+    if (lane == 0) {
+      atomicAdd(&g_region_calls, 1ull);
+      store_region(C, c, O);
+      if (st == RS_OK) {
+        atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf));
+        C.status[c] = (O.mind <= D.too_close_sq) ? CS_TOOCLOSE : CS_OK;
+      } else if (st == RS_OVERFLOW) C.status[c] = CS_OVF;
+      else if (st == RS_MEMBRANE) { C.status[c] = CS_MEMB; C.memb[c] = O.memb; }
+      else C.status[c] = CS_CNSS;
+    }
+    __syncwarp();
+  }
+}
+// bulk construction, warp per pending point (cached cavities re-validated);
+// redo_ovf: the large tier, run on the small tier's overflows
+template <int MAXT, int HASH, int MINB>
+__global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_init_region_warp(Dev D, Cand C, Scr SC, const int* pend, const int* plist,
+                                                                    int Wn, int* hint, const int* succ, const int* touched, int round,
+                                                                    CellHint H, int redo_ovf) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  typedef WarpSharedT<MAXT, HASH> WS;
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WS& W = reinterpret_cast<WS*>(smem_raw)[wib];
+  const int gw = blockIdx.x * WR_WARPS + wib, nw = gridDim.x * WR_WARPS;
+  Scratch S = scratch_for(SC, gw);
+  for (int w = gw; w < Wn; w += nw) {
+    int c = plist[w];
+    if (lane == 0 && g_wdbg) { g_wdbg[2 * gw] = c; g_wdbg[2 * gw + 1] = 0; }
+    DCHK(c >= 0 && c < C.cap);
+    int st0 = C.status[c];
+    if ((st0 == CS_OVF) != (redo_ovf != 0)) continue;
+    if (st0 == CS_OK && C.memb[c] >= 0) {
+      SlabView v = slab(C, c);
+      bool bad = false;
+      for (int k = lane; k < C.ntet[c]; k += 32) {
+        int t = v.tets[k];
+        if (!D.alive[t] || touched[t] >= C.memb[c]) bad = true;
+      }
+      if (!__any_sync(0xffffffffu, bad)) continue;
+    }
+    // a point whose last cavity was large (a box corner far outside the current
+    // hull, recomputed every round while it waits) goes straight to the block
+    // kernel, which grows it with 256 threads instead of 32
+    if (!redo_ovf && st0 == CS_OK && (C.memb[c] == -2 || (C.memb[c] >= 0 && C.ntet[c] > INIT_BLOCK_ROUTE))) {
+      if (lane == 0) { C.status[c] = CS_OVF; C.memb[c] = -1; }
+      __syncwarp();
+      continue;
+    }
+    int vtx = pend[c];
+    if (lane == 0 && g_wdbg) { g_wdbg[2 * gw] = c; g_wdbg[2 * gw + 1] = 1; }
+    DCHK(vtx >= 0 && vtx < D.vcap);
+    const double* p = PT(D, vtx);
+    if (lane == 0) {
+      int h = hint[c];
+      DCHK(h >= -1 && h < D.tcap);
+      if (h < 0) {                      // first walk: start beside a nearby inserted vertex
+        int cv = H.cellv[cell_of(H, p)];
+        h = cv >= 0 ? D.vert_tet[cv] : 0;
+      }
+      while (h >= 0 && !D.alive[h]) h = succ[h];
+      // a ghost hint (last seen outside the hull) restarts at the hull tet behind
+      // it: walk() would otherwise rescan the tet array for a real tet.  The
+      // unconstrained cavity does not depend on the seed.
+      if (h >= 0 && D.tv[h].w == GHOST) h = tnk(D, h, 3) >> 2;
+      int t = walk(D, p, h);
+      hint[c] = t;
+      W.seeds[0] = t;
+    }
+    __syncwarp();
+    SlabView sv = slab(C, c);
+    RegionOut O = region_view(C, c, sv, 0);
+    Allow A; A.n = 0;
+    if (lane == 0 && g_wdbg) g_wdbg[2 * gw + 1] = 2;
+    int r = region_warp(D, p, W.seeds, 1, A, W, S, O, true);
+    if (lane == 0 && g_wdbg) g_wdbg[2 * gw + 1] = 99;
+    if (lane == 0) {
+      atomicAdd(&g_region_calls, 1ull);
+      store_region(C, c, O);
+      C.extra[c] = -1; C.kind[c] = K_TET; C.rank[c] = c; C.memb[c] = round;
+      if (r == RS_OK) { C.status[c] = CS_OK; atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf)); }
+      else if (r == RS_OVERFLOW) { C.status[c] = CS_OVF; C.memb[c] = -1; }
+      else { C.status[c] = CS_CNSS; raise_err(GQ_ERR_DEGEN); }
+    }
+    __syncwarp();
+  }
+}
+
+// oversized cavities: one block per candidate (threads in proportion to
+// region size); big slabs base+w
+__global__ void __launch_bounds__(BR_THREADS) k_region_block(Dev D, Cand C, Scr SB, const int* list, int nb, int base) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BlockShared& B = *reinterpret_cast<BlockShared*>(smem_raw);
+  Scratch S = scratch_for(SB, blockIdx.x);
+  for (int w = blockIdx.x; w < nb; w += gridDim.x) {
+    int c = list[w];
+    if (threadIdx.x == 0) C.bigi[c] = base + w;
+    __syncthreads();
+    SlabView v = slab(C, c);
+    __shared__ int s_seeds[32];
+    __shared__ int s_ns;
+    if (threadIdx.x == 0) s_ns = cand_seeds(D, C, c, s_seeds, S);
+    __syncthreads();
+    RegionOut O = region_view(C, c, v, 0);
+    int st = s_ns == 0 ? RS_CNSS : region_block(D, C.p + 3 * (size_t)c, s_seeds, s_ns, allow_of(C, c), B, S, O);
+    if (threadIdx.x == 0) {
+      atomicAdd(&g_region_calls, 1ull);
+      store_region(C, c, O);
+      if (st == RS_OK) {
+        atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf));
+        C.status[c] = (O.mind <= D.too_close_sq) ? CS_TOOCLOSE : CS_OK;
+      } else if (st == RS_OVERFLOW) { C.status[c] = CS_CNSS; raise_err(GQ_ERR_CAP); }
+      else if (st == RS_MEMBRANE) { C.status[c] = CS_MEMB; C.memb[c] = O.memb; }
+      else C.status[c] = CS_CNSS;
+    }
+    __syncthreads();
+  }
+}
+__global__ void __launch_bounds__(BR_THREADS) k_init_region_block(Dev D, Cand C, Scr SB, const int* pend, const int* list, int nb,
+                                                                  int* hint, const int* succ, int round) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BlockShared& B = *reinterpret_cast<BlockShared*>(smem_raw);
+  Scratch S = scratch_for(SB, blockIdx.x);
+  for (int w = blockIdx.x; w < nb; w += gridDim.x) {
+    int c = list[w];
+    __shared__ int s_t;
+    if (threadIdx.x == 0) {
+      C.bigi[c] = w;
+      const double* p = PT(D, pend[c]);
+      int h = hint[c];
+      if (h < 0) h = 0;
+      while (h >= 0 && !D.alive[h]) h = succ[h];
+      if (h >= 0 && D.tv[h].w == GHOST) h = tnk(D, h, 3) >> 2;
+      s_t = walk(D, p, h);
+      hint[c] = s_t;
+    }
+    __syncthreads();
+    SlabView v = slab(C, c);
+    RegionOut O = region_view(C, c, v, 0);
+    int seeds[1] = {s_t};
+    Allow A; A.n = 0;
+    int st = region_block(D, PT(D, pend[c]), seeds, 1, A, B, S, O);
+    if (threadIdx.x == 0) {
+      atomicAdd(&g_region_calls, 1ull);
+      store_region(C, c, O);
+      C.extra[c] = -1; C.kind[c] = K_TET; C.rank[c] = c; C.memb[c] = round;
+      if (st == RS_OK) { C.status[c] = CS_OK; atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf)); }
+      else if (st == RS_OVERFLOW) { C.status[c] = CS_OVF; C.memb[c] = -1; raise_err(GQ_ERR_CAP); }
+      else { C.status[c] = CS_CNSS; raise_err(GQ_ERR_DEGEN); }
+    }
+    __syncthreads();
+  }
+}
+
+// redirect decision (refine.py:595-613, 615-662); marks records RF_REDIR
+__global__ void k_redirect(Dev D, Cand C, int n0, int n1, int* nredir) {
+  for (int c = n0 + blockIdx.x * blockDim.x + threadIdx.x; c < n1; c += gridDim.x * blockDim.x) {
+    int kind = C.kind[c];
+    if (kind == K_SEG || C.status[c] == CS_DROP) continue;
+    int ns = C.nrseg[c], nf = C.nrface[c];
+    if (ns > 0) {
+      for (int k = 0; k < ns; ++k) atomicOr(D.sg_fl + C.rseg[(size_t)c * CRD + k], RF_REDIR);
+      atomicAdd(nredir, 1);
+      C.status[c] = CS_DROP;
+    } else if (kind == K_TET && nf > 0) {
+      for (int k = 0; k < nf; ++k) atomicOr(D.sf_fl + C.rface[(size_t)c * CRD + k], RF_REDIR);
+      atomicAdd(nredir + 1, 1);
+      C.status[c] = CS_DROP;
+    } else if (kind == K_TET) {
+      // refine.py:378-413 hull-exit walk from the tet toward its circumcentre
+      int t = C.tgt[c];
+      const double* p = C.p + 3 * (size_t)c;
+      int cur = t, prev = -1;
+      int max_steps = walk_cap(D, 64);
+      int hull = -2;   // -2 none, >=0 face rec, -1 not a subface
+      bool done = false;
+      for (int step = 0; step < max_steps && !done; ++step) {
+        int4 q = D.tv[cur];
+        if (q.w == GHOST) {
+          int a = q.x, b = q.y, cc = q.z; sort3(a, b, cc);
+          hull = face_lookup(D, a, b, cc); done = true; break;
+        }
+        bool moved = false;
+        for (int k = 0; k < 4; ++k) {
+          int i = (k + step) & 3;
+          int u = tnk(D, cur, i) >> 2;
+          if (u == prev) continue;
+          int f[3]; face_verts(q, i, f);
+          if (orient3d(PT(D, f[0]), PT(D, f[1]), PT(D, f[2]), p) > 0) {
+            if (D.tv[u].w == GHOST) {
+              sort3(f[0], f[1], f[2]);
+              hull = face_lookup(D, f[0], f[1], f[2]); done = true; break;
+            }
+            prev = cur; cur = u; moved = true; break;
+          }
+        }
+        if (done) break;
+        if (!moved) { hull = -2; done = true; break; }
+      }
+      if (!done) {
+        int end = walk(D, p, t);
+        if (end >= 0 && D.tv[end].w == GHOST) {
+          int4 q = D.tv[end];
+          int a = q.x, b = q.y, cc = q.z; sort3(a, b, cc);
+          hull = face_lookup(D, a, b, cc);
+        }
+      }
+      if (hull >= 0 && !(D.sf_fl[hull] & RF_SKIP)) {
+        atomicOr(D.sf_fl + hull, RF_REDIR);
+        atomicAdd(nredir + 1, 1);
+        C.status[c] = CS_DROP;
+      }
+    }
+  }
+}
+
+
