@@ -92,11 +92,15 @@ __global__ void k_init_cellmark(Dev D, CellHint H, const int* pend, const int* p
 // / SM plus the 512-tet tier for its overflows is no faster than the 512-tet
 // tier alone (the 4% large cavities cost what the occupancy gains), so both
 // tiers are the large one and the second pass is skipped.
+#ifndef WT1_MAXT
 #define WT1_MAXT 512
 #define WT1_HASH 2048
 #define WT1_MINB 1
+#endif
+#ifndef WT2_MAXT
 #define WT2_MAXT 512
 #define WT2_HASH 2048
+#endif
 typedef WarpSharedT<WT1_MAXT, WT1_HASH> WarpShared1;
 typedef WarpSharedT<WT2_MAXT, WT2_HASH> WarpShared2;
 // candidates [n0,n1) (list == nullptr) or list[n0..n1) (the small tier's overflows)

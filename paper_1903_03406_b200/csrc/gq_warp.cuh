@@ -30,7 +30,9 @@ __device__ volatile int* g_wdbg;      // pinned host mirror: [warp][2] = candida
 #ifndef CC_DBG
 #define CC_DBG 96
 #endif
+#ifndef WR_WARPS
 #define WR_WARPS 8          // warps per block
+#endif
 
 // Two instantiations: a small tier (128 tets, 6.5 KB per warp) that runs at
 // 16 warps / SM for the common cavities, and a large tier (512 tets, 25 KB per
@@ -38,7 +40,7 @@ __device__ volatile int* g_wdbg;      // pinned host mirror: [warp][2] = candida
 template <int MAXT, int HASH>
 struct WarpSharedT {
   int hkey[HASH];
-  int hval[HASH];
+  short hval[HASH];          // cavity index (< MAXT) or -2 (tested, outside)
   int cav[MAXT];
   int f0[MAXT];
   int f1[MAXT];
@@ -342,10 +344,10 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
   if (!__any_sync(FULL, cons)) return RS_OK;
   WSTOP(7);
   // occurrences: code = a << 4 | slot (slot 0-3 subface face, 4-9 subsegment edge)
-  int* oc = W.hkey;                  // hkey / hval / cav / comp / in are free after the swallow check
-  int* k0 = W.cav; int* k1 = W.comp; int* k2 = W.hval;
+  int* oc = W.hkey;                  // hkey / cav / comp / in are free after the swallow check
+  int* k0 = W.cav; int* k1 = W.comp; int* k2 = W.hkey + WR_HASH / 2;
   unsigned char* ofirst = W.in;
-  const int OCAP = WR_MAXT;
+  const int OCAP = WR_MAXT < WR_HASH / 2 ? WR_MAXT : WR_HASH / 2;
   int myocc = 0;
   for (int a = lo; a < hi; ++a) {
     int t = W.f0[a];
