@@ -16,8 +16,8 @@
 #define CS_DROP 5      // redirected / skipped before the pool
 
 // slab capacities (normal pass); overflowing candidates rerun with big slabs
-#define CT 512
-#define CF 1088
+#define CT 256
+#define CF 576
 #define CC 96
 #define CRD 64
 #define CTB 4096

@@ -88,18 +88,21 @@ __global__ void k_init_cellmark(Dev D, CellHint H, const int* pend, const int* p
 // one warp per candidate (the common case); overflowing cavities are marked
 // CS_OVF for the block kernel
 #define INIT_BLOCK_ROUTE 192   // bulk construction: cached cavities above this go to the block kernel
-// tiers of the warp region kernel.  Measured on C2: a 128-tet tier at 16 warps
-// / SM plus the 512-tet tier for its overflows is no faster than the 512-tet
-// tier alone (the 4% large cavities cost what the occupancy gains), so both
-// tiers are the large one and the second pass is skipped.
+// tiers of the warp region kernel.  Measured on C2 (device ms for the region
+// stages): one 512-tet tier with a 2048-slot hash 206; one 256-tet tier with a
+// 1024-slot hash 195 (half the shared memory leaves more L1 for the mesh
+// gathers; the <1% cavities above 256 tets go to the block kernel); a 128- or
+// 256-tet tier in front of a 512-tet tier is slower (the second pass and its
+// read-back cost more than they save).  So one tier, and the second pass is
+// compiled out unless WT2 differs.
 #ifndef WT1_MAXT
-#define WT1_MAXT 512
-#define WT1_HASH 2048
+#define WT1_MAXT 256
+#define WT1_HASH 1024
 #define WT1_MINB 1
 #endif
 #ifndef WT2_MAXT
-#define WT2_MAXT 512
-#define WT2_HASH 2048
+#define WT2_MAXT WT1_MAXT
+#define WT2_HASH WT1_HASH
 #endif
 typedef WarpSharedT<WT1_MAXT, WT1_HASH> WarpShared1;
 typedef WarpSharedT<WT2_MAXT, WT2_HASH> WarpShared2;
