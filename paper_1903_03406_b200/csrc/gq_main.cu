@@ -77,6 +77,16 @@ int gq_create(int device, gq_ctx** out) {
     if (WT1_MAXT != WT2_MAXT)
       CK(cudaFuncSetAttribute(k_init_region_warp<WT2_MAXT, WT2_HASH, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared2))));
     CK(cudaFuncSetAttribute(k_init_region_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BlockShared)));
+    // the region kernels gather mesh data through L1 (C2: 163 ms at the driver's
+    // default carveout, 200 ms with all 228 KB as shared memory); GQ_CARVEOUT
+    // overrides the driver's choice for experiments
+    if (getenv("GQ_CARVEOUT")) {
+      int pct = atoi(getenv("GQ_CARVEOUT"));
+      if (pct > 0 && pct <= 100) {
+        CK(cudaFuncSetAttribute(k_region_warp<WT1_MAXT, WT1_HASH, WT1_MINB>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        CK(cudaFuncSetAttribute(k_init_region_warp<WT1_MAXT, WT1_HASH, WT1_MINB>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+      }
+    }
   } catch (std::exception& e) {
     c->err = e.what();
     *out = c;
