@@ -38,6 +38,15 @@ struct Counters {
   int pad;
 };
 
+// A tet is one 32-byte record {tv, tn} (vertices, then packed neighbour
+// links): a cavity step that reads both touches one sector pair of one line.
+// TetRow is one half of the interleaved array, indexed like a plain array.
+struct TetRow {
+  int4* p;          // record r of this half is p[2 r]
+  __host__ __device__ __forceinline__ int4& operator[](size_t r) const { return p[2 * r]; }
+  __host__ __device__ __forceinline__ int4* operator+(size_t r) const { return p + 2 * r; }
+};
+
 struct Dev {
   // vertices
   double* P;
@@ -45,9 +54,9 @@ struct Dev {
   int* vert_tet;
   int* vsid;
   int vcap;
-  // tets
-  int4* tv;
-  int4* tn;
+  // tets: interleaved {tv, tn} records (tv.p is the allocation)
+  TetRow tv;
+  TetRow tn;
   uint8_t* alive;
   uint8_t* sub;
   uint8_t* seg;

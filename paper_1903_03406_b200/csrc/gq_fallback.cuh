@@ -231,7 +231,7 @@ __global__ void k_compact_flags(Dev D, int* flags) {
   int nt = D.ctr->nt;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) flags[t] = D.alive[t] == 1;
 }
-__global__ void k_compact_move(Dev D, const int* remap, int nt, int4* tv2, int4* tn2, uint8_t* sub2, uint8_t* seg2,
+__global__ void k_compact_move(Dev D, const int* remap, int nt, TetRow tv2, TetRow tn2, uint8_t* sub2, uint8_t* seg2,
                                double* ratio2, uint8_t* skip2) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
     if (D.alive[t] != 1) continue;

@@ -102,7 +102,7 @@ struct gq_ctx {
   int big_used = 0;
   int init_rounds = 0;
   long long grid_calls = 0;
-  int4 *tv2 = nullptr, *tn2 = nullptr; uint8_t *sub2 = nullptr, *seg2 = nullptr, *skip2 = nullptr; double* ratio2 = nullptr;
+  int4* tvn2 = nullptr; uint8_t *sub2 = nullptr, *seg2 = nullptr, *skip2 = nullptr; double* ratio2 = nullptr;
   struct QBuf { int *a, *b, *c, *d, *e, *f, *g, *h; size_t cap; } Q{};
   bool allocated = false;
 };
@@ -297,7 +297,7 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   D.vcap = (int)vcap; D.tcap = (int)tcap;
   D.P = dmalloc<double>(3 * vcap); D.vorigin = dmalloc<uint8_t>(vcap); D.vert_tet = dmalloc<int>(vcap);
   D.vsid = dmalloc<int>(vcap);
-  D.tv = dmalloc<int4>(tcap); D.tn = dmalloc<int4>(tcap); D.alive = dmalloc<uint8_t>(tcap);
+  D.tv.p = dmalloc<int4>(2 * tcap); D.tn.p = D.tv.p + 1; D.alive = dmalloc<uint8_t>(tcap);
   D.sub = dmalloc<uint8_t>(tcap); D.seg = dmalloc<uint8_t>(tcap); D.skip = dmalloc<uint8_t>(tcap);
   D.ratio = dmalloc<double>(tcap);
   CK(cudaMemset(D.alive, 0, tcap));
@@ -376,7 +376,7 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
 static void free_all(gq_ctx* c) {
   if (!c->allocated) return;
   Dev& D = c->D;
-  void* ps[] = {D.P, D.vorigin, D.vert_tet, D.vsid, D.tv, D.tn, D.alive, D.sub, D.seg, D.skip, D.ratio, D.sg_uv,
+  void* ps[] = {D.P, D.vorigin, D.vert_tet, D.vsid, D.tv.p, D.alive, D.sub, D.seg, D.skip, D.ratio, D.sg_uv,
                 D.sg_sid, D.sg_fl, D.sg_hk, D.sg_hv, D.sf_v, D.sf_fl, D.sf_hk, D.sf_hv, D.t2v, D.t2alive, D.he_hk,
                 D.he_hv, D.t2count, D.poly_keep, D.poly_obl, D.t2last, D.segpoly_off, D.segpoly, D.sid_uv, c->dctr, c->W.own, c->T.cand,
                 c->T.pid, c->T.state, c->T.cav, c->T.ncav, c->T.rem, c->T.nrem, c->T.own, c->L.rows, c->d_int,
@@ -384,14 +384,14 @@ static void free_all(gq_ctx* c) {
                 c->S.comp, c->SB.tkey, c->SB.tval, c->SB.tep, c->SB.fkey, c->SB.fep, c->SB.epoch, c->SB.list,
                 c->SB.stack, c->SB.in, c->SB.comp, c->tmpA, c->tmpB, c->tmpC, c->k64a, c->k64b, c->k32a, c->k32b,
                 c->cub_tmp, c->d_order, c->G.start, c->G.codes, c->G.cnt, c->G.nbig, c->Q.a, c->Q.b, c->Q.c,
-                c->Q.d, c->Q.e, c->Q.f, c->Q.g, c->Q.h, c->tv2, c->tn2, c->sub2, c->seg2, c->skip2, c->ratio2};
+                c->Q.d, c->Q.e, c->Q.f, c->Q.g, c->Q.h, c->tvn2, c->sub2, c->seg2, c->skip2, c->ratio2};
   for (void* p : ps) if (p) dfree(p);
   free_cands(c->C);
   c->allocated = false;
   c->tmpcap = 0; c->cub_cap = 0; c->cub_tmp = nullptr;
   c->tmpA = c->tmpB = c->tmpC = nullptr; c->k64a = c->k64b = nullptr; c->k32a = c->k32b = nullptr; c->d_order = nullptr;
   c->Q = {};
-  c->tv2 = c->tn2 = nullptr; c->sub2 = c->seg2 = c->skip2 = nullptr; c->ratio2 = nullptr;
+  c->tvn2 = nullptr; c->sub2 = c->seg2 = c->skip2 = nullptr; c->ratio2 = nullptr;
 }
 
 // regions for candidates [n0,n1): normal pass, then the overflow ones with big slabs
@@ -635,14 +635,16 @@ static void compact_tets(gq_ctx* c) {
   int na = last_scan + last_flag;
   Dev& D = c->D;
   // double buffers, allocated once per context
-  if (!c->tv2) {
-    c->tv2 = dmalloc<int4>(D.tcap); c->tn2 = dmalloc<int4>(D.tcap);
+  if (!c->tvn2) {
+    c->tvn2 = dmalloc<int4>(2 * (size_t)D.tcap);
     c->sub2 = dmalloc<uint8_t>(D.tcap); c->seg2 = dmalloc<uint8_t>(D.tcap);
     c->ratio2 = dmalloc<double>(D.tcap); c->skip2 = dmalloc<uint8_t>(D.tcap);
   }
-  LAUNCH(k_compact_move, nt, D, c->tmpB, nt, c->tv2, c->tn2, c->sub2, c->seg2, c->ratio2, c->skip2);
+  TetRow tv2{c->tvn2}, tn2{c->tvn2 + 1};
+  LAUNCH(k_compact_move, nt, D, c->tmpB, nt, tv2, tn2, c->sub2, c->seg2, c->ratio2, c->skip2);
   LAUNCH(k_compact_vt, c->hc.nv, D, c->tmpB, c->tmpA, c->hc.nv);
-  std::swap(D.tv, c->tv2); std::swap(D.tn, c->tn2); std::swap(D.sub, c->sub2); std::swap(D.seg, c->seg2);
+  c->tvn2 = D.tv.p; D.tv = tv2; D.tn = tn2;
+  std::swap(D.sub, c->sub2); std::swap(D.seg, c->seg2);
   std::swap(D.ratio, c->ratio2); std::swap(D.skip, c->skip2);
   CK(cudaMemsetAsync(D.alive, 0, nt, c->st));
   CK(cudaMemsetAsync(D.alive, 1, na, c->st));

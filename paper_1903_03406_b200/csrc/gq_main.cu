@@ -136,8 +136,8 @@ int gq_export_mesh(gq_ctx* c, double* points, uint8_t* vert_origin, int32_t* ver
     if (points) CK(cudaMemcpy(points, D.P, 24 * nv, cudaMemcpyDeviceToHost));
     if (vert_origin) CK(cudaMemcpy(vert_origin, D.vorigin, nv, cudaMemcpyDeviceToHost));
     if (vert_tet) CK(cudaMemcpy(vert_tet, D.vert_tet, 4 * nv, cudaMemcpyDeviceToHost));
-    if (tv) CK(cudaMemcpy(tv, D.tv, 16 * nt, cudaMemcpyDeviceToHost));
-    if (tn) CK(cudaMemcpy(tn, D.tn, 16 * nt, cudaMemcpyDeviceToHost));
+    if (tv && nt) CK(cudaMemcpy2D(tv, 16, D.tv.p, 32, 16, nt, cudaMemcpyDeviceToHost));   // strided halves of the records
+    if (tn && nt) CK(cudaMemcpy2D(tn, 16, D.tn.p, 32, 16, nt, cudaMemcpyDeviceToHost));
     if (alive) CK(cudaMemcpy(alive, D.alive, nt, cudaMemcpyDeviceToHost));
     if (sub_mask) CK(cudaMemcpy(sub_mask, D.sub, nt, cudaMemcpyDeviceToHost));
     if (seg_mask) CK(cudaMemcpy(seg_mask, D.seg, nt, cudaMemcpyDeviceToHost));
