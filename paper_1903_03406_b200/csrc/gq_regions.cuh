@@ -87,7 +87,11 @@ __global__ void k_init_cellmark(Dev D, CellHint H, const int* pend, const int* p
 }
 // one warp per candidate (the common case); overflowing cavities are marked
 // CS_OVF for the block kernel
-#define INIT_BLOCK_ROUTE 192   // bulk construction: cached cavities above this go to the block kernel
+// bulk construction: cached cavities above this go straight to the block kernel
+// (C2 at window 1/32: 96, 128, 192 or never all measure the same)
+#ifndef INIT_BLOCK_ROUTE
+#define INIT_BLOCK_ROUTE (WT1_MAXT * 3 / 4)
+#endif
 // tiers of the warp region kernel.  Measured on C2 (device ms for the region
 // stages): one 512-tet tier with a 2048-slot hash 206; one 256-tet tier with a
 // 1024-slot hash 195 (half the shared memory leaves more L1 for the mesh
