@@ -707,6 +707,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
   // strict-order dependency chain, not the window, so a small window only saves work
   double wf = getenv("GQ_INIT_WINDOW") ? atof(getenv("GQ_INIT_WINDOW")) : 0.03125;   // C2 sweep: 1/64 150, 1/32 132, 1/16 143, 1/8 167 ms
   fine(c, -1);
+  int novf_last = 0;
   for (int round = 0; left > 0; ++round) {
     int W = (int)std::min<double>(left, std::max(64.0, wf * inserted));
     fine(c, 22);
@@ -745,9 +746,12 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     }
     region_end(c);
     fine(c, 0);
-    // big cavities (early rounds): resolve the lowest-order ones, truncate the window at the rest
+    // big cavities (early rounds): resolve the lowest-order ones, truncate the window at the rest.
+    // Only after a round that reported overflowed points in its window: otherwise the
+    // cooperative filter below cuts the window at the first new one on the device, and
+    // the block kernel picks it up next round -- no read-back here in the common case.
     std::vector<int> bl;
-    {
+    if (novf_last > 0 || g_trace || getenv("GQ_INIT_LAUNCHES")) {
       CK(cudaMemsetAsync(c->d_int + 40, 0, 8, c->st));
       LAUNCH(k_count_ovf, W, C, d_plist, W, c->d_int + 40);
       int novf = read_int(c, c->d_int + 40);
@@ -811,10 +815,10 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
       void* args[] = {&c->D, &C, &c->W, &d_plist, &W, &nt, &d_acc, &d_plist2, &d_scan, &tot, &d_succ};
       CK(cudaLaunchCooperativeKernel((void*)k_init_filter_coop, dim3(blocks), dim3(256), args, 0, c->st));
       c->launches++;
-      int h2[2];
-      CK(cudaMemcpyAsync(h2, tot, 8, cudaMemcpyDeviceToHost, c->st));
+      int h2[4];
+      CK(cudaMemcpyAsync(h2, tot, 16, cudaMemcpyDeviceToHost, c->st));
       sync(c);
-      nacc = h2[0]; add_t = h2[1];
+      nacc = h2[0]; add_t = h2[1]; novf_last = h2[2];
       if (nt + add_t > c->D.tcap) throw std::runtime_error("tet capacity exceeded in init");
       fine(c, 3);
     } else {   // debug path: one launch per pass
@@ -868,7 +872,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     inserted += nacc;
     c->hc.nt = nt;
     push(c);
-    if (nacc == 0) throw std::runtime_error("init made no progress");
+    if (nacc == 0 && novf_last == 0) throw std::runtime_error("init made no progress");
     c->init_rounds = round + 1;
     fine(c, 6);
   }

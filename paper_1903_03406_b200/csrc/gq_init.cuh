@@ -130,12 +130,22 @@ __global__ void k_init_unclaim(Dev D, Cand C, Owners W, const int* plist, int nw
 // one cooperative kernel: a warp per window point walks its claims
 // lane-parallel; block 0 scans acceptance and boundary-face counts between the
 // barriers; totals go to tot[0] (accepted) and tot[1] (new tets).
-__global__ void __launch_bounds__(256) k_init_filter_coop(Dev D, Cand C, Owners W, const int* plist, int nw, int nt,
+__global__ void __launch_bounds__(256) k_init_filter_coop(Dev D, Cand C, Owners W, const int* plist, int nw_in, int nt,
                                                           int* acc, int* accscan, int* nbfscan, int* tot, int* succ) {
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
   const unsigned FULL = 0xffffffffu;
+  // the window ends before the first point whose cavity overflowed the warp
+  // kernel (it is computed by the block kernel next round): tot[3] = window,
+  // tot[2] = overflowed points in the window
+  if (blockIdx.x == 0 && threadIdx.x == 0) { tot[2] = 0; tot[3] = nw_in; }
+  grid.sync();
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw_in; w += gridDim.x * blockDim.x)
+    if (C.status[plist[w]] == CS_OVF) { atomicMin(tot + 3, w); atomicAdd(tot + 2, 1); }
+  grid.sync();
+  const int nw = *(volatile int*)(tot + 3);
+  for (int w = nw + blockIdx.x * blockDim.x + threadIdx.x; w < nw_in; w += gridDim.x * blockDim.x) acc[w] = 0;
   for (int w = gw; w < nw; w += nwarp) {                    // claim: lowest order wins
     const int c = plist[w];
     warp_claims(D, C, W, c, lane, [&](int k) { atomicMin(W.own + k, c); });
@@ -157,15 +167,15 @@ __global__ void __launch_bounds__(256) k_init_filter_coop(Dev D, Cand C, Owners 
     __shared__ int carry[2];
     if (threadIdx.x == 0) carry[0] = carry[1] = 0;
     __syncthreads();
-    for (int b0 = 0; b0 < nw; b0 += 256) {
+    for (int b0 = 0; b0 < nw_in; b0 += 256) {   // the whole window: acc is 0 past the cut
       const int w = b0 + threadIdx.x;
-      const int a = w < nw ? acc[w] : 0;
+      const int a = w < nw_in ? acc[w] : 0;
       const int f = a ? C.nbf[plist[w]] : 0;
       int sa, sf, ta, tf;
       BS(ts).ExclusiveSum(a, sa, ta);
       __syncthreads();
       BS(ts).ExclusiveSum(f, sf, tf);
-      if (w < nw) { accscan[w] = carry[0] + sa; nbfscan[w] = carry[1] + sf; }
+      if (w < nw_in) { accscan[w] = carry[0] + sa; nbfscan[w] = carry[1] + sf; }
       __syncthreads();
       if (threadIdx.x == 0) { carry[0] += ta; carry[1] += tf; }
       __syncthreads();
