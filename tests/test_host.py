@@ -69,27 +69,3 @@ def test_generators_deterministic():
     assert validate(t) == [] and len(t.polygons) == 4
     g = synth.generate(synth.SynthSpec(100, 0.05, "cube", 0))
     assert len(g.polygons) == 5 and validate(g) == []
-
-
-def test_curved_hull_gets_box_and_corners_first():
-    """A polygon-tiled hull that is not a box (an icosphere) gets the padded box
-    too, and the insertion order starts with its 8 corners (prepare.insertion_order)."""
-    from paper_1903_03406_b200.plc import box_mode
-    from paper_1903_03406_b200.synth import _icosphere
-
-    V, F = _icosphere(1, 1.0)
-    segs = sorted({(min(a, b), max(a, b)) for f in F for a, b in ((f[0], f[1]), (f[1], f[2]), (f[2], f[0]))})
-    sph = PLC(points=[tuple(float(x) for x in p) for p in V], segments=segs, polygons=[tuple(int(x) for x in f) for f in F])
-    assert hull_covered(sph) and box_mode(sph) == "curved"
-    assert box_mode(synth.cube_points(10, 0)) == "none"
-    assert box_mode(synth.segments_cloud(50, 2, 0)) == "uncovered"
-    p = prepare(sph, seed=0)
-    n = len(sph.points)
-    assert p.points.shape == (n + 8, 3)
-    assert sorted(p.order[:8].tolist()) == list(range(n, n + 8))
-    assert sorted(p.order.tolist()) == list(range(n + 8))
-    first4 = p.points[p.order[:4]]
-    assert abs(np.linalg.det(first4[1:] - first4[0])) > 0       # non-coplanar start
-    # parity inputs keep the reference's shuffle exactly
-    q = prepare(synth.segments_cloud(50, 2, 0), seed=0)
-    assert q.order.tolist() == shuffle_order(len(q.points), 0).tolist()
