@@ -387,37 +387,11 @@ def hull_covered(plc: PLC) -> bool:
     return True
 
 
-def _hull_is_bbox(plc: PLC) -> bool:
-    """True when the 8 bounding-box corners are input points, i.e. the convex
-    hull is the axis-aligned box.  Deviation from refine.py:462-506, which
-    keeps a polygon-tiled hull of any shape: on a curved hull (C4's outer
-    icosphere) the rounded midpoint of a hull edge lands just outside the hull,
-    its cavity takes in the ghost tets on both sides of the edge and the star
-    pinches.  The reference never reaches that point (it crashes on oblique
-    facets in Tri2D), so such inputs get the padded box too; every
-    reference-parity input (box hulls, or hulls not tiled at all) is unchanged."""
-    lo, hi = bounding_box(plc)
-    pts = {tuple(p) for p in plc.points}
-    return all((hi[0] if i else lo[0], hi[1] if j else lo[1], hi[2] if k else lo[2]) in pts
-               for i in (0, 1) for j in (0, 1) for k in (0, 1))
-
-
-def box_mode(plc: PLC) -> str:
-    """'none' (the polygons tile a box hull: no closure), 'uncovered' (the
-    reference's padded box, refine.py:462-506) or 'curved' (tiled hull that is
-    not a box: padded box too, see _hull_is_bbox)."""
-    if not plc.polygons:
-        return "uncovered"
-    if _hull_is_bbox(plc):
-        return "none" if hull_covered(plc) else "uncovered"
-    return "curved" if hull_covered(plc) else "uncovered"
-
-
-def augment_with_box(plc: PLC, mode: str | None = None) -> PLC:
+def augment_with_box(plc: PLC) -> PLC:
     """Wrap the points in an axis-aligned box padded by 0.25*diag unless the
     polygons already tile the hull (refine.py:462-506); corners, edges and
     faces are appended after the input features in the same order."""
-    if (mode or box_mode(plc)) == "none":
+    if plc.polygons and hull_covered(plc):
         return plc
     lo, hi = bounding_box(plc)
     pad = 0.25 * math.dist(lo, hi)

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .errors import AllCoplanar, DuplicatePoint, InvalidPLC
-from .plc import PLC, augment_with_box, box_mode, points_array, validate
+from .plc import PLC, augment_with_box, points_array, validate
 
 
 @dataclass
@@ -36,20 +36,6 @@ def shuffle_order(n: int, seed: int) -> np.ndarray:
     return np.asarray(order, dtype=np.int32)
 
 
-def insertion_order(n: int, n_input: int, seed: int, mode: str) -> np.ndarray:
-    """The reference's shuffle (mesh.py:878-880), except for a box added around
-    a curved polygon-tiled hull (plc.box_mode 'curved', no reference
-    counterpart): there the 8 corners go first, starting with a non-coplanar
-    inscribed tet, so every later point lands inside the hull.  Inserted at a
-    random time instead, a corner sees thousands of the curved hull's facets at
-    once and its cavity outgrows the block-cooperative region kernel."""
-    order = shuffle_order(n, seed)
-    if mode != "curved":
-        return order
-    corners = np.asarray([0, 6, 5, 3, 7, 1, 2, 4], dtype=np.int32) + n_input
-    return np.concatenate([corners, order[order < n_input]]).astype(np.int32)
-
-
 def prepare(plc: PLC, seed: int = 0, check: bool = True) -> Prepared:
     import time
 
@@ -58,8 +44,7 @@ def prepare(plc: PLC, seed: int = 0, check: bool = True) -> Prepared:
         violations = validate(plc)
         if violations:
             raise InvalidPLC(violations)
-    mode = box_mode(plc)
-    aug = augment_with_box(plc, mode)
+    aug = augment_with_box(plc)
     if aug is plc:
         pts = np.ascontiguousarray(points_array(plc))
     else:   # input points (converted once already) + the 8 box corners
@@ -78,7 +63,7 @@ def prepare(plc: PLC, seed: int = 0, check: bool = True) -> Prepared:
         off.append(len(idx))
     return Prepared(plc=aug, n_input=len(plc.points), points=pts, segments=segs,
                     poly_off=np.asarray(off, dtype=np.int32), poly_idx=np.asarray(idx, dtype=np.int32),
-                    order=insertion_order(len(pts), len(plc.points), seed, mode), setup_s=time.perf_counter() - t0)
+                    order=shuffle_order(len(pts), seed), setup_s=time.perf_counter() - t0)
 
 
 def facet_keep(plc: PLC) -> np.ndarray:
