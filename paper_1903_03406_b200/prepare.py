@@ -30,10 +30,12 @@ class Prepared:
 
 
 def shuffle_order(n: int, seed: int) -> np.ndarray:
-    """mesh.py:878-880: list(range(n)) shuffled in place by default_rng(seed)."""
-    order = list(range(n))
+    """mesh.py:878-880: list(range(n)) shuffled in place by default_rng(seed).
+    Generator.shuffle draws the same Fisher-Yates sequence for a 1-D array as
+    for a list (tests/test_host.py checks the two agree), ~4x faster."""
+    order = np.arange(n, dtype=np.int64)
     np.random.default_rng(seed).shuffle(order)
-    return np.asarray(order, dtype=np.int32)
+    return order.astype(np.int32)
 
 
 def prepare(plc: PLC, seed: int = 0, check: bool = True) -> Prepared:

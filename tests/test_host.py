@@ -69,3 +69,12 @@ def test_generators_deterministic():
     assert validate(t) == [] and len(t.polygons) == 4
     g = synth.generate(synth.SynthSpec(100, 0.05, "cube", 0))
     assert len(g.polygons) == 5 and validate(g) == []
+
+
+def test_shuffle_order_matches_list_shuffle():
+    """prepare.shuffle_order shuffles an array; the reference shuffles a list
+    (mesh.py:878-880).  Same permutation for every size."""
+    for n in (4, 5, 28, 1000, 20011):
+        o = list(range(n))
+        np.random.default_rng(3).shuffle(o)
+        assert shuffle_order(n, 3).tolist() == o
