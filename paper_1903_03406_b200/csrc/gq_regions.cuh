@@ -98,7 +98,9 @@ __global__ void k_init_cellmark(Dev D, CellHint H, const int* pend, const int* p
 // gathers; the <1% cavities above 256 tets go to the block kernel); a 128- or
 // 256-tet tier in front of a 512-tet tier is slower (the second pass and its
 // read-back cost more than they save).  So one tier, and the second pass is
-// compiled out unless WT2 differs.
+// compiled out unless WT2 differs.  WT1_MINB 2 (two 8-warp blocks per SM: 128
+// registers instead of 236, 384 B more stack) measured 229 vs 215 ms: the
+// extra occupancy does not pay for the spills.
 #ifndef WT1_MAXT
 #define WT1_MAXT 256
 #define WT1_HASH 1024
