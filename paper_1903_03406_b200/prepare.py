@@ -54,9 +54,12 @@ def prepare(plc: PLC, seed: int = 0, check: bool = True) -> Prepared:
                                                    np.asarray(aug.points[len(plc.points):], dtype=np.float64).reshape(-1, 3)]))
     if len(pts) < 4:
         raise AllCoplanar("need at least 4 points")
-    q = pts[np.lexsort((pts[:, 2], pts[:, 1], pts[:, 0]))]
-    if len(q) > 1 and np.any(np.all(q[1:] == q[:-1], axis=1)):
-        raise DuplicatePoint("duplicate input points")
+    # validate() already rejects duplicate input points, and box corners lie
+    # 0.25*diag outside the input bbox, so the sort is only needed unchecked
+    if not check:
+        q = pts[np.lexsort((pts[:, 2], pts[:, 1], pts[:, 0]))]
+        if len(q) > 1 and np.any(np.all(q[1:] == q[:-1], axis=1)):
+            raise DuplicatePoint("duplicate input points")
     segs = np.ascontiguousarray(np.asarray(aug.segments, dtype=np.int32).reshape(-1, 2))
     off = [0]
     idx = []
