@@ -268,6 +268,9 @@ __device__ inline int region_block(const Dev& D, const double* p, const int* see
     }
   }
   __syncthreads();
+  if (__syncthreads_or(bf_has_ghost_part(D, O.bf, nbf, tid, BR_THREADS)) &&
+      __syncthreads_or(bf_open_part(D, O.bf, nbf, tid, BR_THREADS)))
+    return RS_BADSTAR;
   // swallow check + min distance over boundary vertices: reuse the hash as a
   // vertex set (cavity membership is no longer needed)
   for (int i = tid; i < BR_HASH; i += BR_THREADS) B.hkey[i] = INT_MIN;

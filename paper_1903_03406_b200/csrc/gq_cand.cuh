@@ -72,8 +72,6 @@ __device__ __forceinline__ SlabView slab(const Cand& C, int c) {
   return v;
 }
 
-__device__ unsigned long long g_region_calls;
-__device__ unsigned long long g_tested;       // tets tested for membership (algorithmic bytes)
 
 // ---------------------------------------------------------------------------
 // priorities (refine.py:35-52)
@@ -190,7 +188,7 @@ __device__ __noinline__ int cand_seeds(const Dev& D, const Cand& C, int c, int* 
         else { int mx = 0; for (int k = 1; k < 32; ++k) if (out[k] > out[mx]) mx = k; if (t < out[mx]) out[mx] = t; }
       }
       return false;
-    });
+    }, [&] { n = 0; });
     for (int a = 1; a < n; ++a) { int x = out[a], b = a - 1; while (b >= 0 && out[b] > x) { out[b + 1] = out[b]; --b; } out[b + 1] = x; }
     return n;
   }

@@ -7,10 +7,27 @@
 // a subsegment is tested against the vertices of the tets around it, a
 // subface against the apexes of its two tets (identical to the
 // reference's global KD-tree scans).
+// distance of p from the line (u,v) / plane (a,b,c), relative to the element
+// size: diagnostics only (which verification outcome fired)
+__device__ inline bool near_line(const double* u, const double* v, const double* p) {
+  double d[3] = {v[0] - u[0], v[1] - u[1], v[2] - u[2]}, w[3] = {p[0] - u[0], p[1] - u[1], p[2] - u[2]};
+  double cx = d[1] * w[2] - d[2] * w[1], cy = d[2] * w[0] - d[0] * w[2], cz = d[0] * w[1] - d[1] * w[0];
+  double l2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+  return (cx * cx + cy * cy + cz * cz) < 1e-16 * l2 * l2;
+}
+__device__ inline bool near_plane(const double* a, const double* b, const double* c, const double* p) {
+  double u[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]}, v[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+  double n[3] = {u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2], u[0] * v[1] - u[1] * v[0]};
+  double h = n[0] * (p[0] - a[0]) + n[1] * (p[1] - a[1]) + n[2] * (p[2] - a[2]);
+  double n2 = n[0] * n[0] + n[1] * n[1] + n[2] * n[2];
+  double s2 = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+  return h * h < 1e-16 * n2 * s2;
+}
 __device__ __noinline__ bool seg_check(const Dev& D, int r, Scratch& S) {   // true -> encroached or missing
   int2 e = D.sg_uv[r];
   const double *pu = PT(D, e.x), *pv = PT(D, e.y);
   bool present = false, enc = false;
+  int ew = -1;
   around_vertex(D, e.x, S.tset, S.stack, 2 * S.cap, [&](int t) {
     int4 q = D.tv[t];
     if (!has_v(q, e.y)) return false;
@@ -18,24 +35,32 @@ __device__ __noinline__ bool seg_check(const Dev& D, int r, Scratch& S) {   // t
     for (int k = 0; k < 4; ++k) {
       int w = tvk(q, k);
       if (w == GHOST || w == e.x || w == e.y) continue;
-      if (encroaches_segment(pu, pv, PT(D, w))) { enc = true; return true; }
+      if (encroaches_segment(pu, pv, PT(D, w))) { enc = true; ew = w; return true; }
     }
     return false;
   });
+  if (!present) atomicAdd(&D.ctr->chk[0], 1u);
+  else if (enc) atomicAdd(&D.ctr->chk[near_line(pu, pv, PT(D, ew)) ? 2 : 1], 1u);
   return !present || enc;
 }
 __device__ __noinline__ bool face_check(const Dev& D, int r, Scratch& S) {
   int4 f = D.sf_v[r];
   int slot = find_face(D, f.x, f.y, f.z, S.tset, S.stack, 2 * S.cap);
-  if (slot < 0) return true;
+  if (slot < 0) { atomicAdd(&D.ctr->chk[3], 1u); return true; }
   const double *a = PT(D, f.x), *b = PT(D, f.y), *c = PT(D, f.z);
   int t = slot >> 2, i = slot & 3;
   int w = tvk(D.tv[t], i);
-  if (w != GHOST && encroaches_face(a, b, c, PT(D, w))) return true;
+  if (w != GHOST && encroaches_face(a, b, c, PT(D, w))) {
+    atomicAdd(&D.ctr->chk[near_plane(a, b, c, PT(D, w)) ? 5 : 4], 1u);
+    return true;
+  }
   int nb = tnk(D, t, i);
   int u = nb >> 2, j = nb & 3;
   int w2 = tvk(D.tv[u], j);
-  if (w2 != GHOST && encroaches_face(a, b, c, PT(D, w2))) return true;
+  if (w2 != GHOST && encroaches_face(a, b, c, PT(D, w2))) {
+    atomicAdd(&D.ctr->chk[near_plane(a, b, c, PT(D, w2)) ? 5 : 4], 1u);
+    return true;
+  }
   return false;
 }
 // mode 0: records flagged CHECK; mode 1: every live record (full_verify)

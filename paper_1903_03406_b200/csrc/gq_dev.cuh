@@ -36,6 +36,14 @@ struct Counters {
   int nskip;
   int ncand;
   int pad;
+  // instrumentation (SURVEY 8(d) algorithmic bytes), per context
+  unsigned long long region_calls;   // region computations
+  unsigned long long tested;         // tets tested for membership (cavity + boundary neighbours)
+  // verification outcomes of the last check pass (diagnostics, verbose rounds):
+  // [0] subsegments missing, [1] encroached by a vertex off the segment line,
+  // [2] encroached by a (near-)collinear vertex, [3] subfaces missing,
+  // [4] encroached by an off-plane apex, [5] encroached by a (near-)coplanar apex
+  unsigned int chk[8];
 };
 
 // A tet is one 32-byte record {tv, tn} (vertices, then packed neighbour
@@ -96,6 +104,9 @@ struct Dev {
   int nsid, npoly;
   double too_close_sq, lmin2;
   Counters* ctr;
+  // large arenas for vertex-star queries (around_vertex overflow path)
+  int* vp_key; int* vp_val; unsigned int* vp_ep; unsigned int* vp_epoch; int* vp_stack; int* vp_lock;
+  int vp_cap, vp_n;
 };
 
 __device__ __forceinline__ const double* PT(const Dev& D, int v) { return D.P + 3 * (size_t)v; }
@@ -254,19 +265,20 @@ __device__ __noinline__ int first_alive_with(const Dev& D, int v) {
   return -1;
 }
 
-// visit tets around vertex v; f(t) returns true to stop early.  Returns
-// false when v has no alive tet.
+// One DFS over the tets around v with the given visited set / stack.
+// Returns 1 done (or stopped by f), 0 no alive tet, -1 the set or the stack
+// overflowed (nothing is lost: the caller reruns with a larger arena).
 template <class F>
-__device__ inline bool around_vertex(const Dev& D, int v, ISet& seen, int* stack, int cap, F f) {
+__device__ inline int around_vertex_try(const Dev& D, int v, ISet& seen, int* stack, int cap, F& f) {
   int start = D.vert_tet[v];
   if (start < 0 || start >= D.ctr->nt || !D.alive[start] || !has_v(D.tv[start], v)) {
     start = first_alive_with(D, v);
-    if (start < 0) return false;
+    if (start < 0) return 0;
     D.vert_tet[v] = start;   // same side effect as the reference
   }
   seen.clear();
   seen.put(start, 0);
-  if (f(start)) return true;
+  if (f(start)) return 1;
   int sp = 0;
   stack[sp++] = start;
   while (sp > 0) {
@@ -276,12 +288,50 @@ __device__ inline bool around_vertex(const Dev& D, int v, ISet& seen, int* stack
       if (tvk(q, i) == v) continue;
       int u = tnk(D, t, i) >> 2;
       if (u < 0 || !D.alive[u] || seen.find(u) >= 0) continue;
-      seen.put(u, 0);
-      if (f(u)) return true;
-      if (sp < cap) stack[sp++] = u; else raise_err(GQ_ERR_CAP);
+      if (!seen.put(u, 0) || sp >= cap) return -1;
+      if (f(u)) return 1;
+      stack[sp++] = u;
     }
   }
-  return true;
+  return 1;
+}
+
+// Large vertex stars (a box corner joined to thousands of hull vertices, a
+// vertex of a finely split small input angle): a DFS that outgrows the
+// per-thread arena reruns on one of a few large arenas, taken with a lock.
+// Holders never wait for anything else, so the spin always ends.
+__device__ inline int vpool_acquire(const Dev& D) {
+  unsigned int s0 = (unsigned int)(blockIdx.x * blockDim.x + threadIdx.x) % (unsigned int)D.vp_n;
+  while (true) {
+    for (int k = 0; k < D.vp_n; ++k) {
+      int s = (int)((s0 + k) % (unsigned int)D.vp_n);
+      if (atomicCAS(D.vp_lock + s, 0, 1) == 0) { __threadfence(); return s; }
+    }
+    __nanosleep(256);
+  }
+}
+__device__ inline void vpool_release(const Dev& D, int s) { __threadfence(); atomicExch(D.vp_lock + s, 0); }
+
+// visit tets around vertex v; f(t) returns true to stop early.  Returns
+// false when v has no alive tet.  When the per-thread arena overflows, the
+// walk restarts on a large arena after reset() (f may see a tet twice).
+template <class F, class R>
+__device__ inline bool around_vertex(const Dev& D, int v, ISet& seen, int* stack, int cap, F f, R reset) {
+  int r = around_vertex_try(D, v, seen, stack, cap, f);
+  if (r >= 0) return r > 0;
+  reset();
+  int s = vpool_acquire(D);
+  ISet big;
+  size_t o = (size_t)s * D.vp_cap;
+  big.key = D.vp_key + o; big.val = D.vp_val + o; big.ep = D.vp_ep + o; big.cur = D.vp_epoch + s; big.cap = D.vp_cap;
+  r = around_vertex_try(D, v, big, D.vp_stack + o, D.vp_cap, f);
+  vpool_release(D, s);
+  if (r < 0) raise_err(GQ_ERR_CAP);
+  return r > 0;
+}
+template <class F>
+__device__ inline bool around_vertex(const Dev& D, int v, ISet& seen, int* stack, int cap, F f) {
+  return around_vertex(D, v, seen, stack, cap, f, [] {});
 }
 __device__ inline bool edge_exists(const Dev& D, int u, int v, ISet& seen, int* stack, int cap) {
   bool found = false;
@@ -394,7 +444,41 @@ __device__ __noinline__ bool in_region(const Dev& D, int t, const double* p, con
 
 // ---------------------------------------------------------------------------
 // Delaunay region (mesh.py:450-521, decisions of _kernels.py:392-635)
-enum RegionStatus { RS_OK = 0, RS_CNSS = 1, RS_MEMBRANE = 2, RS_OVERFLOW = 3, RS_TOOCLOSE = 4 };
+enum RegionStatus { RS_OK = 0, RS_CNSS = 1, RS_MEMBRANE = 2, RS_OVERFLOW = 3, RS_TOOCLOSE = 4, RS_BADSTAR = 5 };
+
+// Star validation before anything is written.  The peel makes every real
+// boundary face strictly visible from p, so a cavity of real tets always
+// stars; faces through the ghost vertex are not tested by the peel, and a
+// point that rounds to just outside a curved hull can leave a pinched
+// boundary.  The reference notices only while starring (star_kernel's
+// unmatched-face status, _kernels.py:696,720 -> CavityNotStarShaped,
+// mesh.py:769-770).  Here the cavity is rejected up front (RS_BADSTAR -> a
+// failed candidate, and the sequential fallback skips it with reason
+// cavity_not_star_shaped, refine.py:785-799) when some boundary-face edge
+// (ghost vertex included) lies on other than exactly two boundary faces.
+// Faces [r, r+stride, ...) are checked by the caller's lane r.
+__device__ inline bool bf_has_ghost_part(const Dev& D, const int* bf, int nbf, int r, int stride) {
+  for (int k = r; k < nbf; k += stride) {
+    int f[3]; face_verts(D.tv[bf[k] >> 2], bf[k] & 3, f);
+    if (f[0] == GHOST || f[1] == GHOST || f[2] == GHOST) return true;
+  }
+  return false;
+}
+__device__ inline bool bf_open_part(const Dev& D, const int* bf, int nbf, int r, int stride) {
+  for (int k = r; k < nbf; k += stride) {
+    int f[3]; face_verts(D.tv[bf[k] >> 2], bf[k] & 3, f);
+    for (int e = 0; e < 3; ++e) {
+      int x = f[e], y = f[(e + 1) % 3];
+      int cnt = 0;
+      for (int j = 0; j < nbf && cnt <= 2; ++j) {
+        int g[3]; face_verts(D.tv[bf[j] >> 2], bf[j] & 3, g);
+        cnt += (g[0] == x || g[1] == x || g[2] == x) && (g[0] == y || g[1] == y || g[2] == y);
+      }
+      if (cnt != 2) return true;
+    }
+  }
+  return false;
+}
 
 struct Scratch {     // per-thread scratch views
   ISet tset;         // tet -> list index
@@ -651,6 +735,7 @@ __device__ __noinline__ int region_compute(const Dev& D, const double* p, const 
       }
     }
   }
+  if (bf_has_ghost_part(D, O.bf, O.nbf, 0, 1) && bf_open_part(D, O.bf, O.nbf, 0, 1)) return RS_BADSTAR;
   double mind = __longlong_as_double(0x7ff0000000000000ll);
   for (int a = 0; a < O.nbf; ++a) {
     int t = O.bf[a] >> 2, i = O.bf[a] & 3;

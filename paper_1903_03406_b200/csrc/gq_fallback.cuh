@@ -170,7 +170,7 @@ __global__ void k_fallback(Dev D, Cand C, Scr SCB, FallbackIO F, T2Items T, Skip
     RegionOut O = region_view(C, c, sv, 0);
     int seeds[32];
     int ns = cand_seeds(D, C, c, seeds, S);
-    atomicAdd(&g_region_calls, 1ull);
+    atomicAdd(&D.ctr->region_calls, 1ull);
     int st = ns == 0 ? RS_CNSS : region_compute(D, p, seeds, ns, allow_of(C, c), S, O);
     store_region(C, c, O);
     if (st == RS_OK) {

@@ -16,7 +16,13 @@ struct DevCache {
   std::unordered_multimap<size_t, void*> free_blocks;
   std::unordered_map<void*, size_t> live;
 };
+// A context's calls use the context's own cache (set by CtxScope for the
+// duration of each C-ABI call), so blocks freed by one context's stream are
+// never handed to another context's concurrently running stream.  Calls
+// without a context (gq_batch) use a per-device cache.
+static thread_local DevCache* tl_cache = nullptr;
 static DevCache& dev_cache() {
+  if (tl_cache) return *tl_cache;
   static DevCache caches[64];
   int d = 0;
   cudaGetDevice(&d);
@@ -65,6 +71,7 @@ template <class T> static T* dmalloc(size_t n) {
 }
 
 struct gq_ctx {
+  DevCache cache;
   int device = 0;
   cudaStream_t st = nullptr;
   std::string err;
@@ -107,18 +114,24 @@ struct gq_ctx {
   bool allocated = false;
 };
 
+struct CtxScope {   // binds the calling thread's allocations to a context's cache
+  DevCache* prev;
+  explicit CtxScope(gq_ctx* c) : prev(tl_cache) { tl_cache = &c->cache; }
+  ~CtxScope() { tl_cache = prev; }
+};
+
 static double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
-static double g_prof[8];
+static thread_local double g_prof[8];
 // fine stage timers (GQ_PROFILE=2): synchronise and charge the elapsed time
-static bool g_trace = false;
-static bool g_fine = false;      // GQ_PROFILE=2: host clock after a sync per stage
-static bool g_fine_ev = false;   // GQ_PROFILE=3: events per stage (device timeline, no syncs)
-static double g_fine_t[32];
+static thread_local bool g_trace = false;
+static thread_local bool g_fine = false;      // GQ_PROFILE=2: host clock after a sync per stage
+static thread_local bool g_fine_ev = false;   // GQ_PROFILE=3: events per stage (device timeline, no syncs)
+static thread_local double g_fine_t[32];
 static const char* g_fine_names[32] = {"i.region", "i.big", "i.filter", "i.scan", "i.kill", "i.stars", "i.compact",
   "p.gridsync", "p.newverts", "p.check", "p.compact", "r.sorted", "r.make", "r.redirect", "r.append", "f.states",
   "f.rank", "f.lfmis", "x.acc", "x.ids", "x.star", "x.postins", "i.misc", "r.misc", "g.warp", "g.ovfscan", "g.block",
   "r.setup", "r.gridc", "r.kept", "x.fallback", "r.misc2"};
-static double g_fine_last = 0;
+static thread_local double g_fine_last = 0;
 static void fine(gq_ctx* c, int k);
 static void sync(gq_ctx* c) {
   CK(cudaStreamSynchronize(c->st));
@@ -131,7 +144,8 @@ static void sync(gq_ctx* c) {
   }
 }
 static void pull(gq_ctx* c) { CK(cudaMemcpyAsync(&c->hc, c->dctr, sizeof(Counters), cudaMemcpyDeviceToHost, c->st)); sync(c); }
-static void push(gq_ctx* c) { CK(cudaMemcpyAsync(c->dctr, &c->hc, sizeof(Counters), cudaMemcpyHostToDevice, c->st)); }
+// the mesh / record counts only: the instrumentation counters are device-owned
+static void push(gq_ctx* c) { CK(cudaMemcpyAsync(c->dctr, &c->hc, offsetof(Counters, region_calls), cudaMemcpyHostToDevice, c->st)); }
 static int grid_for(long long n, int bs = 128, int cap = 148 * 16) {
   long long g = (n + bs - 1) / bs;
   if (g < 1) g = 1;
@@ -188,16 +202,21 @@ static void exclusive_scan(gq_ctx* c, const int* in, int* out, int n) {
   ensure_cub(c, need);
   cub::DeviceScan::ExclusiveSum(c->cub_tmp, need, in, out, n, c->st);
 }
+// device -> host copy ordered on the context's stream, complete on return
+static void d2h(gq_ctx* c, void* dst, const void* src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+}
 static int read_int(gq_ctx* c, const int* d) { int v; CK(cudaMemcpyAsync(&v, d, sizeof v, cudaMemcpyDeviceToHost, c->st)); sync(c); return v; }
 
-static void alloc_scratch(Scr& s, int nthreads, int cap, int tcap, int fcap) {
+static void alloc_scratch(Scr& s, int nthreads, int cap, int tcap, int fcap, cudaStream_t st) {
   s.nthreads = nthreads; s.cap = cap; s.tcap = tcap; s.fcap = fcap;
   s.tkey = dmalloc<int>((size_t)nthreads * tcap); s.tval = dmalloc<int>((size_t)nthreads * tcap);
   s.tep = dmalloc<unsigned int>((size_t)nthreads * tcap);
   s.fkey = dmalloc<unsigned long long>((size_t)nthreads * fcap); s.fep = dmalloc<unsigned int>((size_t)nthreads * fcap);
   s.epoch = dmalloc<unsigned int>((size_t)nthreads * 2);
-  CK(cudaMemset(s.tep, 0, (size_t)nthreads * tcap * 4)); CK(cudaMemset(s.fep, 0, (size_t)nthreads * fcap * 4));
-  CK(cudaMemset(s.epoch, 0, (size_t)nthreads * 2 * 4));
+  CK(cudaMemsetAsync(s.tep, 0, (size_t)nthreads * tcap * 4, st)); CK(cudaMemsetAsync(s.fep, 0, (size_t)nthreads * fcap * 4, st));
+  CK(cudaMemsetAsync(s.epoch, 0, (size_t)nthreads * 2 * 4, st));
   s.list = dmalloc<int>((size_t)nthreads * cap); s.stack = dmalloc<int>((size_t)nthreads * cap * 2);
   s.in = dmalloc<uint8_t>((size_t)nthreads * cap); s.comp = dmalloc<uint8_t>((size_t)nthreads * cap);
 }
@@ -246,7 +265,7 @@ static void grow_cands_keep(gq_ctx* c, int need, int n_keep) {
   alloc_cands(c, std::max(need, 2 * old.cap), old.nbigcap);
   Cand& C = c->C;
   size_t k = (size_t)n_keep;
-#define CPY(f, w) CK(cudaMemcpy(C.f, old.f, sizeof(*old.f) * (w) * k, cudaMemcpyDeviceToDevice))
+#define CPY(f, w) CK(cudaMemcpyAsync(C.f, old.f, sizeof(*old.f) * (w) * k, cudaMemcpyDeviceToDevice, c->st))
   CPY(kind, 1); CPY(tgt, 1); CPY(seed, 1); CPY(status, 1); CPY(memb, 1); CPY(pool, 1); CPY(rank, 1);
   CPY(allow, 1); CPY(nallow, 1); CPY(extra, 1); CPY(p, 3); CPY(h, 1); CPY(canon, 1); CPY(state, 1);
   CPY(vid, 1); CPY(nt0, 1); CPY(ntet, 1); CPY(nbf, 1); CPY(ncr, 1); CPY(nbsub, 1); CPY(nbseg, 1);
@@ -254,13 +273,13 @@ static void grow_cands_keep(gq_ctx* c, int need, int n_keep) {
   CPY(bseg, CC); CPY(eseg, CC); CPY(rseg, CRD); CPY(rface, CRD); CPY(nrseg, 1); CPY(nrface, 1); CPY(bigi, 1);
 #undef CPY
   size_t kb = (size_t)old.nbigcap;
-  CK(cudaMemcpy(C.btets, old.btets, 4 * kb * CTB, cudaMemcpyDeviceToDevice));
-  CK(cudaMemcpy(C.bbf, old.bbf, 4 * kb * CFB, cudaMemcpyDeviceToDevice));
-  CK(cudaMemcpy(C.bcr, old.bcr, 4 * kb * CCB, cudaMemcpyDeviceToDevice));
-  CK(cudaMemcpy(C.bcrf, old.bcrf, 4 * kb * CCB, cudaMemcpyDeviceToDevice));
-  CK(cudaMemcpy(C.bbsub, old.bbsub, 4 * kb * CCB, cudaMemcpyDeviceToDevice));
-  CK(cudaMemcpy(C.bbseg, old.bbseg, 4 * kb * CCB, cudaMemcpyDeviceToDevice));
-  CK(cudaMemcpy(C.beseg, old.beseg, 4 * kb * CCB, cudaMemcpyDeviceToDevice));
+  CK(cudaMemcpyAsync(C.btets, old.btets, 4 * kb * CTB, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(C.bbf, old.bbf, 4 * kb * CFB, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(C.bcr, old.bcr, 4 * kb * CCB, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(C.bcrf, old.bcrf, 4 * kb * CCB, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(C.bbsub, old.bbsub, 4 * kb * CCB, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(C.bbseg, old.bbseg, 4 * kb * CCB, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(C.beseg, old.beseg, 4 * kb * CCB, cudaMemcpyDeviceToDevice, c->st));
   free_cands(old);
 }
 // big-region slabs: grow keeping the first c->big_used ones
@@ -271,7 +290,7 @@ static void ensure_big(gq_ctx* c, int need) {
   size_t keep = (size_t)c->big_used;
   auto grow = [&](int*& ptr, size_t w) {
     int* q = dmalloc<int>((size_t)cap * w);
-    if (keep) CK(cudaMemcpy(q, ptr, 4 * keep * w, cudaMemcpyDeviceToDevice));
+    if (keep) CK(cudaMemcpyAsync(q, ptr, 4 * keep * w, cudaMemcpyDeviceToDevice, c->st));
     dfree(ptr);
     ptr = q;
   };
@@ -300,54 +319,64 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   D.tv.p = dmalloc<int4>(2 * tcap); D.tn.p = D.tv.p + 1; D.alive = dmalloc<uint8_t>(tcap);
   D.sub = dmalloc<uint8_t>(tcap); D.seg = dmalloc<uint8_t>(tcap); D.skip = dmalloc<uint8_t>(tcap);
   D.ratio = dmalloc<double>(tcap);
-  CK(cudaMemset(D.alive, 0, tcap));
+  CK(cudaMemsetAsync(D.alive, 0, tcap, c->st));
   if (getenv("GQ_PROFILE")) std::fprintf(stderr, "[gq] capacities: verts %zu tets %zu\n", vcap, tcap);
   size_t sgcap = 65536 + (size_t)m * 32 + vcap / 8;
   D.sgcap = (int)sgcap;
   D.sg_uv = dmalloc<int2>(sgcap); D.sg_sid = dmalloc<int>(sgcap); D.sg_fl = dmalloc<unsigned int>(sgcap);
   unsigned int sgh = pow2_at_least(2 * sgcap);
   D.sg_hk = dmalloc<unsigned long long>(sgh); D.sg_hv = dmalloc<int>(sgh); D.sg_hmask = sgh - 1;
-  CK(cudaMemset(D.sg_hk, 0xff, (size_t)sgh * 8));
+  CK(cudaMemsetAsync(D.sg_hk, 0xff, (size_t)sgh * 8, c->st));
   size_t sfcap = 65536 + (size_t)npidx * 32 + vcap;
   D.sfcap = (int)sfcap;
   D.sf_v = dmalloc<int4>(sfcap); D.sf_fl = dmalloc<unsigned int>(sfcap);
   unsigned int sfh = pow2_at_least(2 * sfcap);
   D.sf_hk = dmalloc<unsigned long long>(sfh); D.sf_hv = dmalloc<int>(sfh); D.sf_hmask = sfh - 1;
-  CK(cudaMemset(D.sf_hk, 0xff, (size_t)sfh * 8));
+  CK(cudaMemsetAsync(D.sf_hk, 0xff, (size_t)sfh * 8, c->st));
   size_t t2cap = 65536 + (size_t)npidx * 8 + 2 * vcap;
   D.t2cap = (int)t2cap;
   D.t2v = dmalloc<int4>(t2cap); D.t2alive = dmalloc<uint8_t>(t2cap);
-  CK(cudaMemset(D.t2alive, 0, t2cap));
+  CK(cudaMemsetAsync(D.t2alive, 0, t2cap, c->st));
   unsigned int heh = pow2_at_least(4 * t2cap);
   D.he_hk = dmalloc<unsigned long long>(heh); D.he_hv = dmalloc<int>(heh); D.he_hmask = heh - 1;
-  CK(cudaMemset(D.he_hk, 0xff, (size_t)heh * 8));
+  CK(cudaMemsetAsync(D.he_hk, 0xff, (size_t)heh * 8, c->st));
   D.t2count = dmalloc<int>(std::max(f, 1));
-  CK(cudaMemset(D.t2count, 0, std::max(f, 1) * 4));
+  CK(cudaMemsetAsync(D.t2count, 0, std::max(f, 1) * 4, c->st));
   D.poly_keep = dmalloc<int2>(std::max(f, 1));
   D.poly_obl = dmalloc<uint8_t>(std::max(f, 1));
   D.t2last = dmalloc<int>(std::max(f, 1));
-  CK(cudaMemset(D.t2last, 0xff, 4 * (size_t)std::max(f, 1)));
+  CK(cudaMemsetAsync(D.t2last, 0xff, 4 * (size_t)std::max(f, 1), c->st));
   D.segpoly_off = dmalloc<int>(m + 1);
   D.segpoly = dmalloc<int>(std::max(npidx, 1));
   D.sid_uv = dmalloc<int2>(std::max(m, 1));
   D.nsid = m; D.npoly = f;
   c->dctr = dmalloc<Counters>(1);
   D.ctr = c->dctr;
+  // large vertex-star arenas (around_vertex overflow path)
+  D.vp_n = 64; D.vp_cap = 1 << 17;
+  {
+    size_t nb = (size_t)D.vp_n * D.vp_cap;
+    D.vp_key = dmalloc<int>(nb); D.vp_val = dmalloc<int>(nb); D.vp_ep = dmalloc<unsigned int>(nb);
+    D.vp_stack = dmalloc<int>(nb); D.vp_epoch = dmalloc<unsigned int>(D.vp_n); D.vp_lock = dmalloc<int>(D.vp_n);
+    CK(cudaMemsetAsync(D.vp_ep, 0, 4 * nb, c->st));
+    CK(cudaMemsetAsync(D.vp_epoch, 0, 4 * (size_t)D.vp_n, c->st));
+    CK(cudaMemsetAsync(D.vp_lock, 0, 4 * (size_t)D.vp_n, c->st));
+  }
   // filter owners: [tets | faces | seg records]
   c->W.toff = 0; c->W.foff = (int)tcap; c->W.soff = (int)(5 * tcap);
   c->W.own = dmalloc<int>(5 * tcap + sgcap);
-  CK(cudaMemset(c->W.own, 0x7f, (5 * tcap + sgcap) * 4));
+  CK(cudaMemsetAsync(c->W.own, 0x7f, (5 * tcap + sgcap) * 4, c->st));
   // 2D items
   c->T.cap = 256; c->T.rcap = 128;
   c->T.icap = 0;
   c->T.cand = c->T.pid = c->T.state = c->T.ncav = c->T.nrem = c->T.cav = c->T.rem = nullptr;   // freed by free_all
   ensure_items(c, 1 << 16);
   c->T.own = dmalloc<int>(t2cap);
-  CK(cudaMemset(c->T.own, 0x7f, t2cap * 4));
+  CK(cudaMemsetAsync(c->T.own, 0x7f, t2cap * 4, c->st));
   c->L.cap = 1 << 20; c->L.rows = dmalloc<int>((size_t)8 * c->L.cap);
   c->d_int = dmalloc<int>(64);
-  alloc_scratch(c->S, 16384, CT * 2, 1024, 2048);
-  alloc_scratch(c->SB, 512, CTB * 2, 32768, 32768);
+  alloc_scratch(c->S, 16384, CT * 2, 1024, 2048, c->st);
+  alloc_scratch(c->SB, 512, CTB * 2, 32768, 32768, c->st);
   alloc_cands(c, 1 << 16, 256);
   {
     int g = (int)std::cbrt(std::max(1.0, n / 2.0));
@@ -378,7 +407,7 @@ static void free_all(gq_ctx* c) {
   Dev& D = c->D;
   void* ps[] = {D.P, D.vorigin, D.vert_tet, D.vsid, D.tv.p, D.alive, D.sub, D.seg, D.skip, D.ratio, D.sg_uv,
                 D.sg_sid, D.sg_fl, D.sg_hk, D.sg_hv, D.sf_v, D.sf_fl, D.sf_hk, D.sf_hv, D.t2v, D.t2alive, D.he_hk,
-                D.he_hv, D.t2count, D.poly_keep, D.poly_obl, D.t2last, D.segpoly_off, D.segpoly, D.sid_uv, c->dctr, c->W.own, c->T.cand,
+                D.he_hv, D.t2count, D.poly_keep, D.poly_obl, D.t2last, D.segpoly_off, D.segpoly, D.sid_uv, D.vp_key, D.vp_val, D.vp_ep, D.vp_stack, D.vp_epoch, D.vp_lock, c->dctr, c->W.own, c->T.cand,
                 c->T.pid, c->T.state, c->T.cav, c->T.ncav, c->T.rem, c->T.nrem, c->T.own, c->L.rows, c->d_int,
                 c->S.tkey, c->S.tval, c->S.tep, c->S.fkey, c->S.fep, c->S.epoch, c->S.list, c->S.stack, c->S.in,
                 c->S.comp, c->SB.tkey, c->SB.tval, c->SB.tep, c->SB.fkey, c->SB.fep, c->SB.epoch, c->SB.list,
@@ -442,9 +471,8 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
     static long long launch_no = 0;
     static unsigned long long t_last = 0, r_last = 0;
     sync(c);
-    unsigned long long rc = 0, tested = 0;
-    CK(cudaMemcpyFromSymbol(&rc, g_region_calls, 8));
-    CK(cudaMemcpyFromSymbol(&tested, g_tested, 8));
+    pull(c);
+    unsigned long long rc = c->hc.region_calls, tested = c->hc.tested;
     float ms = 0; cudaEventElapsedTime(&ms, c->er0, c->er1);
     std::fprintf(stderr, "[region] launch %lld cands %d bytes_alg %llu ms %.3f\n", launch_no++, n1 - n0,
                  58ull * (tested - t_last) + 24ull * (rc - r_last), ms);
@@ -487,7 +515,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
       std::vector<int> nts(nb);
       int mx = 0; long long sm = 0;
       for (int k = 0; k < nb; ++k) {
-        CK(cudaMemcpy(&nts[k], c->C.ntet + big[k], 4, cudaMemcpyDeviceToHost));
+        d2h(c, &nts[k], c->C.ntet + big[k], 4);
         mx = std::max(mx, nts[k]); sm += nts[k];
       }
       std::fprintf(stderr, "[big] n %d of %d tets max %d mean %.0f block %.3f ms\n", nb, n1 - n0, mx, (double)sm / nb, 1e3 * (now_s() - tb));
@@ -496,15 +524,39 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   fine(c, 26);
 }
 
-// candidates sorted by priority (class rank, hash); smaller first
-// (refine.py:45-52).  Equal hashes would fall back to the canonical tuple in
-// the reference; a 64-bit splitmix collision inside one round is ignored.
+// candidates sorted by priority (class rank, hash, canonical tuple); smaller
+// first (refine.py:45-52).  Two radix passes order by (class, hash); a run of
+// equal (class, hash) -- a 64-bit splitmix collision -- is then put in
+// canonical-tuple order by the thread at its head (growblast.py:49 compares
+// the whole priority tuple).
 __global__ void k_rank_keys(Cand C, int n, unsigned long long* kh, unsigned int* kk, int* idx) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     bool ok = C.status[c] == CS_OK;
     kh[c] = ok ? C.h[c] : ~0ull;
     kk[c] = ok ? (unsigned int)C.kind[c] : 7u;
     idx[c] = c;
+  }
+}
+__device__ __forceinline__ bool canon_less(int4 a, int4 b) {
+  if (a.x != b.x) return a.x < b.x;
+  if (a.y != b.y) return a.y < b.y;
+  if (a.z != b.z) return a.z < b.z;
+  return a.w < b.w;
+}
+__global__ void k_rank_ties(Cand C, int* order, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += gridDim.x * blockDim.x) {
+    int a = order[i];
+    if (C.status[a] != CS_OK) continue;
+    auto same = [&](int x, int y) { return C.status[y] == CS_OK && C.kind[x] == C.kind[y] && C.h[x] == C.h[y]; };
+    if (i > 0 && same(order[i - 1], a)) continue;      // not the head of a run
+    int j = i + 1;
+    while (j < n && same(a, order[j])) ++j;
+    for (int x = i + 1; x < j; ++x) {                  // insertion sort of the run by canon
+      int v = order[x], y = x - 1;
+      int4 cv = C.canon[v];
+      while (y >= i && canon_less(cv, C.canon[order[y]])) { order[y + 1] = order[y]; --y; }
+      order[y + 1] = v;
+    }
   }
 }
 static void rank_candidates(gq_ctx* c, int n) {
@@ -520,6 +572,7 @@ static void rank_candidates(gq_ctx* c, int n) {
   cub::DeviceRadixSort::SortPairs(nullptr, need, c->k32b, c->k32a, c->tmpB, c->tmpA, n, 0, 3, c->st);
   ensure_cub(c, need);
   cub::DeviceRadixSort::SortPairs(c->cub_tmp, need, c->k32b, c->k32a, c->tmpB, c->tmpA, n, 0, 3, c->st);
+  LAUNCH(k_rank_ties, n, c->C, c->tmpA, n);
   LAUNCH(k_rank_scatter, n, c->C, c->tmpA, n);
 }
 
@@ -658,7 +711,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
   LAUNCH(k_init_first, 1, c->D, c->d_order, n, c->d_int + 8);
   sync(c);
   int first[4];
-  CK(cudaMemcpy(first, c->d_int + 8, 16, cudaMemcpyDeviceToHost));
+  d2h(c, first, c->d_int + 8, 16);
   std::vector<int> pend;
   pend.reserve(n);
   for (int k = 0; k < n; ++k) {
@@ -686,7 +739,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
   {
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     std::vector<double> P(3 * (size_t)n);
-    CK(cudaMemcpy(P.data(), c->D.P, 24 * (size_t)n, cudaMemcpyDeviceToHost));
+    d2h(c, P.data(), c->D.P, 24 * (size_t)n);
     for (int i = 0; i < n; ++i) for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], P[3 * i + k]); hi[k] = std::max(hi[k], P[3 * i + k]); }
     H.G = std::max(1, std::min(128, (int)std::cbrt(n / 2.0)));
     for (int k = 0; k < 3; ++k) { H.lo[k] = lo[k]; H.inv[k] = hi[k] > lo[k] ? H.G / (hi[k] - lo[k]) : 0.0; }
@@ -862,7 +915,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     if (g_trace) {
       sync(c);
       float rms = 0; cudaEventElapsedTime(&rms, c->rpairs.back().first, c->rpairs.back().second);
-      unsigned long long rc = 0; CK(cudaMemcpyFromSymbol(&rc, g_region_calls, 8));
+      pull(c); unsigned long long rc = c->hc.region_calls;
       static unsigned long long rc_last = 0;
       std::fprintf(stderr, "[init] round %d W %d big %d acc %d nt %d region_ms %.3f computed %llu maxtet %d\n", round, W,
                    (int)bl.size(), nacc, nt, rms, rc - rc_last, read_int(c, c->d_int + 41));
@@ -1173,7 +1226,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     CK(cudaMemsetAsync(c->d_int + 56, 0, 8, c->st));
     LAUNCH(k_count_seed_dead, n, c->D, c->C, n, c->d_int + 56);
     int h2[2];
-    CK(cudaMemcpy(h2, c->d_int + 56, 8, cudaMemcpyDeviceToHost));
+    d2h(c, h2, c->d_int + 56, 8);
     std::fprintf(stderr, "[seed] round %d rejected %d with dead seed tet %d\n", round_no, h2[0], h2[1]);
   }
   g_prof[5] += now_s() - t1;
@@ -1187,6 +1240,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   c->reg_nv = c->hc.nv;
   fine(c, 8);
   CK(cudaMemsetAsync(c->d_int, 0, 16, c->st));
+  CK(cudaMemsetAsync(&c->dctr->chk, 0, sizeof(c->dctr->chk), c->st));
   LAUNCH_S(k_check, c->hc.nsegrec + c->hc.nfacerec, c->D, c->S, 0, c->d_int);
   if (R.inserted > 0) LAUNCH(k_clear_flag, c->hc.nsegrec + c->hc.nfacerec, c->D, RF_BLOCK);
   fine(c, 9);
@@ -1214,21 +1268,18 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   g_fine_ev = getenv("GQ_PROFILE") && atoi(getenv("GQ_PROFILE")) == 3;
   c->rpairs.clear(); c->fev.clear(); c->evused = 0;
   g_trace = getenv("GQ_TRACE") != nullptr;
-  { int ws = getenv("GQ_WSTOP") ? atoi(getenv("GQ_WSTOP")) : 0; CK(cudaMemcpyToSymbol(g_wstop, &ws, 4)); }
+  { int ws = getenv("GQ_WSTOP") ? atoi(getenv("GQ_WSTOP")) : 0; CK(cudaMemcpyToSymbolAsync(g_wstop, &ws, 4, 0, cudaMemcpyHostToDevice, c->st)); }
   c->n_input = n_input; c->npoly = f;
   c->rounds.clear(); c->rtimes.clear(); c->launches = 0; c->region_ms = 0;
   free_all(c);
   unsigned int zero = 0;
-  CK(cudaMemcpyToSymbol(g_err, &zero, 4));
+  CK(cudaMemcpyToSymbolAsync(g_err, &zero, 4, 0, cudaMemcpyHostToDevice, c->st));
   unsigned long long z4[4] = {0, 0, 0, 0};
-  CK(cudaMemcpyToSymbol(g_exact_calls, z4, 32));
-  unsigned long long z1 = 0;
-  CK(cudaMemcpyToSymbol(g_region_calls, &z1, 8));
-  CK(cudaMemcpyToSymbol(g_tested, &z1, 8));
+  CK(cudaMemcpyToSymbolAsync(g_exact_calls, z4, 32, 0, cudaMemcpyHostToDevice, c->st));
   int npidx = f > 0 ? poff[f] : 0;
   double ta = now_s();
   alloc_mesh(c, n, m, f, npidx);
-  CK(cudaDeviceSynchronize());
+  CK(cudaStreamSynchronize(c->st));
   if (getenv("GQ_PROFILE")) std::fprintf(stderr, "[gq] alloc %.1f ms\n", 1000 * (now_s() - ta));
   c->d_order = dmalloc<int>(n);
   Dev& D = c->D;
@@ -1248,6 +1299,7 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   CK(cudaMemsetAsync(D.vsid, 0xff, 4 * (size_t)D.vcap, c->st));
   c->hc = Counters{};
   c->hc.nv = n;
+  CK(cudaMemsetAsync(c->dctr, 0, sizeof(Counters), c->st));
   push(c);
   CK(cudaEventRecord(c->ev0, c->st));
   // polygon info
@@ -1277,7 +1329,7 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
     }
     for (int s = 0; s < m; ++s) { spo[s + 1] = spo[s] + (int)c->polys[s].size(); for (int p : c->polys[s]) sp.push_back(p); }
     for (int s = 0; s < m; ++s) if (c->polys[s].size() > 4) throw std::runtime_error("segment shared by more than 4 polygons");
-    CK(cudaMemcpy(D.poly_keep, keep, 8 * (size_t)f, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(D.poly_keep, keep, 8 * (size_t)f, cudaMemcpyHostToDevice, c->st));
     std::vector<uint8_t> obl(f, 1);
     for (int pid = 0; pid < f; ++pid)
       for (int k = 0; k < 3 && obl[pid]; ++k) {
@@ -1285,10 +1337,10 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
         for (int q = poff[pid] + 1; q < poff[pid + 1] && same; ++q) same = xyz[3 * pidx[q] + k] == xyz[3 * pidx[poff[pid]] + k];
         if (same) obl[pid] = 0;
       }
-    CK(cudaMemcpy(D.poly_obl, obl.data(), f, cudaMemcpyHostToDevice));
-    if (!sp.empty()) CK(cudaMemcpy(D.segpoly, sp.data(), 4 * sp.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(D.poly_obl, obl.data(), f, cudaMemcpyHostToDevice, c->st));
+    if (!sp.empty()) CK(cudaMemcpyAsync(D.segpoly, sp.data(), 4 * sp.size(), cudaMemcpyHostToDevice, c->st));
   }
-  CK(cudaMemcpy(D.segpoly_off, spo.data(), 4 * (size_t)(m + 1), cudaMemcpyHostToDevice));
+  CK(cudaMemcpyAsync(D.segpoly_off, spo.data(), 4 * (size_t)(m + 1), cudaMemcpyHostToDevice, c->st));
   // init_delaunay
   init_delaunay(c, order, n);
   CK(cudaEventRecord(c->ev1, c->st));
@@ -1297,7 +1349,7 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   // constraints
   if (m > 0) {
     int* dseg = dmalloc<int>(2 * (size_t)m);
-    CK(cudaMemcpy(dseg, seg, 8 * (size_t)m, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(dseg, seg, 8 * (size_t)m, cudaMemcpyHostToDevice, c->st));
     LAUNCH(k_segs_init, m, D, dseg, m);
     sync(c);
     dfree(dseg);
@@ -1307,8 +1359,8 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   push(c);
   if (f > 0) {
     int* dpo = dmalloc<int>(f + 1); int* dpi = dmalloc<int>(std::max(npidx, 1));
-    CK(cudaMemcpy(dpo, poff, 4 * (size_t)(f + 1), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(dpi, pidx, 4 * (size_t)npidx, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(dpo, poff, 4 * (size_t)(f + 1), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(dpi, pidx, 4 * (size_t)npidx, cudaMemcpyHostToDevice, c->st));
     LAUNCH_S(k_facets_init, f, D, dpo, dpi, f, c->S, (int*)nullptr);
     sync(c);
     pull(c);
@@ -1340,13 +1392,18 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
     pull(c);
     LAUNCH(k_count_pending, c->hc.nsegrec + c->hc.nfacerec, c->D, c->d_int + 4);
     int h[4];
-    CK(cudaMemcpy(h, c->d_int + 4, 16, cudaMemcpyDeviceToHost));
+    d2h(c, h, c->d_int + 4, 16);
     double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     c->rounds.push_back({round_no, R.phase, R.ncand, R.acc, R.rej, R.failed, R.inserted, h[2], h[3]});
     c->rtimes.push_back(dt);
-    if (c->verbose)
-      std::fprintf(stderr, "round %d phase=%d candidates=%lld accepted=%lld blasted=%lld failed=%lld inserted=%lld time=%.4f\n",
-                   round_no, R.phase, R.ncand, R.acc, R.rej, R.failed, R.inserted, dt);
+    if (c->verbose) {
+      pull(c);
+      const unsigned int* k = c->hc.chk;
+      std::fprintf(stderr, "round %d phase=%d candidates=%lld accepted=%lld blasted=%lld failed=%lld inserted=%lld time=%.4f"
+                   " | nv %d nt %d segs %d faces %d skipped %d | check: seg miss %u enc %u (collinear %u) face miss %u enc %u (coplanar %u)\n",
+                   round_no, R.phase, R.ncand, R.acc, R.rej, R.failed, R.inserted, dt, c->hc.nv, c->hc.nt, c->hc.nsegrec,
+                   c->hc.nfacerec, c->hc.nskip, k[0], k[1], k[2], k[3], k[4], k[5]);
+    }
     round_no += 1;
   }
   CK(cudaEventRecord(c->ev1, c->st));
@@ -1369,8 +1426,8 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
     out->nv = c->hc.nv; out->nt = c->hc.nt;
     // live constraint counts
     std::vector<unsigned int> sf(c->hc.nsegrec), ff(c->hc.nfacerec);
-    CK(cudaMemcpy(sf.data(), D.sg_fl, 4 * sf.size(), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(ff.data(), D.sf_fl, 4 * ff.size(), cudaMemcpyDeviceToHost));
+    d2h(c, sf.data(), D.sg_fl, 4 * sf.size());
+    d2h(c, ff.data(), D.sf_fl, 4 * ff.size());
     for (auto x : sf) out->n_subsegments += (x & RF_LIVE) ? 1 : 0;
     for (auto x : ff) out->n_subfaces += (x & RF_LIVE) ? 1 : 0;
     out->n_rounds = (int64_t)c->rounds.size();
@@ -1380,13 +1437,11 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
     for (int k = 0; k < 4; ++k) out->exact_calls[k] = (int64_t)ex[k];
     out->device_ms = c->dev_ms; out->init_ms = c->init_ms;
     out->kernel_launches = c->launches;
-    unsigned long long rc = 0, tested = 0;
-    CK(cudaMemcpyFromSymbol(&rc, g_region_calls, 8));
-    CK(cudaMemcpyFromSymbol(&tested, g_tested, 8));
+    unsigned long long rc = c->hc.region_calls, tested = c->hc.tested;
     out->region_calls = (int64_t)rc;
     out->region_ms = c->region_ms;
     std::vector<uint8_t> org2(c->hc.nv);
-    CK(cudaMemcpy(org2.data(), D.vorigin, c->hc.nv, cudaMemcpyDeviceToHost));
+    d2h(c, org2.data(), D.vorigin, c->hc.nv);
     for (auto o : org2) { if (o) out->steiner_points++; else out->input_points++; }
     // 144 N_cand + 58 T_tested + 8 K_claims + 51 T_created + 1 T_deleted + 29 N_steiner
     long long ncand = 0, created = 0;

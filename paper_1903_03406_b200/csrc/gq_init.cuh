@@ -98,11 +98,11 @@ __global__ void k_init_region(Dev D, Cand C, Scr SC, const int* pend, const int*
     RegionOut O = region_view(C, c, sv, 0);
     int seeds[1] = {t};
     Allow A; A.n = 0;
-    atomicAdd(&g_region_calls, 1ull);
+    atomicAdd(&D.ctr->region_calls, 1ull);
     int r = region_compute(D, p, seeds, 1, A, S, O, true);
     store_region(C, c, O);
     C.extra[c] = -1; C.kind[c] = K_TET; C.rank[c] = c; C.memb[c] = round;
-    if (r == RS_OK) { C.status[c] = CS_OK; atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf)); }
+    if (r == RS_OK) { C.status[c] = CS_OK; atomicAdd(&D.ctr->tested, (unsigned long long)(O.ntet + O.nbf)); }
     else if (r == RS_OVERFLOW) { C.status[c] = CS_OVF; C.memb[c] = -1; if (big) raise_err(GQ_ERR_CAP); }
     else { C.status[c] = CS_CNSS; raise_err(GQ_ERR_DEGEN); }
   }

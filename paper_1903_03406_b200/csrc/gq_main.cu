@@ -99,7 +99,9 @@ int gq_create(int device, gq_ctx** out) {
 int gq_destroy(gq_ctx* c) {
   if (!c) return GQ_EINVAL;
   try {
+    CtxScope scope(c);
     cudaSetDevice(c->device);
+    if (c->st) cudaStreamSynchronize(c->st);
     free_all(c);
     for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
     { DevCache& C = dev_cache(); std::lock_guard<std::mutex> g(C.mu); cache_trim(C); }
@@ -117,6 +119,7 @@ int gq_refine(gq_ctx* c, const double* xyz, int32_t n, int32_t n_input, const in
   if (!c || !xyz || n < 4 || !order || !cfg) return GQ_EINVAL;
   if (cfg->B <= 0 || cfg->max_rounds < 1) return GQ_EINVAL;
   try {
+    CtxScope scope(c);
     CK(cudaSetDevice(c->device));
     refine_impl(c, xyz, n, n_input, seg, m, poly_off, poly_idx, f, poly_keep, order, cfg, counts);
   } catch (std::exception& e) {
@@ -129,41 +132,44 @@ int gq_refine(gq_ctx* c, const double* xyz, int32_t n, int32_t n_input, const in
 int gq_export_mesh(gq_ctx* c, double* points, uint8_t* vert_origin, int32_t* vert_tet, int32_t* tv, int32_t* tn,
                    uint8_t* alive, uint8_t* sub_mask, uint8_t* seg_mask, double* ratio, uint8_t* skip_flag) {
   if (!c || !c->allocated) return GQ_EINVAL;
+  CtxScope scope(c);
   try {
     pull(c);
     Dev& D = c->D;
     size_t nv = c->hc.nv, nt = c->hc.nt;
-    if (points) CK(cudaMemcpy(points, D.P, 24 * nv, cudaMemcpyDeviceToHost));
-    if (vert_origin) CK(cudaMemcpy(vert_origin, D.vorigin, nv, cudaMemcpyDeviceToHost));
-    if (vert_tet) CK(cudaMemcpy(vert_tet, D.vert_tet, 4 * nv, cudaMemcpyDeviceToHost));
-    if (tv && nt) CK(cudaMemcpy2D(tv, 16, D.tv.p, 32, 16, nt, cudaMemcpyDeviceToHost));   // strided halves of the records
-    if (tn && nt) CK(cudaMemcpy2D(tn, 16, D.tn.p, 32, 16, nt, cudaMemcpyDeviceToHost));
-    if (alive) CK(cudaMemcpy(alive, D.alive, nt, cudaMemcpyDeviceToHost));
-    if (sub_mask) CK(cudaMemcpy(sub_mask, D.sub, nt, cudaMemcpyDeviceToHost));
-    if (seg_mask) CK(cudaMemcpy(seg_mask, D.seg, nt, cudaMemcpyDeviceToHost));
-    if (ratio) CK(cudaMemcpy(ratio, D.ratio, 8 * nt, cudaMemcpyDeviceToHost));
-    if (skip_flag) CK(cudaMemcpy(skip_flag, D.skip, nt, cudaMemcpyDeviceToHost));
+    if (points) d2h(c, points, D.P, 24 * nv);
+    if (vert_origin) d2h(c, vert_origin, D.vorigin, nv);
+    if (vert_tet) d2h(c, vert_tet, D.vert_tet, 4 * nv);
+    if (tv && nt) CK(cudaMemcpy2DAsync(tv, 16, D.tv.p, 32, 16, nt, cudaMemcpyDeviceToHost, c->st));   // strided halves of the records
+    if (tn && nt) CK(cudaMemcpy2DAsync(tn, 16, D.tn.p, 32, 16, nt, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (alive) d2h(c, alive, D.alive, nt);
+    if (sub_mask) d2h(c, sub_mask, D.sub, nt);
+    if (seg_mask) d2h(c, seg_mask, D.seg, nt);
+    if (ratio) d2h(c, ratio, D.ratio, 8 * nt);
+    if (skip_flag) d2h(c, skip_flag, D.skip, nt);
   } catch (std::exception& e) { c->err = e.what(); return GQ_ECUDA; }
   return GQ_OK;
 }
 
 int gq_export_constraints(gq_ctx* c, int32_t* subsegments, int32_t* subfaces) {
   if (!c || !c->allocated) return GQ_EINVAL;
+  CtxScope scope(c);
   try {
     pull(c);
     Dev& D = c->D;
     int ns = c->hc.nsegrec, nf = c->hc.nfacerec;
     std::vector<int2> uv(ns); std::vector<int> sid(ns); std::vector<unsigned int> sfl(ns);
-    CK(cudaMemcpy(uv.data(), D.sg_uv, 8 * (size_t)ns, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(sid.data(), D.sg_sid, 4 * (size_t)ns, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(sfl.data(), D.sg_fl, 4 * (size_t)ns, cudaMemcpyDeviceToHost));
+    d2h(c, uv.data(), D.sg_uv, 8 * (size_t)ns);
+    d2h(c, sid.data(), D.sg_sid, 4 * (size_t)ns);
+    d2h(c, sfl.data(), D.sg_fl, 4 * (size_t)ns);
     std::vector<std::array<int, 3>> s;
     for (int r = 0; r < ns; ++r) if (sfl[r] & RF_LIVE) s.push_back({uv[r].x, uv[r].y, sid[r]});
     std::sort(s.begin(), s.end());
     if (subsegments) for (size_t i = 0; i < s.size(); ++i) for (int k = 0; k < 3; ++k) subsegments[3 * i + k] = s[i][k];
     std::vector<int4> fv(nf); std::vector<unsigned int> ffl(nf);
-    CK(cudaMemcpy(fv.data(), D.sf_v, 16 * (size_t)nf, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(ffl.data(), D.sf_fl, 4 * (size_t)nf, cudaMemcpyDeviceToHost));
+    d2h(c, fv.data(), D.sf_v, 16 * (size_t)nf);
+    d2h(c, ffl.data(), D.sf_fl, 4 * (size_t)nf);
     std::vector<std::array<int, 4>> fs;
     for (int r = 0; r < nf; ++r) if (ffl[r] & RF_LIVE) fs.push_back({fv[r].x, fv[r].y, fv[r].z, fv[r].w});
     std::sort(fs.begin(), fs.end());
@@ -183,11 +189,12 @@ int gq_export_rounds(gq_ctx* c, int64_t* rows, double* seconds) {
 
 int gq_export_skipped(gq_ctx* c, int32_t* rows) {
   if (!c || !c->allocated) return GQ_EINVAL;
+  CtxScope scope(c);
   try {
     pull(c);
     int n = std::min(c->hc.nskip, c->L.cap);
     std::vector<int> r(8 * (size_t)n);
-    if (n) CK(cudaMemcpy(r.data(), c->L.rows, 32 * (size_t)n, cudaMemcpyDeviceToHost));
+    if (n) d2h(c, r.data(), c->L.rows, 32 * (size_t)n);
     for (int i = 0; i < n; ++i) {
       rows[7 * i] = r[8 * i + 1]; rows[7 * i + 1] = r[8 * i + 2]; rows[7 * i + 2] = r[8 * i + 3];
       for (int k = 0; k < 4; ++k) rows[7 * i + 3 + k] = r[8 * i + 4 + k];
@@ -198,15 +205,16 @@ int gq_export_skipped(gq_ctx* c, int32_t* rows) {
 
 int gq_quality(gq_ctx* c, double B, int64_t* bad_count, int64_t* hist36) {
   if (!c || !c->allocated) return GQ_EINVAL;
+  CtxScope scope(c);
   try {
     unsigned long long* d = dmalloc<unsigned long long>(37);
-    CK(cudaMemset(d, 0, 37 * 8));
+    CK(cudaMemsetAsync(d, 0, 37 * 8, c->st));
     pull(c);
     k_quality<<<grid_for(c->hc.nt), 128, 0, c->st>>>(c->D, B, d, d + 1);
     CK(cudaGetLastError());
     sync(c);
     unsigned long long h[37];
-    CK(cudaMemcpy(h, d, 37 * 8, cudaMemcpyDeviceToHost));
+    d2h(c, h, d, 37 * 8);
     dfree(d);
     if (bad_count) *bad_count = (int64_t)h[0];
     if (hist36) for (int k = 0; k < 36; ++k) hist36[k] = (int64_t)h[1 + k];

@@ -53,10 +53,10 @@ __global__ void k_region(Dev D, Cand C, Scr SC, int n0, int n1, const int* list,
     int pr = probe;
     if (pr == 3) pr = C.kind[c] == K_TET ? 2 : (C.kind[c] == K_FACE ? 1 : 0);
     RegionOut O = region_view(C, c, v, pr);
-    atomicAdd(&g_region_calls, 1ull);
+    atomicAdd(&D.ctr->region_calls, 1ull);
     int st = ns == 0 ? RS_CNSS : region_compute(D, C.p + 3 * (size_t)c, seeds, ns, allow_of(C, c), S, O);
     store_region(C, c, O);
-    if (st == RS_OK) atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf));
+    if (st == RS_OK) atomicAdd(&D.ctr->tested, (unsigned long long)(O.ntet + O.nbf));
     if (st == RS_OK) {
       C.status[c] = (O.mind <= D.too_close_sq) ? CS_TOOCLOSE : CS_OK;
     } else if (st == RS_OVERFLOW) {
@@ -133,10 +133,10 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_region_warp(Dev D, Cand
     RegionOut O = region_view(C, c, v, 0);
     int st = ns == 0 ? RS_CNSS : region_warp(D, C.p + 3 * (size_t)c, W.seeds, ns, allow_of(C, c), W, S, O);
     if (lane == 0) {
-      atomicAdd(&g_region_calls, 1ull);
+      atomicAdd(&D.ctr->region_calls, 1ull);
       store_region(C, c, O);
       if (st == RS_OK) {
-        atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf));
+        atomicAdd(&D.ctr->tested, (unsigned long long)(O.ntet + O.nbf));
         C.status[c] = (O.mind <= D.too_close_sq) ? CS_TOOCLOSE : CS_OK;
       } else if (st == RS_OVERFLOW) C.status[c] = CS_OVF;
       else if (st == RS_MEMBRANE) { C.status[c] = CS_MEMB; C.memb[c] = O.memb; }
@@ -208,10 +208,10 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_init_region_warp(Dev D,
     int r = region_warp(D, p, W.seeds, 1, A, W, S, O, true);
     if (lane == 0 && g_wdbg) g_wdbg[2 * gw + 1] = 99;
     if (lane == 0) {
-      atomicAdd(&g_region_calls, 1ull);
+      atomicAdd(&D.ctr->region_calls, 1ull);
       store_region(C, c, O);
       C.extra[c] = -1; C.kind[c] = K_TET; C.rank[c] = c; C.memb[c] = round;
-      if (r == RS_OK) { C.status[c] = CS_OK; atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf)); }
+      if (r == RS_OK) { C.status[c] = CS_OK; atomicAdd(&D.ctr->tested, (unsigned long long)(O.ntet + O.nbf)); }
       else if (r == RS_OVERFLOW) { C.status[c] = CS_OVF; C.memb[c] = -1; }
       else { C.status[c] = CS_CNSS; raise_err(GQ_ERR_DEGEN); }
     }
@@ -237,10 +237,10 @@ __global__ void __launch_bounds__(BR_THREADS) k_region_block(Dev D, Cand C, Scr 
     RegionOut O = region_view(C, c, v, 0);
     int st = s_ns == 0 ? RS_CNSS : region_block(D, C.p + 3 * (size_t)c, s_seeds, s_ns, allow_of(C, c), B, S, O);
     if (threadIdx.x == 0) {
-      atomicAdd(&g_region_calls, 1ull);
+      atomicAdd(&D.ctr->region_calls, 1ull);
       store_region(C, c, O);
       if (st == RS_OK) {
-        atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf));
+        atomicAdd(&D.ctr->tested, (unsigned long long)(O.ntet + O.nbf));
         C.status[c] = (O.mind <= D.too_close_sq) ? CS_TOOCLOSE : CS_OK;
       } else if (st == RS_OVERFLOW) { C.status[c] = CS_CNSS; raise_err(GQ_ERR_CAP); }
       else if (st == RS_MEMBRANE) { C.status[c] = CS_MEMB; C.memb[c] = O.memb; }
@@ -274,10 +274,10 @@ __global__ void __launch_bounds__(BR_THREADS) k_init_region_block(Dev D, Cand C,
     Allow A; A.n = 0;
     int st = region_block(D, PT(D, pend[c]), seeds, 1, A, B, S, O);
     if (threadIdx.x == 0) {
-      atomicAdd(&g_region_calls, 1ull);
+      atomicAdd(&D.ctr->region_calls, 1ull);
       store_region(C, c, O);
       C.extra[c] = -1; C.kind[c] = K_TET; C.rank[c] = c; C.memb[c] = round;
-      if (st == RS_OK) { C.status[c] = CS_OK; atomicAdd(&g_tested, (unsigned long long)(O.ntet + O.nbf)); }
+      if (st == RS_OK) { C.status[c] = CS_OK; atomicAdd(&D.ctr->tested, (unsigned long long)(O.ntet + O.nbf)); }
       else if (st == RS_OVERFLOW) { C.status[c] = CS_OVF; C.memb[c] = -1; raise_err(GQ_ERR_CAP); }
       else { C.status[c] = CS_CNSS; raise_err(GQ_ERR_DEGEN); }
     }

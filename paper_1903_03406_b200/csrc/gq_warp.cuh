@@ -292,6 +292,9 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
     }
   }
   __syncwarp();
+  if (__any_sync(FULL, bf_has_ghost_part(D, O.bf, nbf, lane, 32)) &&
+      __any_sync(FULL, bf_open_part(D, O.bf, nbf, lane, 32)))
+    return RS_BADSTAR;
   WSTOP(5);
   WMARK(15);
   // boundary vertices: min distance and the swallow check (hash reused)

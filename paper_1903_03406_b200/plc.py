@@ -346,25 +346,42 @@ def unit_cube() -> PLC:
 # ---------------------------------------------------------------------------
 # domain closure (refine.py:421-506)
 
-def hull_covered(plc: PLC) -> bool:
-    """True when the polygons tile the convex hull of the points.  Same
-    decision as refine.py:421-459, indexed by vertex instead of scanning all
-    polygons per hull triangle."""
+def hull_simplices(plc: PLC):
+    """Triangles of the convex hull of the points (scipy Qhull, as the
+    reference's _hull_covered uses, refine.py:455-459), or None."""
     from scipy.spatial import ConvexHull, QhullError
 
     try:
-        hull = ConvexHull(points_array(plc))
+        return ConvexHull(points_array(plc)).simplices
     except QhullError:
+        return None
+
+
+def hull_axis_aligned(plc: PLC, simplices) -> bool:
+    """True when every hull triangle lies in a coordinate plane (its three
+    vertices share one coordinate exactly)."""
+    tri = points_array(plc)[np.asarray(simplices)]
+    same = (tri[:, 0, :] == tri[:, 1, :]) & (tri[:, 0, :] == tri[:, 2, :])
+    return bool(np.all(np.any(same, axis=1)))
+
+
+def hull_covered(plc: PLC, simplices=None) -> bool:
+    """True when the polygons tile the convex hull of the points.  Same
+    decision as refine.py:421-459, indexed by vertex instead of scanning all
+    polygons per hull triangle."""
+    if simplices is None:
+        simplices = hull_simplices(plc)
+    if simplices is None:
         return False
     from .setup_fast import certify_hull_covered
-    if certify_hull_covered(plc, hull.simplices):
+    if certify_hull_covered(plc, simplices):
         return True
     by_vertex = {}
     for pid, poly in enumerate(plc.polygons):
         for v in poly:
             by_vertex.setdefault(v, []).append(pid)
     cache = {}
-    for simplex in hull.simplices:
+    for simplex in simplices:
         tri = [int(v) for v in simplex]
         cands = set(by_vertex.get(tri[0], ()))
         for v in tri[1:]:
@@ -390,9 +407,20 @@ def hull_covered(plc: PLC) -> bool:
 def augment_with_box(plc: PLC) -> PLC:
     """Wrap the points in an axis-aligned box padded by 0.25*diag unless the
     polygons already tile the hull (refine.py:462-506); corners, edges and
-    faces are appended after the input features in the same order."""
-    if plc.polygons and hull_covered(plc):
-        return plc
+    faces are appended after the input features in the same order.
+
+    One deliberate difference: a hull tiled by polygons that are not all in
+    coordinate planes (a sphere's triangles) gets the box too.  The reference
+    boxes the domain precisely so that boundary Steiner points round exactly
+    onto their facet planes (refine.py:466-473); on an oblique hull facet a
+    rounded midpoint lands a few ulps outside the hull, and its ghost cavity
+    need not star.  The reference never reaches that case (it stops on
+    oblique facets in Tri2D), so every input it refines is
+    unaffected."""
+    if plc.polygons:
+        hs = hull_simplices(plc)
+        if hs is not None and hull_covered(plc, hs) and hull_axis_aligned(plc, hs):
+            return plc
     lo, hi = bounding_box(plc)
     pad = 0.25 * math.dist(lo, hi)
     lo = tuple(x - pad for x in lo)

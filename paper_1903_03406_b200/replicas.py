@@ -40,7 +40,12 @@ def run_replicas(plcs, B: float, worker=None, group=None):
         secs += float(t)
     if world > 1:
         backend = dist.get_backend(group)
-        dev = "cuda" if backend == "nccl" else "cpu"
+        if backend == "nccl":
+            from .refine import default_device
+            dev = torch.device("cuda", default_device())   # this rank's GPU (LOCAL_RANK)
+            torch.cuda.set_device(dev)
+        else:
+            dev = torch.device("cpu")
         tt = torch.tensor([secs], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX, group=group)
         ss = torch.tensor([steiner, len(mine)], dtype=torch.float64, device=dev)

@@ -5,7 +5,7 @@ import pytest
 
 from paper_1903_03406_b200 import PLC, RefineConfig, synth, unit_cube, validate
 from paper_1903_03406_b200.errors import InvalidPLC
-from paper_1903_03406_b200.plc import augment_with_box, hull_covered
+from paper_1903_03406_b200.plc import augment_with_box, hull_axis_aligned, hull_covered, hull_simplices
 from paper_1903_03406_b200.prepare import facet_keep, prepare, shuffle_order
 
 
@@ -42,6 +42,18 @@ def test_box_closure():
     seg = synth.segments_cloud(50, 2, 0)
     aug = augment_with_box(seg)
     assert len(aug.points) == len(seg.points) + 8 and len(aug.polygons) == 6 and len(aug.segments) == 2 + 12
+
+
+def test_box_for_oblique_hull():
+    """A hull tiled by oblique polygons (a sphere) is boxed too (plc.py
+    augment_with_box docstring); an axis-aligned tiled hull is not."""
+    plc = synth.nested_surfaces(200, level=3, torus=(8, 4))
+    hs = hull_simplices(plc)
+    assert hull_covered(plc, hs) and not hull_axis_aligned(plc, hs)
+    aug = augment_with_box(plc)
+    assert len(aug.points) == len(plc.points) + 8 and len(aug.polygons) == len(plc.polygons) + 6
+    cube = synth.cube_points(10, 0)
+    assert hull_axis_aligned(cube, hull_simplices(cube))
 
 
 def test_prepare_and_order():
