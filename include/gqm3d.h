@@ -51,6 +51,10 @@ typedef struct {
   int64_t region_calls;
   int64_t bytes_alg;           /* region kernels' algorithmic HBM bytes (58 B/tet tested + 24 B/point) */
   double region_ms;            /* time in the region (cavity) kernels */
+  /* SURVEY 8(d) whole-refine algorithmic bytes:
+   *   144 N_cand + 58 T_tested + 8 K_claims + 51 T_created + 1 T_deleted + 29 N_steiner */
+  int64_t n_cand, t_tested, k_claims, t_created, t_deleted;
+  int64_t bytes_refine;
 } gq_counts;
 
 /* create a context on CUDA device `device` */

@@ -29,7 +29,9 @@ class GqCounts(ctypes.Structure):
                 ("input_points", ctypes.c_int64), ("exact_calls", ctypes.c_int64 * 4),
                 ("device_ms", ctypes.c_double), ("init_ms", ctypes.c_double),
                 ("kernel_launches", ctypes.c_int64), ("region_calls", ctypes.c_int64),
-                ("bytes_alg", ctypes.c_int64), ("region_ms", ctypes.c_double)]
+                ("bytes_alg", ctypes.c_int64), ("region_ms", ctypes.c_double),
+                ("n_cand", ctypes.c_int64), ("t_tested", ctypes.c_int64), ("k_claims", ctypes.c_int64),
+                ("t_created", ctypes.c_int64), ("t_deleted", ctypes.c_int64), ("bytes_refine", ctypes.c_int64)]
 
 
 EXPORTS = ("gq_create", "gq_destroy", "gq_last_error", "gq_refine", "gq_export_mesh", "gq_export_constraints",

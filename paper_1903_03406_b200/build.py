@@ -26,17 +26,21 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    if not force and up_to_date():
-        return SO
+SO_DBG = os.path.join(HERE, "libgqm3d_dbg.so")   # diagnostics build: device error sites printed (GQM3D_LIB=...)
+
+
+def build(force: bool = False, verbose: bool = True, debug: bool = False) -> str:
+    so = SO_DBG if debug else SO
+    if not force and os.path.exists(so) and all(os.path.getmtime(d) <= os.path.getmtime(so) for d in DEPS):
+        return so
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", SO + ".tmp", SRC, SRC_IO]
+    cmd = [nvcc, *NVCC_FLAGS, *(["-DGQ_DEBUG2D"] if debug else []), "-o", so + ".tmp", SRC, SRC_IO]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(so + ".tmp", so)
+    return so
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    build(force="--force" in sys.argv, debug="--debug" in sys.argv)

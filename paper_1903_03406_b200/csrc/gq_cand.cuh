@@ -91,6 +91,7 @@ __device__ inline unsigned long long prio_hash(const int* canon, int n, int roun
 // skipped-element log
 struct SkipLog { int* rows; int cap; };   // 8 ints: round, kind, reason, n, v0..v3
 __device__ __noinline__ void log_skip(const Dev& D, const SkipLog& L, int round_no, int kind, int reason, const int* v, int n) {
+  atomicAdd(&D.ctr->skipr[(kind & 3) * 4 + (reason & 3)], 1u);
   int k = atomicAdd(&D.ctr->nskip, 1);
   if (k >= L.cap) { raise_err(GQ_ERR_CAP); return; }
   int* r = L.rows + 8 * (size_t)k;

@@ -39,11 +39,16 @@ struct Counters {
   // instrumentation (SURVEY 8(d) algorithmic bytes), per context
   unsigned long long region_calls;   // region computations
   unsigned long long tested;         // tets tested for membership (cavity + boundary neighbours)
+  unsigned long long cands;          // refinement candidates constructed (N_cand)
+  unsigned long long claims;         // claim keys of the candidates entering a filter (K_claims)
+  unsigned long long created;        // tets created by stars, bulk construction included (T_created)
+  unsigned long long deleted;        // cavity tets deleted (T_deleted)
   // verification outcomes of the last check pass (diagnostics, verbose rounds):
   // [0] subsegments missing, [1] encroached by a vertex off the segment line,
   // [2] encroached by a (near-)collinear vertex, [3] subfaces missing,
   // [4] encroached by an off-plane apex, [5] encroached by a (near-)coplanar apex
   unsigned int chk[8];
+  unsigned int skipr[12];            // skipped elements by kind * 4 + reason (diagnostics)
 };
 
 // A tet is one 32-byte record {tv, tn} (vertices, then packed neighbour
@@ -906,6 +911,7 @@ struct Tri2Ctx {
   int pid;
   int vid;           // vertex being inserted (its 2D position is p)
   double p[2];
+  int follow3d;      // oblique polygon: the 2D cavity is the 3D cavity's crossed subfaces (see tri2_cavity)
   __device__ void pos(int v, double* out) const {
     if (v == vid) { out[0] = p[0]; out[1] = p[1]; return; }
     proj2(*D, pid, PT(*D, v), out);
@@ -961,6 +967,20 @@ __device__ __noinline__ int tri2_cavity(const Tri2Ctx& C, const int* forced, int
   const Dev& D = *C.D;
   set.clear();
   int n = 0;
+  if (C.follow3d) {
+    // Oblique polygon.  Its Steiner points round off the polygon plane, so an
+    // in-plane Delaunay cavity and the 3D cavity disagree near cocircular
+    // configurations; every disagreement leaves a missing subface whose split
+    // makes more (a runaway the reference never meets: it stops on oblique
+    // facets).  The retiling therefore follows the mesh: remove
+    // exactly the subfaces the 3D cavity crossed (plus the split edge's
+    // triangles) and fan p onto their rim, whose edges all lie on the 3D
+    // cavity boundary -- every new subface is a face of the new star
+    // (SURVEY F5's 3D-derived delta).  In-plane Delaunay quality is then
+    // restored by the ordinary encroachment checks.
+    nseeds = 0;
+    if (nforced == 0) return 0;
+  }
   // own Delaunay cavity from the first seed in region
   int seed = -1;
   for (int k = 0; k < nseeds && seed < 0; ++k)

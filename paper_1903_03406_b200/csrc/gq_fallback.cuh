@@ -50,7 +50,7 @@ __device__ __noinline__ void insert_one(const Dev& D, const Cand& C, int c, Scra
     for (int k = 0; k < np; ++k) {
       int w = item0 + k;
       int pid = pids[k];
-      Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = vid;
+      Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = vid; X.follow3d = D.poly_obl[pid];
       proj2(D, pid, p, X.p);
       int forced[CC + 2]; int nf;
       t2_forced(D, C, c, pid, forced, nf, CC + 2);
@@ -101,6 +101,7 @@ __device__ __noinline__ void insert_one(const Dev& D, const Cand& C, int c, Scra
   if (nt0 + C.nbf[c] > D.tcap) { raise_err(GQ_ERR_CAP); return; }
   C.nt0[c] = nt0;
   star_insert(D, vid, v.bf, C.nbf[c], nt0, false);
+  atomicAdd(&D.ctr->created, (unsigned long long)C.nbf[c]); atomicAdd(&D.ctr->deleted, (unsigned long long)C.ntet[c]);
   for (int j = 0; j < C.nbsub[c]; ++j) { int r = v.bsub[j]; if (r >= 0 && (D.sf_fl[r] & RF_LIVE)) D.sf_fl[r] |= RF_CHECK; }
   for (int j = 0; j < C.nbseg[c]; ++j) { int r = v.bseg[j]; if (r >= 0 && (D.sg_fl[r] & RF_LIVE)) D.sg_fl[r] |= RF_CHECK; }
   for (int w = item0; w < item0 + nitems; ++w) {

@@ -311,8 +311,11 @@ static unsigned int pow2_at_least(size_t n) { unsigned int p = 1024; while (p < 
 
 static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   Dev& D = c->D;
-  size_t vcap = 65536 + (size_t)n * 8;
-  size_t tcap = std::max<size_t>(1 << 21, (size_t)n * 64);
+  double capx = getenv("GQ_CAPX") ? atof(getenv("GQ_CAPX")) : 1.0;   // experiments: capacity multiplier
+  // (the minimums cover bulk construction and the initial constraints; the
+  // rounds grow everything on demand, gq_grow.cuh)
+  size_t vcap = std::max<size_t>((size_t)(capx * (65536 + (size_t)n * 8)), (size_t)n + 1024);
+  size_t tcap = std::max<size_t>((size_t)(capx * std::max<size_t>(1 << 21, (size_t)n * 64)), (size_t)n * 16 + 4096);
   D.vcap = (int)vcap; D.tcap = (int)tcap;
   D.P = dmalloc<double>(3 * vcap); D.vorigin = dmalloc<uint8_t>(vcap); D.vert_tet = dmalloc<int>(vcap);
   D.vsid = dmalloc<int>(vcap);
@@ -321,19 +324,19 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   D.ratio = dmalloc<double>(tcap);
   CK(cudaMemsetAsync(D.alive, 0, tcap, c->st));
   if (getenv("GQ_PROFILE")) std::fprintf(stderr, "[gq] capacities: verts %zu tets %zu\n", vcap, tcap);
-  size_t sgcap = 65536 + (size_t)m * 32 + vcap / 8;
+  size_t sgcap = std::max<size_t>((size_t)(capx * (65536 + (size_t)m * 32 + vcap / 8)), (size_t)m + 1024);
   D.sgcap = (int)sgcap;
   D.sg_uv = dmalloc<int2>(sgcap); D.sg_sid = dmalloc<int>(sgcap); D.sg_fl = dmalloc<unsigned int>(sgcap);
   unsigned int sgh = pow2_at_least(2 * sgcap);
   D.sg_hk = dmalloc<unsigned long long>(sgh); D.sg_hv = dmalloc<int>(sgh); D.sg_hmask = sgh - 1;
   CK(cudaMemsetAsync(D.sg_hk, 0xff, (size_t)sgh * 8, c->st));
-  size_t sfcap = 65536 + (size_t)npidx * 32 + vcap;
+  size_t sfcap = std::max<size_t>((size_t)(capx * (65536 + (size_t)npidx * 32 + vcap)), (size_t)npidx + 1024);
   D.sfcap = (int)sfcap;
   D.sf_v = dmalloc<int4>(sfcap); D.sf_fl = dmalloc<unsigned int>(sfcap);
   unsigned int sfh = pow2_at_least(2 * sfcap);
   D.sf_hk = dmalloc<unsigned long long>(sfh); D.sf_hv = dmalloc<int>(sfh); D.sf_hmask = sfh - 1;
   CK(cudaMemsetAsync(D.sf_hk, 0xff, (size_t)sfh * 8, c->st));
-  size_t t2cap = 65536 + (size_t)npidx * 8 + 2 * vcap;
+  size_t t2cap = std::max<size_t>((size_t)(capx * (65536 + (size_t)npidx * 8 + 2 * vcap)), 2 * (size_t)npidx + 1024);
   D.t2cap = (int)t2cap;
   D.t2v = dmalloc<int4>(t2cap); D.t2alive = dmalloc<uint8_t>(t2cap);
   CK(cudaMemsetAsync(D.t2alive, 0, t2cap, c->st));
@@ -937,14 +940,17 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
 
 // ------------------------------------------------------------------ round
 
-__global__ void k_states(Cand C, int n, int* okf, int* failf) {
+__global__ void k_states(Dev D, Cand C, int n, int* okf, int* failf) {
+  unsigned long long claims = 0;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     int st = C.status[c];
     int s = st == CS_OK ? 0 : (st == CS_DROP ? -1 : 3);
     C.state[c] = s;
     okf[c] = s == 0;
     failf[c] = s == 3;
+    if (s == 0) claims += C.ntet[c] + C.nbf[c] + C.ncr[c] + C.nbseg[c] + C.neseg[c] + (C.extra[c] >= 0);
   }
+  if (claims) atomicAdd(&D.ctr->claims, claims);
 }
 __global__ void k_kept(Cand C, int n, int* keep) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) keep[c] = C.status[c] != CS_DROP;
@@ -1007,6 +1013,8 @@ static int scan_total(gq_ctx* c, const int* in, int* out, int n) {
   return a + b;
 }
 
+#include "gq_grow.cuh"
+
 static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* inserted, int round_no) {
   Cand& C = c->C;
   double t0 = now_s();
@@ -1027,7 +1035,7 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
   int nv = c->hc.nv, nt = c->hc.nt;
   LAUNCH(k_gather_nbf, ni, C, ins, ni, flags);
   int tot = scan_total(c, flags, pos, ni);
-  if (nt + tot > c->D.tcap || nv + ni > c->D.vcap) throw std::runtime_error("mesh capacity exceeded");
+  ensure_mesh_room(c, (long long)nv + ni, (long long)nt + tot);
   LAUNCH(k_assign_ids, ni, C, ins, ni, pos, nv, nt);
   Ins I; I.list = ins; I.n = ni; I.nv0 = nv; I.nt0base = nt;
   fine(c, 18);
@@ -1125,6 +1133,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   RoundOut R;
   c->big_used = 0;
   pull(c);
+  maintain_capacity(c);
   ensure_q(c, (size_t)std::max(std::max(c->hc.nt, c->hc.nsegrec + c->hc.nfacerec), c->C.cap) * 2 + 4096);
   ensure_tmp(c, (size_t)std::max(std::max(c->hc.nt, c->hc.nsegrec + c->hc.nfacerec), c->C.cap) + 4096);
   double t0 = now_s();
@@ -1197,7 +1206,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   fine(c, 23);
   double t1 = now_s();
   ensure_tmp(c, n + 1);
-  LAUNCH(k_states, n, c->C, n, c->Q.a, c->Q.b);
+  LAUNCH(k_states, n, c->D, c->C, n, c->Q.a, c->Q.b);
   int nok = scan_total(c, c->Q.a, c->Q.c, n);
   int nfail = select_flagged(c, c->Q.b, n, c->Q.h);
   fine(c, 15);
@@ -1213,6 +1222,8 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   t1 = now_s();
   fine(c, -1);
   if (nfail > 0) {
+    pull(c);
+    ensure_mesh_room(c, (long long)c->hc.nv + nfail, (long long)c->hc.nt + 1024LL * nfail + 65536);
     FallbackIO F; F.list = c->Q.h; F.n = nfail; F.round_no = round_no; F.seed = c->seed;
     F.with_facets = c->npoly > 0; F.lmin2 = lmin2; F.inserted = c->d_int + 20;
     CK(cudaMemsetAsync(c->d_int + 20, 0, 4, c->st));
@@ -1400,9 +1411,12 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
       pull(c);
       const unsigned int* k = c->hc.chk;
       std::fprintf(stderr, "round %d phase=%d candidates=%lld accepted=%lld blasted=%lld failed=%lld inserted=%lld time=%.4f"
-                   " | nv %d nt %d segs %d faces %d skipped %d | check: seg miss %u enc %u (collinear %u) face miss %u enc %u (coplanar %u)\n",
+                   " | nv %d nt %d segs %d faces %d skipped %d | check: seg miss %u enc %u (collinear %u) face miss %u enc %u (coplanar %u)"
+                   " | skips seg %u/%u/%u/%u face %u/%u/%u/%u tet %u/%u/%u/%u\n",
                    round_no, R.phase, R.ncand, R.acc, R.rej, R.failed, R.inserted, dt, c->hc.nv, c->hc.nt, c->hc.nsegrec,
-                   c->hc.nfacerec, c->hc.nskip, k[0], k[1], k[2], k[3], k[4], k[5]);
+                   c->hc.nfacerec, c->hc.nskip, k[0], k[1], k[2], k[3], k[4], k[5], c->hc.skipr[0], c->hc.skipr[1],
+                   c->hc.skipr[2], c->hc.skipr[3], c->hc.skipr[4], c->hc.skipr[5], c->hc.skipr[6], c->hc.skipr[7],
+                   c->hc.skipr[8], c->hc.skipr[9], c->hc.skipr[10], c->hc.skipr[11]);
     }
     round_no += 1;
   }
@@ -1453,6 +1467,10 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
     // (cavity + boundary neighbours: tv 16 + tn 16 + masks 2 + one vertex 24)
     // + 24 B per candidate point
     out->bytes_alg = 58 * (long long)tested + 24 * (long long)rc;
+    out->n_cand = (int64_t)c->hc.cands; out->t_tested = (int64_t)tested; out->k_claims = (int64_t)c->hc.claims;
+    out->t_created = (int64_t)c->hc.created; out->t_deleted = (int64_t)c->hc.deleted;
+    out->bytes_refine = 144 * out->n_cand + 58 * out->t_tested + 8 * out->k_claims + 51 * out->t_created +
+                        out->t_deleted + 29 * (int64_t)(c->hc.nv - n);
   }
 }
 

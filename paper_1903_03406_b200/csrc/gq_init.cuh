@@ -270,7 +270,7 @@ __global__ void k_facets_init(Dev D, const int* poff, const int* pidx, int f, Sc
   Scratch S = scratch_for(SC, tid);
   for (int pid = tid; pid < f; pid += gridDim.x * blockDim.x) {
     int o0 = poff[pid], o1 = poff[pid + 1];
-    Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = -2;
+    Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = -2; X.follow3d = 0;
     int base[3]; int nb = 0;
     int last = -1;
     for (int k = o0; k < o1; ++k) {

@@ -118,7 +118,7 @@ __device__ void t2_compute_body(const Dev& D, const Cand& C, const T2Items& T, S
   for (int w = start; w < T.n; w += stride) {
     if (T.state[w] != 0) continue;
     int c = T.cand[w], pid = T.pid[w];
-    Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = C.vid[c];
+    Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = C.vid[c]; X.follow3d = D.poly_obl[pid];
     proj2(D, pid, C.p + 3 * (size_t)c, X.p);
     int forced[CC + 2]; int nf;
     t2_forced(D, C, c, pid, forced, nf, CC + 2);
@@ -171,7 +171,7 @@ __device__ void t2_commit_body(const Dev& D, const Cand& C, const T2Items& T, Sc
   for (int w = start; w < T.n; w += stride) {
     if (T.state[w] != 2) continue;
     int c = T.cand[w], pid = T.pid[w];
-    Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = C.vid[c];
+    Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = C.vid[c]; X.follow3d = D.poly_obl[pid];
     proj2(D, pid, C.p + 3 * (size_t)c, X.p);
     int n = T.ncav[w];
     int* cav = T.cav + (size_t)w * T.cap;
@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(32 * WS_WARPS) k_star_warp(Dev D, Cand C, Ins 
     int nbf = C.nbf[c];
     if (nbf <= WS_MAXF) star_warp(D, C.vid[c], v.bf, nbf, C.nt0[c], true, star_hash_shared(X), nullptr, 0);
     else star_warp(D, C.vid[c], v.bf, nbf, C.nt0[c], true, big_star_hash(SB, gw, &X.flag), nullptr, 0);
+    if (lane == 0) { atomicAdd(&D.ctr->created, (unsigned long long)nbf); atomicAdd(&D.ctr->deleted, (unsigned long long)C.ntet[c]); }
     __syncwarp();
   }
 }
@@ -307,6 +308,7 @@ __global__ void __launch_bounds__(32 * WS_WARPS) k_init_stars_warp(Dev D, Cand C
     int nbf = C.nbf[c];
     if (nbf <= WS_MAXF) star_warp(D, pend[c], v.bf, nbf, C.nt0[c], true, star_hash_shared(X), touched, round);
     else star_warp(D, pend[c], v.bf, nbf, C.nt0[c], true, big_star_hash(SB, gw, &X.flag), touched, round);
+    if (lane == 0) { atomicAdd(&D.ctr->created, (unsigned long long)nbf); atomicAdd(&D.ctr->deleted, (unsigned long long)C.ntet[c]); }
     __syncwarp();
     if (lane == 0) C.status[c] = CS_DROP;
   }

@@ -12,6 +12,7 @@ __global__ void k_make_cands(Dev D, Cand C, Scr SC, int n0, int n1, CandCtx X, S
   for (int c = n0 + tid; c < n1; c += gridDim.x * blockDim.x) {
     C.status[c] = CS_OK;
     C.bigi[c] = -1;
+    atomicAdd(&D.ctr->cands, 1ull);
     bool ok = make_cand(D, C, c, X, S);
     if (C.kind[c] == K_TET) {
       int t = C.tgt[c];

@@ -11,6 +11,7 @@ so validation never flips on near-degenerate input.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from fractions import Fraction
 
@@ -419,7 +420,8 @@ def augment_with_box(plc: PLC) -> PLC:
     unaffected."""
     if plc.polygons:
         hs = hull_simplices(plc)
-        if hs is not None and hull_covered(plc, hs) and hull_axis_aligned(plc, hs):
+        oblique_box = os.environ.get("GQM3D_OBLIQUE_BOX", "1") != "0"   # experiments: 0 = reference rule
+        if hs is not None and hull_covered(plc, hs) and (not oblique_box or hull_axis_aligned(plc, hs)):
             return plc
     lo, hi = bounding_box(plc)
     pad = 0.25 * math.dist(lo, hi)

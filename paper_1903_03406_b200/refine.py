@@ -80,6 +80,9 @@ def refine(plc: PLC, cfg: RefineConfig = None, device: int = None):
                   "export_s": t_exp,
                   "kernel_launches": int(cnt.kernel_launches), "region_calls": int(cnt.region_calls),
                   "region_ms": cnt.region_ms, "bytes_alg": int(cnt.bytes_alg),
+                  "bytes_refine": int(cnt.bytes_refine),
+                  "alg_counts": {"n_cand": int(cnt.n_cand), "t_tested": int(cnt.t_tested), "k_claims": int(cnt.k_claims),
+                                 "t_created": int(cnt.t_created), "t_deleted": int(cnt.t_deleted)},
                   "exact_calls": [int(x) for x in cnt.exact_calls]}
     if cfg.verbose:
         for r in rep.per_round:
