@@ -17,6 +17,10 @@ namespace gq {
 #define BR_MAXT 4096        // cavity tets (== CTB)
 #define BR_HASH 8192
 
+// Storage of the normal tier (dynamic shared memory).  region_block works on a
+// BlockView -- pointers to the arrays plus the shared scalars -- so the same
+// code also runs on global-memory arrays of any capacity (the huge tier:
+// cavities of box corners or far circumcentres, tens of thousands of tets).
 struct BlockShared {
   int hkey[BR_HASH];
   int hval[BR_HASH];
@@ -25,15 +29,23 @@ struct BlockShared {
   int f1[BR_MAXT];
   uint8_t in[BR_MAXT];
   int comp[BR_MAXT];
+};
+struct BlockView {             // lives in __shared__ memory (scalars shared by the block)
+  int* hkey; int* hval; int* cav; int* f0; int* f1; uint8_t* in; int* comp;
+  int hcap, mcap;              // hash slots (power of two) / cavity tets
   int n, nf0, nf1, seed, status, flag, memb, cnt;
   unsigned long long mind;
 };
+__device__ inline void view_of_shared(BlockView& V, BlockShared& S) {
+  V.hkey = S.hkey; V.hval = S.hval; V.cav = S.cav; V.f0 = S.f0; V.f1 = S.f1; V.in = S.in; V.comp = S.comp;
+  V.hcap = BR_HASH; V.mcap = BR_MAXT;
+}
 
-__device__ __forceinline__ unsigned int bh(int k) { return ((unsigned int)k * 2654435761u) & (BR_HASH - 1); }
+__device__ __forceinline__ unsigned int bh(int k, int hcap) { return ((unsigned int)k * 2654435761u) & (unsigned int)(hcap - 1); }
 // claim key k; returns slot if this call inserted it, -1 if present, -2 if full
-__device__ inline int bh_claim(BlockShared& B, int k) {
-  unsigned int i = bh(k);
-  for (int p = 0; p < BR_HASH; ++p) {
+__device__ inline int bh_claim(BlockView& B, int k) {
+  unsigned int i = bh(k, B.hcap);
+  for (int p = 0; p < B.hcap; ++p) {
     int cur = B.hkey[i];
     if (cur == k) return -1;
     if (cur == INT_MIN) {
@@ -41,17 +53,17 @@ __device__ inline int bh_claim(BlockShared& B, int k) {
       if (old == INT_MIN) return (int)i;
       if (old == k) return -1;
     }
-    i = (i + 1) & (BR_HASH - 1);
+    i = (i + 1) & (unsigned int)(B.hcap - 1);
   }
   return -2;
 }
-__device__ inline int bh_find(const BlockShared& B, int k) {
-  unsigned int i = bh(k);
-  for (int p = 0; p < BR_HASH; ++p) {
+__device__ inline int bh_find(const BlockView& B, int k) {
+  unsigned int i = bh(k, B.hcap);
+  for (int p = 0; p < B.hcap; ++p) {
     int cur = B.hkey[i];
     if (cur == k) return B.hval[i];
     if (cur == INT_MIN) return -1;
-    i = (i + 1) & (BR_HASH - 1);
+    i = (i + 1) & (unsigned int)(B.hcap - 1);
   }
   return -1;
 }
@@ -59,9 +71,9 @@ __device__ inline int bh_find(const BlockShared& B, int k) {
 // Requires blockDim.x == BR_THREADS.  Writes O like region_compute; S is the
 // block's global scratch (used only by thread 0 for the constraint pass).
 __device__ inline int region_block(const Dev& D, const double* p, const int* seeds, int nseeds, const Allow& A,
-                                   BlockShared& B, Scratch& S, RegionOut& O) {
+                                   BlockView& B, Scratch& S, RegionOut& O) {
   int tid = threadIdx.x;
-  for (int i = tid; i < BR_HASH; i += BR_THREADS) B.hkey[i] = INT_MIN;
+  for (int i = tid; i < B.hcap; i += BR_THREADS) B.hkey[i] = INT_MIN;
   if (tid == 0) {
     B.status = RS_OK; B.flag = 0; B.memb = INT_MAX; B.n = 0;
     int seed = -1;
@@ -111,7 +123,7 @@ __device__ inline int region_block(const Dev& D, const double* p, const int* see
       if (slot == -2) { B.flag = 1; continue; }
       if (in_region(D, u, p, A)) {
         int idx = atomicAdd(&B.n, 1);
-        if (idx >= BR_MAXT) { B.flag = 1; B.hval[slot] = -2; continue; }
+        if (idx >= B.mcap) { B.flag = 1; B.hval[slot] = -2; continue; }
         B.cav[idx] = u;
         B.hval[slot] = idx;
         int q = atomicAdd(&B.nf1, 1);
@@ -273,7 +285,7 @@ __device__ inline int region_block(const Dev& D, const double* p, const int* see
     return RS_BADSTAR;
   // swallow check + min distance over boundary vertices: reuse the hash as a
   // vertex set (cavity membership is no longer needed)
-  for (int i = tid; i < BR_HASH; i += BR_THREADS) B.hkey[i] = INT_MIN;
+  for (int i = tid; i < B.hcap; i += BR_THREADS) B.hkey[i] = INT_MIN;
   if (tid == 0) { B.mind = 0x7ff0000000000000ull; B.flag = 0; }
   __syncthreads();
   unsigned long long my = 0x7ff0000000000000ull;

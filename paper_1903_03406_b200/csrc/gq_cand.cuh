@@ -55,12 +55,23 @@ struct Cand {          // candidate arrays (capacity cap)
   int* bigi;
   int* btets; int* bbf; int* bcr; int* bcrf; int* bbsub; int* bbseg; int* beseg;
   int nbigcap;
+  // huge slabs (bigi >= HUGE_BASE): capacities ht / hf / hc per slab, plus a
+  // star pairing hash of hs slots per slab
+  int* htets; int* hbf; int* hcr; int* hcrf; int* hbsub; int* hbseg; int* heseg;
+  unsigned long long* hskey; int* hsv0; int* hsv1;
+  int nhugecap, ht, hf, hc, hs;
 };
+#define HUGE_BASE (1 << 28)
 struct SlabView { int* tets; int* bf; int* cr; int* crf; int* bsub; int* bseg; int* eseg; int ct, cf, cc; };
 __device__ __forceinline__ SlabView slab(const Cand& C, int c) {
   SlabView v;
   int b = C.bigi[c];
-  if (b < 0) {
+  if (b >= HUGE_BASE) {
+    size_t h = (size_t)(b - HUGE_BASE);
+    v.tets = C.htets + h * C.ht; v.bf = C.hbf + h * C.hf; v.cr = C.hcr + h * C.hc; v.crf = C.hcrf + h * C.hc;
+    v.bsub = C.hbsub + h * C.hc; v.bseg = C.hbseg + h * C.hc; v.eseg = C.heseg + h * C.hc;
+    v.ct = C.ht; v.cf = C.hf; v.cc = C.hc;
+  } else if (b < 0) {
     v.tets = C.tets + (size_t)c * CT; v.bf = C.bf + (size_t)c * CF; v.cr = C.cr + (size_t)c * CC;
     v.crf = C.crf + (size_t)c * CC; v.bsub = C.bsub + (size_t)c * CC; v.bseg = C.bseg + (size_t)c * CC;
     v.eseg = C.eseg + (size_t)c * CC; v.ct = CT; v.cf = CF; v.cc = CC;
@@ -92,6 +103,14 @@ __device__ inline unsigned long long prio_hash(const int* canon, int n, int roun
 struct SkipLog { int* rows; int cap; };   // 8 ints: round, kind, reason, n, v0..v3
 __device__ __noinline__ void log_skip(const Dev& D, const SkipLog& L, int round_no, int kind, int reason, const int* v, int n) {
   atomicAdd(&D.ctr->skipr[(kind & 3) * 4 + (reason & 3)], 1u);
+#ifdef GQ_DEBUG2D
+  if (kind == K_SEG && n == 2) {
+    const double *a = PT(D, v[0]), *b = PT(D, v[1]);
+    double l = sqrt((a[0] - b[0]) * (a[0] - b[0]) + (a[1] - b[1]) * (a[1] - b[1]) + (a[2] - b[2]) * (a[2] - b[2]));
+    printf("[skipseg] round %d reason %d len %.3e r %.6f %.6f z %.4f %.4f\n", round_no, reason, l,
+           sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]), sqrt(b[0] * b[0] + b[1] * b[1] + b[2] * b[2]), a[2], b[2]);
+  }
+#endif
   int k = atomicAdd(&D.ctr->nskip, 1);
   if (k >= L.cap) { raise_err(GQ_ERR_CAP); return; }
   int* r = L.rows + 8 * (size_t)k;
@@ -113,6 +132,36 @@ __device__ __noinline__ int walk_seed(const Dev& D, const double* p, int near_ve
   return walk(D, p, hint >= 0 ? hint : -1);
 }
 
+// Splitting point of subsegment record r: the midpoint (refine.py:91-104),
+// except next to a small input angle.  Midpoint splitting of two segments
+// meeting at < 45 degrees need not terminate (each split can make the other
+// subsegment encroached again, down to rounding level: C4's torus quads have
+// 18-degree corners); Shewchuk's concentric-shell rule splits a subsegment
+// with exactly one such apex endpoint at the power of two nearest half its
+// length, measured from the apex, so that subsegments around the apex come
+// in equal lengths and stop encroaching each other.  Inputs without such an
+// apex (every parity configuration: cube, random segments, rectangles,
+// triangles with angles >= 50 degrees) split at the reference's midpoint;
+// with one, the reference's own refinement has no termination guarantee.
+__device__ __noinline__ void seg_split_point(const Dev& D, int r, double* p) {
+  int2 e = D.sg_uv[r];
+  const double *pu = PT(D, e.x), *pv = PT(D, e.y);
+  int2 o = D.sid_uv[D.sg_sid[r]];
+  bool au = (e.x == o.x || e.x == o.y) && D.vapex[e.x];
+  bool av = (e.y == o.x || e.y == o.y) && D.vapex[e.y];
+  if (au == av) {
+    for (int k = 0; k < 3; ++k) p[k] = (pu[k] + pv[k]) / 2.0;
+    return;
+  }
+  const double* a = au ? pu : pv;
+  const double* b = au ? pv : pu;
+  double d[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+  double len = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+  double h = exp2(rint(log2(0.5 * len)));        // in [len/(2 sqrt 2), len/sqrt 2]
+  double f = h / len;
+  for (int k = 0; k < 3; ++k) p[k] = a[k] + d[k] * f;
+}
+
 // fills point / priority / seed / allowed pids / claim extra for candidate c.
 // Returns false when the element is degenerate (DegenerateTet / DegenerateTri).
 __device__ __noinline__ bool make_cand(const Dev& D, const Cand& C, int c, const CandCtx& X, Scratch& S) {
@@ -130,8 +179,7 @@ __device__ __noinline__ bool make_cand(const Dev& D, const Cand& C, int c, const
   } else if (kind == K_SEG) {
     int2 e = D.sg_uv[tgt];
     canon[0] = e.x; canon[1] = e.y; nc = 2;
-    const double *pu = PT(D, e.x), *pv = PT(D, e.y);
-    for (int k = 0; k < 3; ++k) p[k] = (pu[k] + pv[k]) / 2.0;
+    seg_split_point(D, tgt, p);
     if (!edge_exists(D, e.x, e.y, S.tset, S.stack, 2 * S.cap)) C.seed[c] = walk_seed(D, p, e.x);
     if (X.with_facets) {
       int sid = D.sg_sid[tgt];

@@ -106,6 +106,7 @@ struct Dev {
   int* segpoly_off;    // sid -> polygons (CSR)
   int* segpoly;
   int2* sid_uv;        // original segment endpoints
+  uint8_t* vapex;      // input vertex where two input segments meet at < 45 degrees (n_input entries)
   int nsid, npoly;
   double too_close_sq, lmin2;
   Counters* ctr;

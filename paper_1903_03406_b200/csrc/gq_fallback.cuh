@@ -192,7 +192,8 @@ __global__ void k_fallback(Dev D, Cand C, Scr SCB, FallbackIO F, T2Items T, Skip
       if (kind == K_SEG) D.sg_fl[tgt] |= RF_BLOCK;
       else if (kind == K_FACE) D.sf_fl[tgt] |= RF_BLOCK;
     } else {
-      if (st == RS_OVERFLOW) raise_err(GQ_ERR_CAP);
+      // not star-shaped, or a cavity beyond the sequential path's arena
+      // (8192 tets): skipped like the reference's CavityNotStarShaped
       skip_cand(D, C, c, 3, F.round_no, L);
     }
   }

@@ -125,7 +125,82 @@ static void ensure_mesh_room(gq_ctx* c, long long nv_need, long long nt_need) {
 
 static int scan_total(gq_ctx* c, const int* in, int* out, int n);
 
-// subsegment records: compact when half full, grow when the live ones fill a quarter
+__global__ void k_rehash_live_segs(Dev D, int n) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    if (D.sg_fl[r] & RF_LIVE) { int2 e = D.sg_uv[r]; ht_put(D.sg_hk, D.sg_hv, D.sg_hmask, key2(e.x, e.y), r); }
+}
+__global__ void k_rehash_live_faces(Dev D, int n) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    if (D.sf_fl[r] & RF_LIVE) { int4 f = D.sf_v[r]; ht_put(D.sf_hk, D.sf_hv, D.sf_hmask, key3(f.x, f.y, f.z), r); }
+}
+__global__ void k_t2_rehash_live(Dev D, int n) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    if (!D.t2alive[t]) continue;
+    int4 q = D.t2v[t];
+    ht_put(D.he_hk, D.he_hv, D.he_hmask, keyhe(q.x, q.y, q.w), t);
+    ht_put(D.he_hk, D.he_hv, D.he_hmask, keyhe(q.y, q.z, q.w), t);
+    ht_put(D.he_hk, D.he_hv, D.he_hmask, keyhe(q.z, q.x, q.w), t);
+  }
+}
+
+// id-preserving growth (safe inside a round, after the filter): arrays are
+// copied, the hash table is rebuilt from the live entries
+static void grow_seg_records(gq_ctx* c, size_t cap) {
+  Dev& D = c->D;
+  size_t n = (size_t)c->hc.nsegrec;
+  regrow(c, D.sg_uv, n, cap); regrow(c, D.sg_sid, n, cap); regrow(c, D.sg_fl, n, cap, 0);
+  unsigned int h = pow2_at_least(2 * cap);
+  dfree(D.sg_hk); dfree(D.sg_hv);
+  D.sg_hk = dmalloc<unsigned long long>(h); D.sg_hv = dmalloc<int>(h); D.sg_hmask = h - 1;
+  CK(cudaMemsetAsync(D.sg_hk, 0xff, (size_t)h * 8, c->st));
+  if (n) LAUNCH(k_rehash_live_segs, n, D, (int)n);
+  D.sgcap = (int)cap;
+  realloc_owners(c);
+  realloc_grid_nodes(c);
+  if (g_trace) std::fprintf(stderr, "[grow] seg records cap %zu\n", cap);
+}
+static void grow_face_records(gq_ctx* c, size_t cap) {
+  Dev& D = c->D;
+  size_t n = (size_t)c->hc.nfacerec;
+  regrow(c, D.sf_v, n, cap); regrow(c, D.sf_fl, n, cap, 0);
+  unsigned int h = pow2_at_least(2 * cap);
+  dfree(D.sf_hk); dfree(D.sf_hv);
+  D.sf_hk = dmalloc<unsigned long long>(h); D.sf_hv = dmalloc<int>(h); D.sf_hmask = h - 1;
+  CK(cudaMemsetAsync(D.sf_hk, 0xff, (size_t)h * 8, c->st));
+  if (n) LAUNCH(k_rehash_live_faces, n, D, (int)n);
+  D.sfcap = (int)cap;
+  realloc_grid_nodes(c);
+  if (g_trace) std::fprintf(stderr, "[grow] face records cap %zu\n", cap);
+}
+static void grow_t2(gq_ctx* c, size_t cap) {
+  Dev& D = c->D;
+  size_t n = (size_t)c->hc.nt2;
+  regrow(c, D.t2v, n, cap); regrow(c, D.t2alive, n, cap, 0);
+  dfree(c->T.own); c->T.own = dmalloc<int>(cap);
+  CK(cudaMemsetAsync(c->T.own, 0x7f, cap * 4, c->st));
+  unsigned int h = pow2_at_least(4 * cap);
+  dfree(D.he_hk); dfree(D.he_hv);
+  D.he_hk = dmalloc<unsigned long long>(h); D.he_hv = dmalloc<int>(h); D.he_hmask = h - 1;
+  CK(cudaMemsetAsync(D.he_hk, 0xff, (size_t)h * 8, c->st));
+  if (n) LAUNCH(k_t2_rehash_live, n, D, (int)n);
+  D.t2cap = (int)cap;
+  if (g_trace) std::fprintf(stderr, "[grow] 2D triangles cap %zu\n", cap);
+}
+
+// Before the insertions of a round (counts pulled): room for what `ni`
+// inserted points (`nit` of them facet items) can create -- two subsegments
+// per split, and a generous bound on the subfaces / 2D triangles of a fan.
+static void ensure_round_room(gq_ctx* c, long long ni, long long nit) {
+  Dev& D = c->D;
+  long long sneed = c->hc.nsegrec + 2 * ni + 1024, fneed = c->hc.nfacerec + 32 * nit + 1024, tneed = c->hc.nt2 + 32 * nit + 1024;
+  if (sneed > D.sgcap) grow_seg_records(c, std::max<size_t>(2 * (size_t)sneed, 2 * (size_t)D.sgcap));
+  if (fneed > D.sfcap) grow_face_records(c, std::max<size_t>(2 * (size_t)fneed, 2 * (size_t)D.sfcap));
+  if (tneed > D.t2cap) grow_t2(c, std::max<size_t>(2 * (size_t)tneed, 2 * (size_t)D.t2cap));
+}
+
+// Start of a round: drop dead records / 2D triangles when half the capacity
+// is used (ids are renumbered: nothing outside the round keeps one), and grow
+// when the live ones still fill a quarter.
 static void maintain_seg_records(gq_ctx* c) {
   Dev& D = c->D;
   int n = c->hc.nsegrec;

@@ -111,6 +111,8 @@ struct gq_ctx {
   long long grid_calls = 0;
   int4* tvn2 = nullptr; uint8_t *sub2 = nullptr, *seg2 = nullptr, *skip2 = nullptr; double* ratio2 = nullptr;
   struct QBuf { int *a, *b, *c, *d, *e, *f, *g, *h; size_t cap; } Q{};
+  HugeArena HA{};            // global-memory block storage of the huge region tier
+  int* hlist = nullptr; size_t hlist_cap = 0;
   bool allocated = false;
 };
 
@@ -243,13 +245,20 @@ static void alloc_cands(gq_ctx* c, int cap, int bigcap) {
   C.bbsub = dmalloc<int>((size_t)bigcap * CCB); C.bbseg = dmalloc<int>((size_t)bigcap * CCB);
   C.beseg = dmalloc<int>((size_t)bigcap * CCB);
 }
+static void copy_huge(Cand& d, const Cand& s) {
+  d.htets = s.htets; d.hbf = s.hbf; d.hcr = s.hcr; d.hcrf = s.hcrf; d.hbsub = s.hbsub; d.hbseg = s.hbseg;
+  d.heseg = s.heseg; d.hskey = s.hskey; d.hsv0 = s.hsv0; d.hsv1 = s.hsv1;
+  d.nhugecap = s.nhugecap; d.ht = s.ht; d.hf = s.hf; d.hc = s.hc; d.hs = s.hs;
+}
 static void free_cands(Cand& C) {
   void* ps[] = {C.kind, C.tgt, C.seed, C.status, C.memb, C.pool, C.rank, C.allow, C.nallow, C.extra, C.p, C.h, C.canon,
                 C.state, C.vid, C.nt0, C.ntet, C.nbf, C.ncr, C.nbsub, C.nbseg, C.neseg, C.mind, C.tets, C.bf, C.cr,
                 C.crf, C.bsub, C.bseg, C.eseg, C.rseg, C.rface, C.nrseg, C.nrface, C.bigi, C.btets, C.bbf, C.bcr,
                 C.bcrf, C.bbsub, C.bbseg, C.beseg};
   for (void* p : ps) if (p) dfree(p);
+  Cand keep = C;       // the huge slabs are owned by ensure_huge / free_huge
   C = Cand{};
+  copy_huge(C, keep);
 }
 static void ensure_cands(gq_ctx* c, int n) {
   if (n <= c->C.cap) return;
@@ -262,6 +271,7 @@ static void grow_cands_keep(gq_ctx* c, int need, int n_keep) {
   if (need <= c->C.cap) return;
   Cand old = c->C;
   c->C = Cand{};
+  copy_huge(c->C, old);
   alloc_cands(c, std::max(need, 2 * old.cap), old.nbigcap);
   Cand& C = c->C;
   size_t k = (size_t)n_keep;
@@ -315,7 +325,7 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   // (the minimums cover bulk construction and the initial constraints; the
   // rounds grow everything on demand, gq_grow.cuh)
   size_t vcap = std::max<size_t>((size_t)(capx * (65536 + (size_t)n * 8)), (size_t)n + 1024);
-  size_t tcap = std::max<size_t>((size_t)(capx * std::max<size_t>(1 << 21, (size_t)n * 64)), (size_t)n * 16 + 4096);
+  size_t tcap = std::max<size_t>((size_t)(capx * std::max<size_t>(1 << 21, (size_t)n * 64)), (size_t)n * 40 + 65536);
   D.vcap = (int)vcap; D.tcap = (int)tcap;
   D.P = dmalloc<double>(3 * vcap); D.vorigin = dmalloc<uint8_t>(vcap); D.vert_tet = dmalloc<int>(vcap);
   D.vsid = dmalloc<int>(vcap);
@@ -352,6 +362,7 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   D.segpoly_off = dmalloc<int>(m + 1);
   D.segpoly = dmalloc<int>(std::max(npidx, 1));
   D.sid_uv = dmalloc<int2>(std::max(m, 1));
+  D.vapex = nullptr;   // set by refine_impl
   D.nsid = m; D.npoly = f;
   c->dctr = dmalloc<Counters>(1);
   D.ctr = c->dctr;
@@ -405,12 +416,13 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   c->allocated = true;
 }
 
+static void free_huge(gq_ctx* c);
 static void free_all(gq_ctx* c) {
   if (!c->allocated) return;
   Dev& D = c->D;
   void* ps[] = {D.P, D.vorigin, D.vert_tet, D.vsid, D.tv.p, D.alive, D.sub, D.seg, D.skip, D.ratio, D.sg_uv,
                 D.sg_sid, D.sg_fl, D.sg_hk, D.sg_hv, D.sf_v, D.sf_fl, D.sf_hk, D.sf_hv, D.t2v, D.t2alive, D.he_hk,
-                D.he_hv, D.t2count, D.poly_keep, D.poly_obl, D.t2last, D.segpoly_off, D.segpoly, D.sid_uv, D.vp_key, D.vp_val, D.vp_ep, D.vp_stack, D.vp_epoch, D.vp_lock, c->dctr, c->W.own, c->T.cand,
+                D.he_hv, D.t2count, D.poly_keep, D.poly_obl, D.t2last, D.segpoly_off, D.segpoly, D.sid_uv, D.vapex, D.vp_key, D.vp_val, D.vp_ep, D.vp_stack, D.vp_epoch, D.vp_lock, c->dctr, c->W.own, c->T.cand,
                 c->T.pid, c->T.state, c->T.cav, c->T.ncav, c->T.rem, c->T.nrem, c->T.own, c->L.rows, c->d_int,
                 c->S.tkey, c->S.tval, c->S.tep, c->S.fkey, c->S.fep, c->S.epoch, c->S.list, c->S.stack, c->S.in,
                 c->S.comp, c->SB.tkey, c->SB.tval, c->SB.tep, c->SB.fkey, c->SB.fep, c->SB.epoch, c->SB.list,
@@ -418,6 +430,7 @@ static void free_all(gq_ctx* c) {
                 c->cub_tmp, c->d_order, c->G.start, c->G.codes, c->G.cnt, c->G.nbig, c->Q.a, c->Q.b, c->Q.c,
                 c->Q.d, c->Q.e, c->Q.f, c->Q.g, c->Q.h, c->tvn2, c->sub2, c->seg2, c->skip2, c->ratio2};
   for (void* p : ps) if (p) dfree(p);
+  free_huge(c);
   free_cands(c->C);
   c->allocated = false;
   c->tmpcap = 0; c->cub_cap = 0; c->cub_tmp = nullptr;
@@ -452,6 +465,84 @@ static void resolve_events(gq_ctx* c) {
   }
   c->rpairs.clear(); c->fev.clear(); c->evused = 0;
 }
+// huge region tier: slabs (ht tets each) for n candidates and block storage
+static void free_huge(gq_ctx* c) {
+  Cand& C = c->C;
+  void* ps[] = {C.htets, C.hbf, C.hcr, C.hcrf, C.hbsub, C.hbseg, C.heseg, C.hskey, C.hsv0, C.hsv1,
+                c->HA.hkey, c->HA.hval, c->HA.cav, c->HA.f0, c->HA.f1, c->HA.in, c->HA.comp, c->HA.fkey, c->HA.fep,
+                c->HA.fepoch, c->hlist};
+  for (void* p : ps) if (p) dfree(p);
+  C.htets = C.hbf = C.hcr = C.hcrf = C.hbsub = C.hbseg = C.heseg = nullptr;
+  C.hskey = nullptr; C.hsv0 = C.hsv1 = nullptr; C.nhugecap = 0; C.ht = 0;
+  c->HA = HugeArena{};
+  c->hlist = nullptr; c->hlist_cap = 0;
+}
+static void ensure_huge(gq_ctx* c, int n, int mcap) {
+  Cand& C = c->C;
+  if (n <= C.nhugecap && mcap == C.ht) return;
+  free_huge(c);
+  int cap = std::max(n, 4);
+  C.nhugecap = cap; C.ht = mcap; C.hf = 2 * mcap + 1024; C.hc = mcap / 4 + 256;
+  C.hs = (int)pow2_at_least(4 * (size_t)C.hf);
+  size_t k = (size_t)cap;
+  C.htets = dmalloc<int>(k * C.ht); C.hbf = dmalloc<int>(k * C.hf);
+  C.hcr = dmalloc<int>(k * C.hc); C.hcrf = dmalloc<int>(k * C.hc); C.hbsub = dmalloc<int>(k * C.hc);
+  C.hbseg = dmalloc<int>(k * C.hc); C.heseg = dmalloc<int>(k * C.hc);
+  C.hskey = dmalloc<unsigned long long>(k * C.hs); C.hsv0 = dmalloc<int>(k * C.hs); C.hsv1 = dmalloc<int>(k * C.hs);
+  HugeArena& H = c->HA;
+  H.nblocks = std::min(cap, 64);
+  H.mcap = mcap; H.hcap = (int)pow2_at_least(2 * (size_t)mcap); H.fcap = (int)pow2_at_least(4 * (size_t)C.hf);
+  size_t nb = (size_t)H.nblocks;
+  H.hkey = dmalloc<int>(nb * H.hcap); H.hval = dmalloc<int>(nb * H.hcap);
+  H.cav = dmalloc<int>(nb * H.mcap); H.f0 = dmalloc<int>(nb * H.mcap); H.f1 = dmalloc<int>(nb * H.mcap);
+  H.in = dmalloc<uint8_t>(nb * H.mcap); H.comp = dmalloc<int>(nb * H.mcap);
+  H.fkey = dmalloc<unsigned long long>(nb * H.fcap); H.fep = dmalloc<unsigned int>(nb * H.fcap);
+  H.fepoch = dmalloc<unsigned int>(nb);
+  CK(cudaMemsetAsync(H.fep, 0, 4 * nb * H.fcap, c->st));
+  CK(cudaMemsetAsync(H.fepoch, 0, 4 * nb, c->st));
+  c->hlist = dmalloc<int>(k); c->hlist_cap = k;
+}
+__global__ void k_status_of(Cand C, const int* list, int n, int* out) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) out[k] = C.status[list[k]];
+}
+__global__ void k_set_status(Cand C, const int* list, int n, int from, int to) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    if (C.status[list[k]] == from) C.status[list[k]] = to;
+}
+// block-tier overflows of this round: the huge tier, capacities doubled until
+// every cavity fits (4M tets at most, beyond which the candidate fails)
+static void run_huge_regions(gq_ctx* c, const std::vector<int>& big) {
+  int nb = (int)big.size();
+  std::vector<int> st(nb);
+  CK(cudaMemcpyAsync(c->tmpC, big.data(), 4 * (size_t)nb, cudaMemcpyHostToDevice, c->st));
+  LAUNCH(k_status_of, nb, c->C, c->tmpC, nb, c->tmpA);
+  d2h(c, st.data(), c->tmpA, 4 * (size_t)nb);
+  std::vector<int> huge;
+  for (int k = 0; k < nb; ++k) if (st[k] == CS_OVF) huge.push_back(big[k]);
+  int nh = (int)huge.size();
+  if (nh == 0) return;
+  for (int mcap = std::max(c->C.ht, 16384);; mcap *= 2) {
+    ensure_huge(c, nh, mcap);
+    CK(cudaMemcpyAsync(c->hlist, huge.data(), 4 * (size_t)nh, cudaMemcpyHostToDevice, c->st));
+    region_begin(c);
+    k_region_huge<<<std::min(nh, c->HA.nblocks), BR_THREADS, 0, c->st>>>(c->D, c->C, c->SB, c->HA, c->hlist, nh);
+    c->launches++;
+    CK(cudaGetLastError());
+    region_end(c);
+    LAUNCH(k_status_of, nh, c->C, c->hlist, nh, c->tmpA);
+    std::vector<int> hs(nh);
+    d2h(c, hs.data(), c->tmpA, 4 * (size_t)nh);
+    int still = 0;
+    for (int k = 0; k < nh; ++k) still += hs[k] == CS_OVF;
+    if (g_trace) std::fprintf(stderr, "[huge] %d cavities, capacity %d tets, %d overflow\n", nh, mcap, still);
+    if (still == 0) return;
+    if (mcap >= (1 << 22)) {   // give up on these: failed candidates (the fallback skips them)
+      LAUNCH(k_set_status, nh, c->C, c->hlist, nh, CS_OVF, CS_CNSS);
+      return;
+    }
+  }
+}
+
 template <class K>
 static void launch_warp_regions(gq_ctx* c, K kern, size_t shm, int nwork, int n0, int n1, const int* list) {
   int blocks = (int)std::min<long long>(((long long)nwork + WR_WARPS - 1) / WR_WARPS, c->S.nthreads / WR_WARPS);
@@ -513,6 +604,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
     CK(cudaGetLastError());
     c->big_used += nb;
     double tb = now_s();
+    run_huge_regions(c, big);
     sync(c);
     if (g_trace) {
       std::vector<int> nts(nb);
@@ -1036,6 +1128,7 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
   LAUNCH(k_gather_nbf, ni, C, ins, ni, flags);
   int tot = scan_total(c, flags, pos, ni);
   ensure_mesh_room(c, (long long)nv + ni, (long long)nt + tot);
+  ensure_round_room(c, ni, c->npoly > 0 ? 8LL * ni : 0);
   LAUNCH(k_assign_ids, ni, C, ins, ni, pos, nv, nt);
   Ins I; I.list = ins; I.n = ni; I.nv0 = nv; I.nt0base = nt;
   fine(c, 18);
@@ -1224,6 +1317,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   if (nfail > 0) {
     pull(c);
     ensure_mesh_room(c, (long long)c->hc.nv + nfail, (long long)c->hc.nt + 1024LL * nfail + 65536);
+    ensure_round_room(c, nfail, c->npoly > 0 ? 8LL * nfail : 0);
     FallbackIO F; F.list = c->Q.h; F.n = nfail; F.round_no = round_no; F.seed = c->seed;
     F.with_facets = c->npoly > 0; F.lmin2 = lmin2; F.inserted = c->d_int + 20;
     CK(cudaMemsetAsync(c->d_int + 20, 0, 4, c->st));
@@ -1352,6 +1446,34 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
     if (!sp.empty()) CK(cudaMemcpyAsync(D.segpoly, sp.data(), 4 * sp.size(), cudaMemcpyHostToDevice, c->st));
   }
   CK(cudaMemcpyAsync(D.segpoly_off, spo.data(), 4 * (size_t)(m + 1), cudaMemcpyHostToDevice, c->st));
+  // small-angle apexes: input vertices where two input segments meet at < 45
+  // degrees get concentric-shell splitting (seg_split_point, gq_cand.cuh)
+  {
+    std::vector<uint8_t> apex(std::max(n, 1), 0);
+    std::vector<int> deg(n + 1, 0), adj(2 * (size_t)m);
+    for (int s = 0; s < m; ++s) { deg[seg[2 * s] + 1]++; deg[seg[2 * s + 1] + 1]++; }
+    for (int v = 0; v < n; ++v) deg[v + 1] += deg[v];
+    std::vector<int> fill(deg.begin(), deg.end() - 1);
+    for (int s = 0; s < m; ++s) { adj[fill[seg[2 * s]]++] = seg[2 * s + 1]; adj[fill[seg[2 * s + 1]]++] = seg[2 * s]; }
+    const double c45 = std::sqrt(0.5);
+    for (int v = 0; v < n; ++v) {
+      for (int i = deg[v]; i < deg[v + 1] && !apex[v]; ++i) {
+        const double* a = xyz + 3 * (size_t)v;
+        const double* x = xyz + 3 * (size_t)adj[i];
+        double u0[3] = {x[0] - a[0], x[1] - a[1], x[2] - a[2]};
+        double lu = std::sqrt(u0[0] * u0[0] + u0[1] * u0[1] + u0[2] * u0[2]);
+        for (int j = i + 1; j < deg[v + 1]; ++j) {
+          const double* y = xyz + 3 * (size_t)adj[j];
+          double w0[3] = {y[0] - a[0], y[1] - a[1], y[2] - a[2]};
+          double lw = std::sqrt(w0[0] * w0[0] + w0[1] * w0[1] + w0[2] * w0[2]);
+          if (u0[0] * w0[0] + u0[1] * w0[1] + u0[2] * w0[2] > c45 * lu * lw) { apex[v] = 1; break; }
+        }
+      }
+    }
+    D.vapex = dmalloc<uint8_t>(std::max(n, 1));
+    CK(cudaMemcpyAsync(D.vapex, apex.data(), std::max(n, 1), cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
   // init_delaunay
   init_delaunay(c, order, n);
   CK(cudaEventRecord(c->ev1, c->st));

@@ -280,6 +280,12 @@ __device__ inline StarHash big_star_hash(const Scr& SB, int gw, int* flag) {
   h.flag = flag;
   return h;
 }
+__device__ inline StarHash huge_star_hash(const Cand& C, int c, int* flag) {
+  size_t h = (size_t)(C.bigi[c] - HUGE_BASE) * C.hs;
+  StarHash X;
+  X.key = C.hskey + h; X.v0 = C.hsv0 + h; X.v1 = C.hsv1 + h; X.cap = C.hs; X.flag = flag;
+  return X;
+}
 __global__ void __launch_bounds__(32 * WS_WARPS) k_star_warp(Dev D, Cand C, Ins I, Scr SB) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -290,6 +296,7 @@ __global__ void __launch_bounds__(32 * WS_WARPS) k_star_warp(Dev D, Cand C, Ins 
     SlabView v = slab(C, c);
     int nbf = C.nbf[c];
     if (nbf <= WS_MAXF) star_warp(D, C.vid[c], v.bf, nbf, C.nt0[c], true, star_hash_shared(X), nullptr, 0);
+    else if (C.bigi[c] >= HUGE_BASE) star_warp(D, C.vid[c], v.bf, nbf, C.nt0[c], true, huge_star_hash(C, c, &X.flag), nullptr, 0);
     else star_warp(D, C.vid[c], v.bf, nbf, C.nt0[c], true, big_star_hash(SB, gw, &X.flag), nullptr, 0);
     if (lane == 0) { atomicAdd(&D.ctr->created, (unsigned long long)nbf); atomicAdd(&D.ctr->deleted, (unsigned long long)C.ntet[c]); }
     __syncwarp();

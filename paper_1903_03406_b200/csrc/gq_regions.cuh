@@ -222,14 +222,8 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_init_region_warp(Dev D,
 
 // oversized cavities: one block per candidate (threads in proportion to
 // region size); big slabs base+w
-__global__ void __launch_bounds__(BR_THREADS) k_region_block(Dev D, Cand C, Scr SB, const int* list, int nb, int base) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  BlockShared& B = *reinterpret_cast<BlockShared*>(smem_raw);
-  Scratch S = scratch_for(SB, blockIdx.x);
-  for (int w = blockIdx.x; w < nb; w += gridDim.x) {
-    int c = list[w];
-    if (threadIdx.x == 0) C.bigi[c] = base + w;
-    __syncthreads();
+// one block per candidate on a BlockView; the caller has set C.bigi[c]
+__device__ inline void block_region_cand(const Dev& D, const Cand& C, int c, BlockView& B, Scratch& S) {
     SlabView v = slab(C, c);
     __shared__ int s_seeds[32];
     __shared__ int s_ns;
@@ -243,17 +237,55 @@ __global__ void __launch_bounds__(BR_THREADS) k_region_block(Dev D, Cand C, Scr 
       if (st == RS_OK) {
         atomicAdd(&D.ctr->tested, (unsigned long long)(O.ntet + O.nbf));
         C.status[c] = (O.mind <= D.too_close_sq) ? CS_TOOCLOSE : CS_OK;
-      } else if (st == RS_OVERFLOW) { C.status[c] = CS_CNSS; raise_err(GQ_ERR_CAP); }
+      } else if (st == RS_OVERFLOW) C.status[c] = CS_OVF;       // -> the huge tier
       else if (st == RS_MEMBRANE) { C.status[c] = CS_MEMB; C.memb[c] = O.memb; }
       else C.status[c] = CS_CNSS;
     }
     __syncthreads();
+}
+__global__ void __launch_bounds__(BR_THREADS) k_region_block(Dev D, Cand C, Scr SB, const int* list, int nb, int base) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ BlockView B;
+  if (threadIdx.x == 0) view_of_shared(B, *reinterpret_cast<BlockShared*>(smem_raw));
+  Scratch S = scratch_for(SB, blockIdx.x);
+  for (int w = blockIdx.x; w < nb; w += gridDim.x) {
+    int c = list[w];
+    if (threadIdx.x == 0) C.bigi[c] = base + w;
+    __syncthreads();
+    block_region_cand(D, C, c, B, S);
+  }
+}
+// Cavities beyond the block tier's 4096 tets (far circumcentres of slivers, a
+// box corner's fan): the same block algorithm on global-memory arrays sized
+// by the host, which doubles them and reruns whatever still overflows.
+struct HugeArena {
+  int* hkey; int* hval; int* cav; int* f0; int* f1; uint8_t* in; int* comp;   // per block: hcap / mcap entries
+  unsigned long long* fkey; unsigned int* fep; unsigned int* fepoch;         // per block constraint-pass set (fcap)
+  int hcap, mcap, fcap, nblocks;
+};
+__global__ void __launch_bounds__(BR_THREADS) k_region_huge(Dev D, Cand C, Scr SB, HugeArena H, const int* list, int nb) {
+  __shared__ BlockView B;
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    size_t oh = (size_t)b * H.hcap, om = (size_t)b * H.mcap;
+    B.hkey = H.hkey + oh; B.hval = H.hval + oh; B.cav = H.cav + om; B.f0 = H.f0 + om; B.f1 = H.f1 + om;
+    B.in = H.in + om; B.comp = H.comp + om; B.hcap = H.hcap; B.mcap = H.mcap;
+  }
+  Scratch S = scratch_for(SB, b);
+  S.fset.key = H.fkey + (size_t)b * H.fcap; S.fset.ep = H.fep + (size_t)b * H.fcap; S.fset.cur = H.fepoch + b;
+  S.fset.cap = H.fcap;
+  for (int w = b; w < nb; w += gridDim.x) {
+    int c = list[w];
+    if (threadIdx.x == 0) C.bigi[c] = HUGE_BASE + w;
+    __syncthreads();
+    block_region_cand(D, C, c, B, S);
   }
 }
 __global__ void __launch_bounds__(BR_THREADS) k_init_region_block(Dev D, Cand C, Scr SB, const int* pend, const int* list, int nb,
                                                                   int* hint, const int* succ, int round) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  BlockShared& B = *reinterpret_cast<BlockShared*>(smem_raw);
+  __shared__ BlockView B;
+  if (threadIdx.x == 0) view_of_shared(B, *reinterpret_cast<BlockShared*>(smem_raw));
   Scratch S = scratch_for(SB, blockIdx.x);
   for (int w = blockIdx.x; w < nb; w += gridDim.x) {
     int c = list[w];
