@@ -97,6 +97,17 @@ int gq_write_mesh(const char* node_path, const char* ele_path, const char* face_
                   const uint8_t* origins, int32_t nv, const int32_t* tv, const uint8_t* alive, int32_t nt,
                   const int32_t* faces, int32_t nf);
 
+/* Device certification of PLC validity, the feature-pair part of
+ * tetrefine.plc.validate (plc.py:355-383): candidate pairs from a grid over
+ * the segment / triangle boxes, each decided with exact predicates.
+ *   tri[f][3]   triangular polygons (features numbered segments first)
+ *   status      0 no certain conflict (pairs lists the undecided ones for the
+ *               caller's exact pair test), 1 a certain conflict, 2 more than
+ *               pair_cap undecided pairs, 3 device arithmetic failure
+ * Replaces the pair loop of validate() (and setup_fast.certify_valid). */
+int gq_certify_pairs(int device, const double* xyz, int32_t n, const int32_t* seg, int32_t m, const int32_t* tri,
+                     int32_t f, int32_t* status, int32_t* pairs, int64_t pair_cap, int64_t* n_pairs);
+
 /* batched exact predicates / constructions on the device, for parity tests:
  * which 0 orient3d(12) 1 insphere(15) 2 orient2d(6) 3 incircle2d(8)
  * 4 incircle3d(12) 5 encroaches_segment(9) 6 encroaches_face(12) -> out8;

@@ -35,7 +35,7 @@ class GqCounts(ctypes.Structure):
 
 
 EXPORTS = ("gq_create", "gq_destroy", "gq_last_error", "gq_refine", "gq_export_mesh", "gq_export_constraints",
-           "gq_export_rounds", "gq_export_skipped", "gq_quality", "gq_batch", "gq_write_mesh")
+           "gq_export_rounds", "gq_export_skipped", "gq_quality", "gq_batch", "gq_write_mesh", "gq_certify_pairs")
 
 
 def lib_path() -> str:
@@ -63,6 +63,7 @@ def lib():
         L.gq_quality.argtypes = [vp, ctypes.c_double, vp, vp]
         L.gq_batch.argtypes = [ctypes.c_int, vp, i32, i32, vp, vp]
         L.gq_write_mesh.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, vp, vp, i32, vp, vp, i32, vp, i32]
+        L.gq_certify_pairs.argtypes = [ctypes.c_int, vp, i32, vp, i32, vp, i32, vp, vp, ctypes.c_int64, vp]
         for name in EXPORTS:
             if name not in ("gq_last_error",):
                 getattr(L, name).restype = ctypes.c_int
@@ -167,3 +168,20 @@ def batch(name: str, arr: np.ndarray) -> np.ndarray:
     if st != 0:
         raise NativeError(st, "gq_batch failed")
     return out
+
+
+def certify_pairs(points: np.ndarray, segments: np.ndarray, triangles: np.ndarray, device: int = 0,
+                  cap: int = 1 << 20):
+    """Feature-pair certification of a PLC on the device (include/gqm3d.h
+    gq_certify_pairs).  Returns (status, undecided pairs (k, 2))."""
+    P = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    S = np.ascontiguousarray(segments, dtype=np.int32).reshape(-1, 2)
+    T = np.ascontiguousarray(triangles, dtype=np.int32).reshape(-1, 3)
+    st = np.zeros(1, np.int32)
+    npairs = np.zeros(1, np.int64)
+    pairs = np.zeros((cap, 2), np.int32)
+    rc = lib().gq_certify_pairs(int(device), _p(P), len(P), _p(S), len(S), _p(T), len(T), _p(st), _p(pairs),
+                                int(cap), _p(npairs))
+    if rc != 0:
+        raise NativeError(rc, "gq_certify_pairs failed")
+    return int(st[0]), pairs[:int(npairs[0])]

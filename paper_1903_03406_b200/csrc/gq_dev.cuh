@@ -741,7 +741,8 @@ __device__ __noinline__ int region_compute(const Dev& D, const double* p, const 
       }
     }
   }
-  if (bf_has_ghost_part(D, O.bf, O.nbf, 0, 1) && bf_open_part(D, O.bf, O.nbf, 0, 1)) return RS_BADSTAR;
+  // (sequential path: every cavity is checked, see k_star_check for why the peel is not enough)
+  if (bf_open_part(D, O.bf, O.nbf, 0, 1)) return RS_BADSTAR;
   double mind = __longlong_as_double(0x7ff0000000000000ll);
   for (int a = 0; a < O.nbf; ++a) {
     int t = O.bf[a] >> 2, i = O.bf[a] & 3;

@@ -352,3 +352,99 @@ __global__ void k_batch(int which, const double* in, int n, signed char* out8, d
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Star validation of the accepted set, before anything is written.  The peel
+// leaves every boundary face strictly visible from p, but a cavity whose
+// boundary pinches along an edge (two wedges of tets meeting at it, one of
+// them reflex) passes that test and cannot be starred; neither can a ghost
+// cavity of a point rounded just outside a curved hull.  The reference meets
+// such cavities only while starring (star_kernel's unmatched-face status,
+// _kernels.py:696,720 -> CavityNotStarShaped, mesh.py:769-770): inside
+// _fallback it skips the element (refine.py:785-799), on the main path the
+// exception ends the refine.  Here an accepted candidate whose boundary faces
+// do not pair up is skipped with reason cavity_not_star_shaped and nothing is
+// inserted for it.  Same pairing as star_warp (gq_warp.cuh), no writes.
+__device__ inline bool star_pairs_ok(const Dev& D, const int* bf, int nbf, const StarHash& X) {
+  const int lane = threadIdx.x & 31;
+  const int vid = -2;                       // the new vertex (no id yet); not GHOST, not a vertex id
+  for (int i = lane; i < X.cap; i += 32) { X.key[i] = EMPTY_KEY; X.v0[i] = -1; X.v1[i] = -1; }
+  if (lane == 0) *X.flag = 0;
+  __syncwarp();
+  for (int k = lane; k < nbf; k += 32) {
+    int t = bf[k] >> 2, i = bf[k] & 3;
+    int packed = tnk(D, t, i);
+    int u = packed >> 2, j = packed & 3;
+    int f[3]; face_verts(D.tv[u], j, f);
+    int4 q;
+    if (f[0] == GHOST || f[1] == GHOST || f[2] == GHOST) {
+      int e0, e1;
+      if (f[0] == GHOST) { e0 = f[1]; e1 = f[2]; }
+      else if (f[1] == GHOST) { e0 = f[2]; e1 = f[0]; }
+      else { e0 = f[0]; e1 = f[1]; }
+      q = make_int4(e1, e0, vid, GHOST);
+    } else {
+      q = make_int4(f[0], f[1], f[2], vid);
+    }
+    int a0 = f[0], b0 = f[1], c0 = f[2];
+    sort3(a0, b0, c0);
+    int om = -1;
+    for (int m = 0; m < 4; ++m) {
+      int g[3]; face_verts(q, m, g);
+      int x = g[0], y = g[1], z = g[2];
+      sort3(x, y, z);
+      if (om < 0 && x == a0 && y == b0 && z == c0) { om = m; continue; }
+      int h = star_slot(X, inner_key(g, vid), true);
+      if (h < 0) { *X.flag = 1; continue; }
+      int mine = 4 * k + m;
+      if (atomicCAS(&X.v0[h], -1, mine) != -1 && atomicCAS(&X.v1[h], -1, mine) != -1) *X.flag = 1;
+    }
+    if (om < 0) *X.flag = 1;
+  }
+  __syncwarp();
+  for (int k = lane; k < nbf && !*X.flag; k += 32) {
+    int t = bf[k] >> 2, i = bf[k] & 3;
+    int packed = tnk(D, t, i);
+    int f[3]; face_verts(D.tv[packed >> 2], packed & 3, f);
+    int4 q = (f[0] == GHOST || f[1] == GHOST || f[2] == GHOST) ? make_int4(0, 0, 0, GHOST) : make_int4(f[0], f[1], f[2], vid);
+    if (q.w == GHOST) {
+      int e0, e1;
+      if (f[0] == GHOST) { e0 = f[1]; e1 = f[2]; }
+      else if (f[1] == GHOST) { e0 = f[2]; e1 = f[0]; }
+      else { e0 = f[0]; e1 = f[1]; }
+      q = make_int4(e1, e0, vid, GHOST);
+    }
+    for (int m = 0; m < 4; ++m) {
+      int g[3]; face_verts(q, m, g);
+      if (g[0] != vid && g[1] != vid && g[2] != vid) continue;
+      int h = star_slot(X, inner_key(g, vid), false);
+      int mine = 4 * k + m;
+      int other = h < 0 ? -1 : (X.v0[h] == mine ? X.v1[h] : X.v0[h]);
+      if (other < 0) *X.flag = 1;
+    }
+  }
+  __syncwarp();
+  return *X.flag == 0;
+}
+__global__ void __launch_bounds__(32 * WS_WARPS) k_star_check(Dev D, Cand C, const int* acc, int nacc, int* insflag,
+                                                            Scr SB, SkipLog L, int round_no) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  StarShared& X = reinterpret_cast<StarShared*>(smem_raw)[wib];
+  const int gw = blockIdx.x * WS_WARPS + wib, nw = gridDim.x * WS_WARPS;
+  for (int k = gw; k < nacc; k += nw) {
+    if (!insflag[k]) continue;
+    int c = acc[k];
+    SlabView v = slab(C, c);
+    int nbf = C.nbf[c];
+    bool ok;
+    if (nbf <= WS_MAXF) ok = star_pairs_ok(D, v.bf, nbf, star_hash_shared(X));
+    else if (C.bigi[c] >= HUGE_BASE) ok = star_pairs_ok(D, v.bf, nbf, huge_star_hash(C, c, &X.flag));
+    else ok = star_pairs_ok(D, v.bf, nbf, big_star_hash(SB, gw, &X.flag));
+    if (!ok && lane == 0) {
+      insflag[k] = 0;
+      skip_cand(D, C, c, 3, round_no, L);
+    }
+    __syncwarp();
+  }
+}

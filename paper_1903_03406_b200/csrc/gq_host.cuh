@@ -1119,6 +1119,12 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
   if (na == 0) return;
   LAUNCH(k_gather_i32, na, byrank, pos, na, acc);
   LAUNCH(k_accept_flags, na, c->D, C, acc, na, flags, c->L, round_no, c->D.lmin2);
+  {
+    int blocks = std::max(1, std::min((na + WS_WARPS - 1) / WS_WARPS, c->SB.nthreads / WS_WARPS));
+    k_star_check<<<blocks, 32 * WS_WARPS, WS_WARPS * sizeof(StarShared), c->st>>>(c->D, C, acc, na, flags, c->SB, c->L, round_no);
+    c->launches++;
+    CK(cudaGetLastError());
+  }
   int ni = select_flagged(c, flags, na, pos);
   *inserted += ni;
   if (ni == 0) return;

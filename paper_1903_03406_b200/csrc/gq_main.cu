@@ -50,6 +50,7 @@ using namespace gq;
 #include "gq_check.cuh"
 #include "gq_init.cuh"
 #include "gq_fallback.cuh"
+#include "gq_setup.cuh"
 #include "gq_host.cuh"
 
 // ===========================================================================
@@ -72,6 +73,7 @@ int gq_create(int device, gq_ctx** out) {
     if (WT1_MAXT != WT2_MAXT)
       CK(cudaFuncSetAttribute(k_region_warp<WT2_MAXT, WT2_HASH, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared2))));
     CK(cudaFuncSetAttribute(k_star_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WS_WARPS * sizeof(StarShared))));
+    CK(cudaFuncSetAttribute(k_star_check, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WS_WARPS * sizeof(StarShared))));
     CK(cudaFuncSetAttribute(k_init_stars_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WS_WARPS * sizeof(StarShared))));
     CK(cudaFuncSetAttribute(k_init_region_warp<WT1_MAXT, WT1_HASH, WT1_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared1))));
     if (WT1_MAXT != WT2_MAXT)
@@ -219,6 +221,77 @@ int gq_quality(gq_ctx* c, double B, int64_t* bad_count, int64_t* hist36) {
     if (bad_count) *bad_count = (int64_t)h[0];
     if (hist36) for (int k = 0; k < 36; ++k) hist36[k] = (int64_t)h[1 + k];
   } catch (std::exception& e) { c->err = e.what(); return GQ_ECUDA; }
+  return GQ_OK;
+}
+
+int gq_certify_pairs(int device, const double* xyz, int32_t n, const int32_t* seg, int32_t m, const int32_t* tri, int32_t f,
+                     int32_t* status, int32_t* pairs, int64_t pair_cap, int64_t* n_pairs) {
+  if (!xyz || n < 1 || !status || !n_pairs || m < 0 || f < 0) return GQ_EINVAL;
+  try {
+    CK(cudaSetDevice(device));
+    *status = 0; *n_pairs = 0;
+    int nf = m + f;
+    if (nf < 2) return GQ_OK;
+    double* dP = dmalloc<double>(3 * (size_t)n);
+    int* dseg = dmalloc<int>(2 * (size_t)std::max(m, 1));
+    int* dtri = dmalloc<int>(3 * (size_t)std::max(f, 1));
+    CK(cudaMemcpy(dP, xyz, 24 * (size_t)n, cudaMemcpyHostToDevice));
+    if (m) CK(cudaMemcpy(dseg, seg, 8 * (size_t)m, cudaMemcpyHostToDevice));
+    if (f) CK(cudaMemcpy(dtri, tri, 12 * (size_t)f, cudaMemcpyHostToDevice));
+    CertIn I;
+    I.P = dP; I.seg = dseg; I.tri = dtri; I.m = m; I.f = f;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int i = 0; i < n; ++i) for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], xyz[3 * i + k]); hi[k] = std::max(hi[k], xyz[3 * i + k]); }
+    // cell = max(2 x median feature extent, span / 256), then coarsened to <= 2^24 cells
+    double* dext = dmalloc<double>(nf);
+    k_cert_extent<<<grid_for(nf, 256, 4096), 256>>>(I, dext);
+    std::vector<double> ext(nf);
+    CK(cudaMemcpy(ext.data(), dext, 8 * (size_t)nf, cudaMemcpyDeviceToHost));
+    std::nth_element(ext.begin(), ext.begin() + nf / 2, ext.end());
+    double span = std::max(std::max(hi[0] - lo[0], hi[1] - lo[1]), std::max(hi[2] - lo[2], 1e-300));
+    double cell = std::max(2.0 * ext[nf / 2], span / 256.0);
+    for (;;) {
+      long long tot = 1;
+      for (int k = 0; k < 3; ++k) { I.G[k] = (int)std::ceil((hi[k] - lo[k]) / cell) + 1; tot *= I.G[k]; }
+      if (tot <= (1LL << 24)) break;
+      cell *= 1.5;
+    }
+    for (int k = 0; k < 3; ++k) I.lo[k] = lo[k];
+    I.inv = 1.0 / cell;
+    int ncell = I.G[0] * I.G[1] * I.G[2];
+    int* cnt = dmalloc<int>(ncell + 1); int* start = dmalloc<int>(ncell + 1); int* fillp = dmalloc<int>(ncell + 1);
+    int* big = dmalloc<int>(nf); int* scal = dmalloc<int>(4);
+    CK(cudaMemset(cnt, 0, 4 * (size_t)(ncell + 1)));
+    CK(cudaMemset(fillp, 0, 4 * (size_t)(ncell + 1)));
+    CK(cudaMemset(scal, 0, 16));
+    k_cert_bin<<<grid_for(nf, 256, 4096), 256>>>(I, cnt, start, fillp, nullptr, big, scal, 0);
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, start, ncell + 1);
+    void* tmp = dmalloc<char>(need);
+    cub::DeviceScan::ExclusiveSum(tmp, need, cnt, start, ncell + 1);
+    int h[2];
+    CK(cudaMemcpy(h, start + ncell, 4, cudaMemcpyDeviceToHost));
+    int* lists = dmalloc<int>(std::max(h[0], 1));
+    k_cert_bin<<<grid_for(nf, 256, 4096), 256>>>(I, cnt, start, fillp, lists, big, scal, 1);
+    CK(cudaMemcpy(h, scal, 4, cudaMemcpyDeviceToHost));
+    int nbig = h[0];
+    int cap = (int)std::min<int64_t>(pair_cap, 1 << 24);
+    int* dpairs = dmalloc<int>(2 * (size_t)std::max(cap, 1));
+    CertOut O; O.flag = scal + 1; O.npairs = scal + 2; O.pairs = dpairs; O.cap = cap;
+    k_cert_pairs<<<grid_for(nf, 128, 148 * 32), 128>>>(I, start, lists, O);
+    if (nbig) k_cert_big<<<grid_for((long long)nbig * nf, 128, 148 * 32), 128>>>(I, big, nbig, O);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    unsigned int e = 0;
+    CK(cudaMemcpyFromSymbol(&e, g_err, 4));
+    CK(cudaMemcpy(h, scal + 1, 8, cudaMemcpyDeviceToHost));
+    int np = std::min(h[1], cap);
+    if (np && pairs) CK(cudaMemcpy(pairs, dpairs, 8 * (size_t)np, cudaMemcpyDeviceToHost));
+    *status = e ? 3 : (h[0] & 1 ? 1 : (h[0] & 2 ? 2 : 0));
+    *n_pairs = np;
+    for (void* p : {(void*)dP, (void*)dseg, (void*)dtri, (void*)dext, (void*)cnt, (void*)start, (void*)fillp, (void*)big,
+                    (void*)scal, tmp, (void*)lists, (void*)dpairs}) dfree(p);
+  } catch (std::exception&) { return GQ_ECUDA; }
   return GQ_OK;
 }
 

@@ -23,6 +23,8 @@ exact path"); they never report a violation themselves.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 _EPS = 2.0 ** -53
@@ -131,6 +133,19 @@ def overlapping_pairs(lo: np.ndarray, hi: np.ndarray, max_span: int = 3):
 # ---------------------------------------------------------------------------
 # validate (plc.py:267-383)
 
+def _native_pairs(P, S, tri):
+    """(status, undecided pairs) from the device certifier, or None without a
+    usable GPU / library (then the numpy path decides)."""
+    if os.environ.get("GQM3D_HOST_SETUP") == "1":
+        return None
+    try:
+        from . import _native
+        from .refine import default_device
+        return _native.certify_pairs(P, S, tri, device=default_device())
+    except Exception:
+        return None
+
+
 def certify_valid(plc, exact_pair) -> bool | None:
     """True when the PLC has no violation; None when the exact path must
     decide.  ``exact_pair(u, v)`` runs the exact pair test of plc.validate
@@ -181,7 +196,17 @@ def certify_valid(plc, exact_pair) -> bool | None:
             pos = np.minimum(pos, max(len(ek_sorted) - 1, 0))
             if len(ek_sorted) == 0 or np.any(ek_sorted[pos] != key):
                 return None
-    # feature pairs with overlapping boxes
+    # feature pairs with overlapping boxes: on the device when there is one
+    # (exact predicates, gq_certify_pairs), else the vectorised filter below
+    native = _native_pairs(P, S, tri)
+    if native is not None:
+        status, undecided = native
+        if status != 0:
+            return None
+        for x, y in undecided.tolist():
+            if exact_pair(int(x), int(y)):
+                return None
+        return True
     nseg = len(S)
     lo = np.concatenate([np.minimum(P[S[:, 0]], P[S[:, 1]]), P[tri].min(axis=1)]) if len(tri) else \
         np.minimum(P[S[:, 0]], P[S[:, 1]])

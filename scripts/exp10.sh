@@ -1,0 +1,4 @@
+mkdir -p gpurun_out/exp10
+GQM3D_OBLIQUE_BOX=0 GQM3D_LIB=paper_1903_03406_b200/libgqm3d_dbg.so GQ_PROFILE=1 timeout 1500 python scripts/run_cfg.py C4 --verbose --audit > gpurun_out/exp10/c4_full_nobox.log 2>&1; echo "exit $?" >> gpurun_out/exp10/c4_full_nobox.log
+timeout 400 python -m pytest tests -m gpu -x -q > gpurun_out/exp10/pytest.log 2>&1; echo "exit $?" >> gpurun_out/exp10/pytest.log
+timeout 300 python scripts/time_prepare.py C4 > gpurun_out/exp10/prepare.log 2>&1
