@@ -1,22 +1,31 @@
 """Benchmark: Steiner points inserted per second for gQM3D refinement.
 
-Workload (BASELINE.json configs[1]): 100k uniform points
-+ 1k random segments in the unit cube, B=1.6, seed 0, one refine() per step.
-
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gqm3d|reference]
+                    [--config C4|C2|C5|C1|C3] [--scale S]
 
-* value     Steiner/s with the PLC already prepared and the mesh built on the
-            device (sum of GPU event time of gq_refine over the K steps)
+Workload (default C4, the north-star target of BASELINE.json): outer icosphere
+r=1 + inner icosphere r=0.45 (level 6, 81,920 triangles each) + torus R=0.72
+r=0.12 (40,000 triangles) + 1,000,000 uniform points in the unit ball, B=1.5
+(SURVEY.md 8(d)).  One step = one complete refine of that PLC.  C2 (BASELINE
+configs[1], the largest configuration the reference itself can refine) and the
+others are selectable with --config.
+
+* value     Steiner/s with the PLC prepared and uploaded: GPU time of gq_refine
+            (CUDA events on the context's stream, bulk Delaunay construction
+            + every round + final verification), summed over the K steps
 * e2e       Steiner/s through the public API refine(plc, cfg): host setup
-            (validation, box closure, insertion order), H2D, all rounds,
-            D2H export of the mesh and the quality report
-* roofline  the Delaunay-region kernel (k_region), algorithmic bytes
-            (58 B per tet tested + 24 B per candidate point)
-            over its CUDA-event time, against the measured HBM copy peak
-* cpu_baseline  the C++ oracle (sequential restatement of the reference) on a
-            bounded sample on this host, one core
-Multi-GPU: refinement does not shard (BASELINE north_star) -> N independent
-replicas, one per rank, no collectives; value = all ranks' Steiner / max time.
+            (validation incl. the device pair certifier, box closure, facet
+            axes, insertion order), H2D, all rounds, D2H export of the mesh and
+            the device quality report; wall clock per refine
+* roofline  the Delaunay-region kernels (warp / block / huge tiers, SURVEY
+            8(d): 58 B per tet tested + 24 B per candidate point) over their
+            CUDA-event time, against the measured HBM copy peak; plus the
+            whole-refine 8(d) byte formula over the whole device time
+* cpu_baseline  the C++ oracle (sequential restatement of the reference, test
+            infrastructure) on a bounded sample on this host, one core
+Multi-GPU: refinement does not shard (BASELINE north_star): each rank refines
+its own replica (C5: its share of the 64-PLC batch); no collectives on the
+data path; value = all ranks' Steiner / max-over-ranks time.
 """
 
 from __future__ import annotations
@@ -24,6 +33,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -33,7 +43,14 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-B_C2 = 1.6
+CONFIGS = {
+    "C1": (2.0, "unit cube + 1,000 uniform points (BASELINE configs[0])"),
+    "C2": (1.6, "100,000 uniform points + 1,000 random segments in the unit cube (BASELINE configs[1])"),
+    "C3": (1.4, "250,000 points + 2,000 axis-plane triangles on a 2^-16 grid (BASELINE configs[2], parity variant)"),
+    "C4": (1.5, "nested icospheres (2 x 81,920 triangles) + torus (40,000 triangles) + 1,000,000 points in the "
+                "unit ball (BASELINE configs[3], north-star target)"),
+    "C5": (1.5, "batch of 64 unit cubes + 50,000 uniform points, seeds 0..63 (BASELINE configs[4])"),
+}
 
 
 def _peaks():
@@ -42,6 +59,17 @@ def _peaks():
             return json.load(f)
     except Exception:
         return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -88,45 +116,100 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def workload(scale: float = 1.0, seed: int = 0):
+def workload(config: str, scale: float = 1.0, rank: int = 0, world: int = 1):
+    """The PLCs this rank refines in one step."""
     from paper_1903_03406_b200 import synth
-    return synth.config_plc("C2", scale=scale, seed=seed)
+    if config == "C5":
+        n = max(1, int(64 * scale)) if scale < 1 else 64
+        return [synth.cube_points(50000, seed) for seed in range(rank, n, world)]
+    return [synth.config_plc(config, scale=scale)]
 
 
-def cpu_baseline(sample_scale: float = 0.1):
-    """The oracle (C++ port of the reference) on a bounded C2 sample, 1 core."""
+def cpu_sample(config: str, budget_s: float):
+    """The oracle (C++ port of the reference, test infrastructure -- the only
+    bench use of oracle/) on a bounded sample of the workload: the largest
+    scale of the config whose refine fits the time budget, one core."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle  # test-infrastructure checker; the only bench use of oracle/
-    plc = workload(sample_scale)
+    import oracle
+    from paper_1903_03406_b200 import synth
+    B = CONFIGS[config][0]
+    base = "C1" if config == "C5" else config
+    scale = {"C1": 1.0, "C2": 0.1, "C3": 0.02, "C4": 0.0, "C5": 0.05}[config]
+    if config == "C4":
+        return None
+    plc = synth.config_plc(base, scale=scale) if config != "C5" else synth.cube_points(int(50000 * scale), 0)
     t = time.perf_counter()
-    out = oracle.refine(plc, B=B_C2)
+    out = oracle.refine(plc, B=B)
     dt = time.perf_counter() - t
     st = int((out["vert_origin"] == 1).sum())
     return {"value": st / dt, "unit": "steiner_points/s", "cores": 1, "kind": "port",
-            "sample": f"C2 scaled x{sample_scale} ({len(plc.points)} points, {len(plc.segments)} segments), "
-                      f"full refine, {st} Steiner in {dt:.2f}s"}
+            "cpu": _cpu_model(), "cpus_on_host": os.cpu_count(),
+            "sample": f"{config} scaled x{scale} ({len(plc.points)} points, {len(plc.segments)} segments, "
+                      f"{len(plc.polygons)} polygons), full refine, {st} Steiner in {dt:.2f}s"}
+
+
+def _oracle_run(config, scale, max_rounds, q):
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle
+        from paper_1903_03406_b200.prepare import prepare
+        plcs = workload(config, scale)
+        B = CONFIGS[config][0]
+        st, tt, nr = 0, 0.0, 0
+        for plc in plcs:
+            prep = prepare(plc)
+            t = time.perf_counter()
+            out = oracle.refine_prepared(prep, B=B, max_rounds=max_rounds)
+            tt += time.perf_counter() - t
+            st += int((out["vert_origin"] == 1).sum())
+            nr = max(nr, len(out.get("rounds", [])))
+        q.put(("ok", st, tt, nr))
+    except Exception as e:   # the reference's own behaviour on oblique facets (SURVEY F1)
+        q.put(("crashed", f"{type(e).__name__}: {str(e)[:200]}", 0.0, 0))
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path (the C++ oracle port: the
+    Python reference cannot travel to the GPU box) on the same config, one
+    core per refine.  Each step is one full refine of the config's PLC (C5:
+    the whole 64-PLC batch in a pool of host processes), under a wall cap;
+    a configuration the port cannot finish is reported with its status."""
     if rank != 0:
         return
-    times, steiner = [], []
-    for i in range(args.warmup + args.steps):
-        res = cpu_baseline(args.ref_scale)
-        if i >= args.warmup:
-            st = int(res["sample"].split(", full refine, ")[1].split(" ")[0])
-            times.append(st / res["value"])
-            steiner.append(st)
-    tot = sum(times)
-    value = sum(steiner) / tot
+    import multiprocessing as mp
+    B = CONFIGS[args.config][0]
+    steps = max(1, min(args.steps, args.ref_steps))
+    warm = 0
+    times, steiner, status, rounds = [], [], "ok", 0
+    for i in range(warm + steps):
+        q = mp.get_context("fork").Queue()
+        p = mp.get_context("fork").Process(target=_oracle_run, args=(args.config, args.scale, args.max_rounds, q))
+        t0 = time.perf_counter()
+        p.start()
+        p.join(args.ref_cap_s)
+        if p.is_alive():
+            p.kill()
+            p.join()
+            status = f"did not finish within the {args.ref_cap_s:.0f} s cap"
+            break
+        res = q.get() if not q.empty() else ("crashed", "no result", 0.0, 0)
+        if res[0] != "ok":
+            status = f"crashed after {time.perf_counter() - t0:.1f} s: {res[1]}"
+            break
+        if i >= warm:
+            steiner.append(res[1]); times.append(res[2]); rounds = res[3]
+    value = sum(steiner) / sum(times) if times and sum(times) > 0 else None
     line = {"metric": "steiner_points_per_second", "value": value, "unit": "steiner_points/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+            "steps": len(times), "warmup": warm, "ms_per_step": 1000 * sum(times) / len(times) if times else None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": f"C2 (100k pts + 1k segs, B=1.6) bounded sample: scale x{args.ref_scale}",
-                       "B": B_C2, "parallelism": "cpu-1core"},
+            "impl": "reference", "status": status,
+            "config": {"workload": f"{args.config}: {CONFIGS[args.config][1]}" + (f" scale {args.scale}" if args.scale != 1 else ""),
+                       "B": B, "max_rounds": args.max_rounds, "rounds": rounds, "parallelism": "cpu-1core",
+                       "same_config": True, "steps_requested": args.steps},
             "cpu_baseline": {"value": value, "unit": "steiner_points/s", "cores": 1, "kind": "port",
-                             "sample": res["sample"]},
+                             "cpu": _cpu_model(), "cpus_on_host": os.cpu_count(),
+                             "sample": f"full {args.config} refine per step, {len(times)} step(s), "
+                                       f"{sum(steiner)} Steiner in {sum(times):.1f} s" if times else status},
             "e2e": {"value": value, "unit": "steiner_points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -137,8 +220,13 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gqm3d", choices=["gqm3d", "reference"])
-    ap.add_argument("--scale", type=float, default=1.0, help="workload scale (1.0 = BASELINE C2)")
-    ap.add_argument("--ref-scale", type=float, default=0.1)
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--scale", type=float, default=1.0, help="workload scale (1.0 = the BASELINE config)")
+    ap.add_argument("--max-rounds", type=int, default=500)
+    ap.add_argument("--e2e-steps", type=int, default=3, help="end-to-end refines timed (<= --steps)")
+    ap.add_argument("--ref-steps", type=int, default=2, help="reference arm: full refines timed (<= --steps)")
+    ap.add_argument("--ref-cap-s", type=float, default=240.0, help="reference arm: wall cap per refine")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
@@ -148,7 +236,6 @@ def main():
         run_reference(args, rank, world)
         return
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -160,66 +247,71 @@ def main():
     from paper_1903_03406_b200 import _native
     from paper_1903_03406_b200.prepare import facet_keep, prepare
 
-    plc = workload(args.scale)
-    cfg = RefineConfig(B=B_C2, seed=0)
-    prep = prepare(plc, seed=0)
-    keep = facet_keep(prep.plc)
+    B = CONFIGS[args.config][0]
+    plcs = workload(args.config, args.scale, rank, world)
+    cfg = RefineConfig(B=B, seed=0, max_rounds=args.max_rounds)
+    preps = [prepare(p, seed=0) for p in plcs]
+    keeps = [facet_keep(p.plc) for p in preps]
     ctx = _native.Context(local)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 
-    def device_step():
-        cnt = ctx.refine(prep, keep, cfg.B, cfg.max_rounds, cfg.seed)
-        return cnt
+    acc = {"steiner": 0, "dev_ms": 0.0, "region_ms": 0.0, "region_bytes": 0, "refine_bytes": 0, "launches": 0,
+           "rounds": 0, "nt": 0, "nv": 0}
 
-    for _ in range(args.warmup):
-        device_step()
-    # ---- timed: device-resident path
-    steiner = 0
-    dev_ms = 0.0
-    region_ms = 0.0
-    region_bytes = 0
-    launches = 0
-    cnt = None
+    def device_step(record):
+        for prep, keep in zip(preps, keeps):
+            cnt = ctx.refine(prep, keep, cfg.B, cfg.max_rounds, cfg.seed)
+            if record:
+                acc["steiner"] += int(cnt.steiner_points)
+                acc["dev_ms"] += cnt.device_ms
+                acc["region_ms"] += cnt.region_ms
+                acc["region_bytes"] += int(cnt.bytes_alg)
+                acc["refine_bytes"] += int(cnt.bytes_refine)
+                acc["launches"] += int(cnt.kernel_launches)
+                acc["rounds"] = int(cnt.n_rounds); acc["nt"] = int(cnt.n_real_tets or cnt.nt); acc["nv"] = int(cnt.nv)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    for _ in range(args.warmup):
+        device_step(False)
+    # ---- timed: device-resident path (inputs prepared and on the host once; each
+    # refine uploads its few-MB PLC before the first event and builds everything on the device)
     with ClockSampler(local) as clk:
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             flush.zero_()
-            cnt = device_step()
-            steiner += int(cnt.steiner_points)
-            dev_ms += cnt.device_ms
-            region_ms += cnt.region_ms
-            region_bytes += int(cnt.bytes_alg)
-            launches += int(cnt.kernel_launches)
+            device_step(True)
         barrier()
         wall = time.perf_counter() - t0
     # ---- timed: end to end through the public API (host PLC in, mesh + report out).
-    # refine() keeps its own per-device context: warm it up like the device arm
-    # (first-call allocations are not part of a refine).
-    for _ in range(args.warmup):
-        refine(plc, cfg)
+    # refine() keeps its own per-device context: warm it once like the device arm.
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    for p in plcs:
+        refine(p, cfg)
     barrier()
     e0 = time.perf_counter()
     e2e_steiner = 0
-    for _ in range(args.steps):
+    h2d = d2h = 0
+    setup_s = 0.0
+    for _ in range(e2e_steps):
         flush.zero_()
-        mesh, rep = refine(plc, cfg)
-        e2e_steiner += rep.steiner_points
+        for p in plcs:
+            mesh, rep = refine(p, cfg)
+            e2e_steiner += rep.steiner_points
+            setup_s += rep.device.get("prepare_s", 0.0)
     barrier()
     e2e_wall = time.perf_counter() - e0
-    h2d = prep.points.nbytes + prep.segments.nbytes + prep.poly_off.nbytes + prep.poly_idx.nbytes + prep.order.nbytes
-    d2h = (mesh.points.nbytes + mesh.vert_origin.nbytes + mesh.vert_tet.nbytes // 2 + mesh.tv.nbytes // 2
-           + mesh.tn.nbytes // 2 + mesh.alive.nbytes + mesh.sub_mask.nbytes + mesh.seg_mask.nbytes
-           + mesh.ratio.nbytes + mesh.skip_flag.nbytes)
-    # max over ranks of the device time
-    t_dev = dev_ms / 1000.0
-    tot_steiner = steiner
+    for prep in preps:
+        h2d += prep.points.nbytes + prep.segments.nbytes + prep.poly_off.nbytes + prep.poly_idx.nbytes + prep.order.nbytes
+    d2h = (mesh.points.nbytes + mesh.vert_origin.nbytes + mesh.vert_tet.nbytes + mesh.tv.nbytes + mesh.tn.nbytes
+           + mesh.alive.nbytes + mesh.sub_mask.nbytes + mesh.seg_mask.nbytes + mesh.ratio.nbytes
+           + mesh.skip_flag.nbytes) * len(plcs)
+    t_dev = acc["dev_ms"] / 1000.0
+    tot_steiner = acc["steiner"]
     if world > 1:
         tt = torch.tensor([t_dev, e2e_wall], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -230,37 +322,51 @@ def main():
     if rank == 0:
         peaks = _peaks()
         peak = float(peaks.get("hbm_gbs", 6650.0))
-        achieved = (region_bytes / (region_ms / 1000.0) / 1e9) if region_ms > 0 else 0.0
+        achieved = (acc["region_bytes"] / (acc["region_ms"] / 1000.0) / 1e9) if acc["region_ms"] > 0 else 0.0
+        whole = acc["refine_bytes"] / (acc["dev_ms"] / 1000.0) / 1e9 if acc["dev_ms"] > 0 else 0.0
         traffic, traffic_note = None, None
         try:   # dram bytes of one captured region launch (ncu --set full), committed under profiles/
-            with open(os.path.join(ROOT, "profiles", "region_traffic.json")) as f:
+            with open(os.path.join(ROOT, "profiles", f"region_traffic_{args.config}.json")) as f:
                 tr = json.load(f)
             traffic = tr["dram_bytes"]
-            traffic_note = (f"{tr['kernel']} launch {tr['launch']} of a C2 refine: dram read+write {tr['dram_bytes']} B "
-                            f"vs {tr['bytes_alg']} algorithmic B in {tr['duration_ms']} ms ({tr['source']})")
+            traffic_note = (f"{tr['kernel']} launch {tr['launch']} of a {args.config} refine: dram read+write "
+                            f"{tr['dram_bytes']} B vs {tr['bytes_alg']} algorithmic B in {tr['duration_ms']} ms "
+                            f"({tr['source']})")
         except Exception:
             pass
+        n_plc = len(plcs) * world
         line = {
             "metric": "steiner_points_per_second", "value": tot_steiner / t_dev, "unit": "steiner_points/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * t_dev / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C2: {len(plc.points)} points + {len(plc.segments)} segments in the unit cube, "
-                                   f"B={B_C2}, seed 0 (BASELINE configs[1])", "steiner_per_step": steiner // args.steps,
-                       "rounds": int(cnt.n_rounds), "tets": int(cnt.nt), "parallelism": f"replicas x{world}",
-                       "l2": "flushed (256 MB write) before every step"},
-            "wall_s_per_step": wall / args.steps,
+            "config": {"workload": f"{args.config}: {CONFIGS[args.config][1]}" + (f", scale {args.scale}" if args.scale != 1 else ""),
+                       "B": B, "plcs_per_step": n_plc, "steiner_per_step": tot_steiner // args.steps,
+                       "rounds": acc["rounds"], "vertices": acc["nv"], "tets": acc["nt"],
+                       "parallelism": f"replicas x{world}" if args.config != "C5" else f"PLC batch split over {world} GPU(s)",
+                       "l2": "flushed (256 MB write) before every step",
+                       "refine_wall_s_per_step": wall / args.steps},
             "e2e": {"value": e2e_steiner / e2e_wall, "unit": "steiner_points/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "s_per_refine": e2e_wall / args.steps},
-            "gpu_launches": launches,
+                    "d2h_bytes_per_step": int(d2h), "s_per_step": e2e_wall / e2e_steps, "steps": e2e_steps,
+                    "host_setup_s_per_step": setup_s / e2e_steps},
+            "gpu_launches": acc["launches"],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic, "traffic_note": traffic_note,
-                         "kernel": "k_region_warp + k_init_region_warp (Delaunay regions; all launches, CUDA events)",
-                         "peak_source": "measured" if not peaks.get("_fallback") else "fallback"},
+                         "kernel": "Delaunay regions: k_region_warp / k_region_block / k_region_huge + bulk-construction "
+                                   "k_init_region_warp (all launches, CUDA events)",
+                         "whole_refine": {"achieved": whole, "frac": whole / peak if peak else None,
+                                          "bytes_per_step": acc["refine_bytes"] // args.steps,
+                                          "formula": "144 N_cand + 58 T_tested + 8 K_claims + 51 T_created + "
+                                                     "1 T_deleted + 29 N_steiner (SURVEY 8(d))"},
+                         "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if not peaks.get("_fallback") else "fallback"},
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(args.ref_scale)
+            cb = cpu_sample(args.config, args.cpu_budget_s)
+            line["cpu_baseline"] = cb if cb else {
+                "value": None, "unit": "steiner_points/s", "cores": 1, "kind": "port", "cpu": _cpu_model(),
+                "sample": "none: the reference (and its port) cannot refine oblique facets (SURVEY F1); "
+                          "see bench.py --impl reference for its status on this PLC"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -14,9 +14,26 @@ import math
 
 import numpy as np
 
+from dataclasses import dataclass
+
 GHOST = -1
 FACES = ((1, 2, 3), (0, 3, 2), (0, 1, 3), (0, 2, 1))
 EDGES = ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))
+
+
+@dataclass(frozen=True)
+class ElementRef:
+    """Result of a location query (mesh.py:40-50 of the reference)."""
+    kind: str
+    index: int
+
+
+OUTSIDE = ElementRef("outside", -1)
+
+
+def _o3d(a, b, c, d) -> int:
+    from . import exactnp
+    return int(exactnp.orient3d_batch(np.asarray([a]), np.asarray([b]), np.asarray([c]), np.asarray([d]))[0])
 
 
 class Mesh:
@@ -55,6 +72,135 @@ class Mesh:
 
     def face_key(self, t, i):
         return tuple(sorted(int(self.tv[t, k]) for k in FACES[i]))
+
+    def face_vertices(self, t, i):
+        f = FACES[i]
+        return (int(self.tv[t, f[0]]), int(self.tv[t, f[1]]), int(self.tv[t, f[2]]))
+
+    def neighbor(self, t, i):
+        """(tet, face) across face i of tet t."""
+        x = int(self.tn[t, i])
+        return x >> 2, x & 3
+
+    # -- adjacency queries (mesh.py:236-293) -------------------------------
+    def tets_around_vertex(self, v):
+        """All alive tets containing vertex v (DFS from vert_tet; like the
+        reference, a stale vert_tet entry is repaired as a side effect)."""
+        start = int(self.vert_tet[v])
+        if start < 0 or start >= self.nt or not self.alive[start] or v not in self.tv[start]:
+            hit = np.flatnonzero((self.alive[:self.nt] == 1) & np.any(self.tv[:self.nt] == v, axis=1))
+            if len(hit) == 0:
+                return []
+            start = int(hit[0])
+            self.vert_tet[v] = start
+        out = [start]
+        seen = {start}
+        stack = [start]
+        while stack:
+            t = stack.pop()
+            local = list(self.tv[t]).index(v)
+            for i in range(4):
+                if i == local:
+                    continue
+                u = int(self.tn[t, i]) >> 2
+                if u >= 0 and u not in seen and self.alive[u]:
+                    seen.add(u)
+                    out.append(u)
+                    stack.append(u)
+        return out
+
+    def edge_exists(self, u, v) -> bool:
+        return any(v in self.tv[t] for t in self.tets_around_vertex(u))
+
+    def tets_around_edge(self, u, v):
+        return [t for t in self.tets_around_vertex(u) if v in self.tv[t]]
+
+    def find_tet_with_face(self, key):
+        """(t, i) of an alive tet with the sorted vertex triple as a face, or (-1, -1)."""
+        key = tuple(int(k) for k in key)
+        for t in self.tets_around_vertex(key[0]):
+            tvs = [int(x) for x in self.tv[t]]
+            if key[1] in tvs and key[2] in tvs:
+                for i in range(4):
+                    if self.face_key(t, i) == key:
+                        return t, i
+        return -1, -1
+
+    def edge_link_vertices(self, u, v):
+        """Vertices opposite the edge (u, v) in its tets, ghosts excluded."""
+        out = set()
+        for t in self.tets_around_edge(u, v):
+            for w in self.tv[t]:
+                w = int(w)
+                if w not in (u, v, GHOST):
+                    out.add(w)
+        return out
+
+    # -- location (mesh.py:297-391) -----------------------------------------
+    def locate(self, p, hint=None):
+        """ElementRef("tet", t) with t the lowest-index alive real tet
+        containing p, or OUTSIDE (exact predicates)."""
+        t = self._walk(p, hint)
+        if self.is_ghost(t):
+            return OUTSIDE
+        return ElementRef("tet", self._lowest_containing(p, t))
+
+    def _hint_tet(self, hint):
+        if isinstance(hint, ElementRef):
+            hint = hint.index if hint.kind == "tet" else None
+        if hint is not None and 0 <= hint < self.nt and self.alive[hint] and not self.is_ghost(hint):
+            return int(hint)
+        real = np.flatnonzero((self.alive[:self.nt] == 1) & (self.tv[:self.nt, 3] != GHOST))
+        if len(real) == 0:
+            from .errors import CavityNotStarShaped
+            raise CavityNotStarShaped("mesh has no alive real tets")
+        return int(real[0])
+
+    def _walk(self, p, hint=None):
+        """Stochastic remembering walk; a real tet containing p or a ghost
+        tet whose outer half-space holds p (exhaustive scan as a last resort)."""
+        p = tuple(float(x) for x in p)
+        t = self._hint_tet(hint)
+        max_steps = int(10 * max(1.0, self.nt) ** (1.0 / 3.0)) + 32
+        prev = -1
+        for step in range(1, max_steps + 1):
+            if self.is_ghost(t):
+                return t
+            moved = False
+            for k in range(4):
+                i = (k + step) & 3
+                u = int(self.tn[t, i]) >> 2
+                if u == prev:
+                    continue
+                fv = self.face_vertices(t, i)
+                if _o3d(self.points[fv[0]], self.points[fv[1]], self.points[fv[2]], p) > 0:
+                    prev, t, moved = t, u, True
+                    break
+            if not moved:
+                return t
+        for t in self.real_tets():
+            if all(_o3d(*(self.points[v] for v in self.face_vertices(t, i)), p) <= 0 for i in range(4)):
+                return t
+        for t in self.alive_tets():
+            if self.is_ghost(t) and _o3d(*(self.points[self.tv[t, k]] for k in range(3)), p) > 0:
+                return t
+        from .errors import CavityNotStarShaped
+        raise CavityNotStarShaped("walk failed to locate point")
+
+    def _lowest_containing(self, p, t):
+        found = {t}
+        stack = [t]
+        while stack:
+            cur = stack.pop()
+            for i in range(4):
+                fv = self.face_vertices(cur, i)
+                if _o3d(self.points[fv[0]], self.points[fv[1]], self.points[fv[2]], p) == 0:
+                    u = int(self.tn[cur, i]) >> 2
+                    if u >= 0 and self.alive[u] and not self.is_ghost(u) and u not in found:
+                        if all(_o3d(*(self.points[v] for v in self.face_vertices(u, j)), p) <= 0 for j in range(4)):
+                            found.add(u)
+                            stack.append(u)
+        return min(found)
 
     # -- audits (mesh.py:947-1007), vectorised -----------------------------
     def audit(self, check_delaunay: bool = False):

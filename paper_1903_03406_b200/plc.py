@@ -52,6 +52,15 @@ def points_array(plc: PLC) -> np.ndarray:
     return cache[1]
 
 
+def polygon_index_array(plc: PLC) -> np.ndarray:
+    """All polygon vertex indices, flattened (one conversion of the list)."""
+    polys = plc.polygons
+    try:
+        return np.asarray(polys, dtype=np.int64).reshape(-1)     # uniform polygons (all triangles, ...)
+    except ValueError:
+        return np.fromiter((v for p in polys for v in p), dtype=np.int64)
+
+
 def bounding_box(plc: PLC):
     if not plc.points:
         raise EmptyPLC("PLC has no points")
@@ -349,11 +358,33 @@ def unit_cube() -> PLC:
 
 def hull_simplices(plc: PLC):
     """Triangles of the convex hull of the points (scipy Qhull, as the
-    reference's _hull_covered uses, refine.py:455-459), or None."""
+    reference's _hull_covered uses, refine.py:455-459), or None.
+
+    With polygons, the hull of their vertices is built first; points strictly
+    inside its inscribed ball (with a relative margin) cannot be hull
+    vertices and are left out of the final hull computation (C4: 1M interior
+    points, 122k surface vertices)."""
     from scipy.spatial import ConvexHull, QhullError
 
+    P = points_array(plc)
     try:
-        return ConvexHull(points_array(plc)).simplices
+        if plc.polygons and len(P) > 10000:
+            sv = np.unique(polygon_index_array(plc))
+            if len(sv) >= 4:
+                h0 = ConvexHull(P[sv])
+                ctr = P[sv][h0.vertices].mean(axis=0)
+                r_in = float(np.min(-(h0.equations[:, :3] @ ctr + h0.equations[:, 3])))
+                scale = float(np.max(np.abs(P[sv] - ctr)))
+                if r_in > 1e-6 * scale:
+                    d = np.sqrt(np.sum((P - ctr) ** 2, axis=1))
+                    keep = d >= r_in * (1.0 - 1e-9) - 1e-12 * scale
+                    keep[sv] = True
+                    idx = np.flatnonzero(keep)
+                    if len(idx) == len(sv):
+                        return sv[h0.simplices]
+                    if len(idx) < len(P):
+                        return idx[ConvexHull(P[idx]).simplices]
+        return ConvexHull(P).simplices
     except QhullError:
         return None
 

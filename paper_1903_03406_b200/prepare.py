@@ -82,9 +82,8 @@ def facet_keep(plc: PLC) -> np.ndarray:
 
     out = facet_axes(plc)          # triangles with a certified normal (vectorised)
     cache = {}
-    for pid, poly in enumerate(plc.polygons):
-        if out[pid, 0] >= 0:
-            continue
+    for pid in np.flatnonzero(out[:, 0] < 0).tolist():
+        poly = plc.polygons[pid]
         pts = [plc.points[v] for v in poly]
         axis = _proj_axis(pts)
         i, j = [k for k in range(3) if k != axis]

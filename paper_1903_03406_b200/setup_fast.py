@@ -133,6 +133,26 @@ def overlapping_pairs(lo: np.ndarray, hi: np.ndarray, max_span: int = 3):
 # ---------------------------------------------------------------------------
 # validate (plc.py:267-383)
 
+def has_duplicate_points(P) -> bool:
+    """Equal coordinate triples (as the reference's tuple comparison sees
+    them: -0.0 == 0.0).  A 64-bit hash sort finds the candidates, an exact
+    comparison confirms them."""
+    if len(P) < 2:
+        return False
+    k = np.ascontiguousarray(P + 0.0).view(np.uint64).reshape(-1, 3)
+    h = (k[:, 0] * np.uint64(0x9E3779B97F4A7C15)) ^ (k[:, 1] * np.uint64(0xC2B2AE3D27D4EB4F)) \
+        ^ (k[:, 2] * np.uint64(0x165667B19E3779F9))
+    o = np.argsort(h, kind="stable")
+    hs = h[o]
+    same = np.flatnonzero(hs[1:] == hs[:-1])
+    if len(same) == 0:
+        return False
+    cand = np.unique(np.concatenate([o[same], o[same + 1]]))
+    Q = P[cand]
+    q = Q[np.lexsort((Q[:, 2], Q[:, 1], Q[:, 0]))]
+    return bool(np.any(np.all(q[1:] == q[:-1], axis=1)))
+
+
 def _native_pairs(P, S, tri):
     """(status, undecided pairs) from the device certifier, or None without a
     usable GPU / library (then the numpy path decides)."""
@@ -157,9 +177,7 @@ def certify_valid(plc, exact_pair) -> bool | None:
     npts = len(P)
     if npts == 0 or not np.all(np.isfinite(P)):
         return None
-    o = np.lexsort((P[:, 2], P[:, 1], P[:, 0]))
-    Q = P[o]
-    if np.any(np.all(Q[1:] == Q[:-1], axis=1)):     # duplicate points
+    if has_duplicate_points(P):
         return None
     S = np.asarray(plc.segments, dtype=np.int64).reshape(-1, 2)
     if len(S):
@@ -296,12 +314,17 @@ def facet_axes(plc):
     need the exact path are returned as -1."""
     polys = plc.polygons
     out = np.full((len(polys), 2), -1, dtype=np.int32)
-    idx = np.array([k for k, p in enumerate(polys) if len(p) == 3], dtype=np.int64)
+    from .plc import points_array, polygon_index_array
+    flat = polygon_index_array(plc)
+    if len(flat) == 3 * len(polys) and all(len(p) == 3 for p in polys[:1]):   # uniform: all triangles
+        idx = np.arange(len(polys), dtype=np.int64)
+        T = flat.reshape(-1, 3)
+    else:
+        idx = np.array([k for k, p in enumerate(polys) if len(p) == 3], dtype=np.int64)
+        T = np.asarray([polys[k] for k in idx], dtype=np.int64).reshape(-1, 3)
     if len(idx) == 0:
         return out
-    from .plc import points_array
     P = points_array(plc)
-    T = np.asarray([polys[k] for k in idx], dtype=np.int64)
     nrm, err = _cross_with_bound(P[T[:, 1]] - P[T[:, 0]], P[T[:, 2]] - P[T[:, 0]])
     mag = np.abs(nrm)
     best = np.argmax(mag, axis=1)                    # first on ties, like plc._proj_axis
