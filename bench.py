@@ -178,12 +178,15 @@ def run_reference(args, rank, world):
         return
     import multiprocessing as mp
     B = CONFIGS[args.config][0]
-    steps = max(1, min(args.steps, args.ref_steps))
+    # C4: the port refines ~1 round per 100 s on this PLC and stops on oblique
+    # facets later on, so both arms are compared at equal rounds
+    max_rounds = args.ref_rounds if args.config == "C4" else args.max_rounds
+    steps = max(1, min(args.steps, args.ref_steps if args.config != "C4" else 1))
     warm = 0
     times, steiner, status, rounds = [], [], "ok", 0
     for i in range(warm + steps):
         q = mp.get_context("fork").Queue()
-        p = mp.get_context("fork").Process(target=_oracle_run, args=(args.config, args.scale, args.max_rounds, q))
+        p = mp.get_context("fork").Process(target=_oracle_run, args=(args.config, args.scale, max_rounds, q))
         t0 = time.perf_counter()
         p.start()
         p.join(args.ref_cap_s)
@@ -204,7 +207,7 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference", "status": status,
             "config": {"workload": f"{args.config}: {CONFIGS[args.config][1]}" + (f" scale {args.scale}" if args.scale != 1 else ""),
-                       "B": B, "max_rounds": args.max_rounds, "rounds": rounds, "parallelism": "cpu-1core",
+                       "B": B, "max_rounds": max_rounds, "rounds": rounds, "parallelism": "cpu-1core",
                        "same_config": True, "steps_requested": args.steps},
             "cpu_baseline": {"value": value, "unit": "steiner_points/s", "cores": 1, "kind": "port",
                              "cpu": _cpu_model(), "cpus_on_host": os.cpu_count(),
@@ -224,9 +227,13 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0, help="workload scale (1.0 = the BASELINE config)")
     ap.add_argument("--max-rounds", type=int, default=500)
     ap.add_argument("--e2e-steps", type=int, default=3, help="end-to-end refines timed (<= --steps)")
-    ap.add_argument("--ref-steps", type=int, default=2, help="reference arm: full refines timed (<= --steps)")
+    ap.add_argument("--ref-steps", type=int, default=2, help="reference arm: refines timed (<= --steps)")
+    ap.add_argument("--ref-rounds", type=int, default=2,
+                    help="C4: rounds both arms run for the like-for-like comparison (SURVEY 8(d): equal max_rounds; "
+                         "the port needs ~100 s per C4 round)")
     ap.add_argument("--ref-cap-s", type=float, default=240.0, help="reference arm: wall cap per refine")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--streams", type=int, default=8, help="C5: PLCs in flight per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
@@ -258,9 +265,15 @@ def main():
     acc = {"steiner": 0, "dev_ms": 0.0, "region_ms": 0.0, "region_bytes": 0, "refine_bytes": 0, "launches": 0,
            "rounds": 0, "nt": 0, "nv": 0}
 
+    concurrent = args.config == "C5"
+    from paper_1903_03406_b200.replicas import refine_batch
+
     def device_step(record):
-        for prep, keep in zip(preps, keeps):
-            cnt = ctx.refine(prep, keep, cfg.B, cfg.max_rounds, cfg.seed)
+        if concurrent:   # the batch, args.streams PLCs in flight (one context + host thread each)
+            cnts = refine_batch(plcs, cfg, local, args.streams, prepared=(preps, keeps))
+        else:
+            cnts = (ctx.refine(prep, keep, cfg.B, cfg.max_rounds, cfg.seed) for prep, keep in zip(preps, keeps))
+        for cnt in cnts:
             if record:
                 acc["steiner"] += int(cnt.steiner_points)
                 acc["dev_ms"] += cnt.device_ms
@@ -279,19 +292,38 @@ def main():
         device_step(False)
     # ---- timed: device-resident path (inputs prepared and on the host once; each
     # refine uploads its few-MB PLC before the first event and builds everything on the device)
+    batch_ms = 0.0
     with ClockSampler(local) as clk:
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             flush.zero_()
-            device_step(True)
+            if concurrent:
+                # several contexts' streams at once: device time of the whole batch,
+                # CUDA events around it with the device drained on both sides
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                device_step(True)
+                torch.cuda.synchronize()
+                e1.record()
+                e1.synchronize()
+                batch_ms += e0.elapsed_time(e1)
+            else:
+                device_step(True)
         barrier()
         wall = time.perf_counter() - t0
+    if concurrent:
+        acc["dev_ms_sum"] = acc["dev_ms"]
+        acc["dev_ms"] = batch_ms
     # ---- timed: end to end through the public API (host PLC in, mesh + report out).
     # refine() keeps its own per-device context: warm it once like the device arm.
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    for p in plcs:
-        refine(p, cfg)
+    if concurrent:
+        refine_batch(plcs[:args.streams], cfg, local, args.streams)
+    else:
+        for p in plcs:
+            refine(p, cfg)
     barrier()
     e0 = time.perf_counter()
     e2e_steiner = 0
@@ -299,8 +331,8 @@ def main():
     setup_s = 0.0
     for _ in range(e2e_steps):
         flush.zero_()
-        for p in plcs:
-            mesh, rep = refine(p, cfg)
+        outs = refine_batch(plcs, cfg, local, args.streams) if concurrent else (refine(p, cfg) for p in plcs)
+        for mesh, rep in outs:
             e2e_steiner += rep.steiner_points
             setup_s += rep.device.get("prepare_s", 0.0)
     barrier()
@@ -343,7 +375,8 @@ def main():
             "config": {"workload": f"{args.config}: {CONFIGS[args.config][1]}" + (f", scale {args.scale}" if args.scale != 1 else ""),
                        "B": B, "plcs_per_step": n_plc, "steiner_per_step": tot_steiner // args.steps,
                        "rounds": acc["rounds"], "vertices": acc["nv"], "tets": acc["nt"],
-                       "parallelism": f"replicas x{world}" if args.config != "C5" else f"PLC batch split over {world} GPU(s)",
+                       "parallelism": f"replicas x{world}" if args.config != "C5" else
+                       f"PLC batch split over {world} GPU(s), {args.streams} PLCs in flight per GPU",
                        "l2": "flushed (256 MB write) before every step",
                        "refine_wall_s_per_step": wall / args.steps},
             "e2e": {"value": e2e_steiner / e2e_wall, "unit": "steiner_points/s", "h2d_bytes_per_step": int(h2d),
@@ -361,6 +394,14 @@ def main():
                          "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if not peaks.get("_fallback") else "fallback"},
             "clocks": clk.summary(),
         }
+        if args.config == "C4":
+            # like-for-like with the reference arm: the same PLC, the same round cap
+            prep, keep = preps[0], keeps[0]
+            cnt = ctx.refine(prep, keep, cfg.B, args.ref_rounds, cfg.seed)
+            line["equal_rounds"] = {"rounds": int(cnt.n_rounds), "steiner": int(cnt.steiner_points),
+                                    "device_s": cnt.device_ms / 1000.0,
+                                    "value": int(cnt.steiner_points) / (cnt.device_ms / 1000.0),
+                                    "note": "GPU refine stopped after the reference arm's round cap (--ref-rounds)"}
         if not args.no_cpu_baseline and world == 1:
             cb = cpu_sample(args.config, args.cpu_budget_s)
             line["cpu_baseline"] = cb if cb else {

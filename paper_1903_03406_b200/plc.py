@@ -448,12 +448,17 @@ def augment_with_box(plc: PLC) -> PLC:
     rounded midpoint lands a few ulps outside the hull, and its ghost cavity
     need not star.  The reference never reaches that case (it stops on
     oblique facets in Tri2D), so every input it refines is
-    unaffected."""
+    unaffected.  Such a box is marked (``box_for_oblique_hull``): bulk
+    construction then inserts its corners first (prepare.py), since a corner
+    inserted after the curved hull would see a quarter of it at once."""
+    for_oblique = False
     if plc.polygons:
         hs = hull_simplices(plc)
         oblique_box = os.environ.get("GQM3D_OBLIQUE_BOX", "1") != "0"   # experiments: 0 = reference rule
-        if hs is not None and hull_covered(plc, hs) and (not oblique_box or hull_axis_aligned(plc, hs)):
-            return plc
+        if hs is not None and hull_covered(plc, hs):
+            if not oblique_box or hull_axis_aligned(plc, hs):
+                return plc
+            for_oblique = True
     lo, hi = bounding_box(plc)
     pad = 0.25 * math.dist(lo, hi)
     lo = tuple(x - pad for x in lo)
@@ -471,6 +476,8 @@ def augment_with_box(plc: PLC) -> PLC:
                 quad.append(n + 4 * bits[0] + 2 * bits[1] + bits[2])
             faces.append(tuple(quad))
     edges = sorted({(min(q[k], q[(k + 1) % 4]), max(q[k], q[(k + 1) % 4])) for q in faces for k in range(4)})
-    return PLC._normalised(list(plc.points) + [tuple(float(x) for x in q) for q in corners],
-                           list(plc.segments) + [tuple(int(i) for i in e) for e in edges],
-                           list(plc.polygons) + [tuple(int(i) for i in f) for f in faces])
+    out = PLC._normalised(list(plc.points) + [tuple(float(x) for x in q) for q in corners],
+                          list(plc.segments) + [tuple(int(i) for i in e) for e in edges],
+                          list(plc.polygons) + [tuple(int(i) for i in f) for f in faces])
+    out.__dict__["box_for_oblique_hull"] = for_oblique
+    return out

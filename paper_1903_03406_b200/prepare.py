@@ -38,6 +38,15 @@ def shuffle_order(n: int, seed: int) -> np.ndarray:
     return order.astype(np.int32)
 
 
+def insertion_order(aug: PLC, n_input: int, n: int, seed: int) -> np.ndarray:
+    """The reference's shuffled order (mesh.py:878-880); for a box added
+    around an oblique hull (plc.augment_with_box) its 8 corners go first and
+    the input points follow in the shuffled order of the input alone."""
+    if not aug.__dict__.get("box_for_oblique_hull"):
+        return shuffle_order(n, seed)
+    return np.concatenate([np.arange(n_input, n, dtype=np.int32), shuffle_order(n_input, seed)])
+
+
 def prepare(plc: PLC, seed: int = 0, check: bool = True) -> Prepared:
     import time
 
@@ -68,7 +77,7 @@ def prepare(plc: PLC, seed: int = 0, check: bool = True) -> Prepared:
         off.append(len(idx))
     return Prepared(plc=aug, n_input=len(plc.points), points=pts, segments=segs,
                     poly_off=np.asarray(off, dtype=np.int32), poly_idx=np.asarray(idx, dtype=np.int32),
-                    order=shuffle_order(len(pts), seed), setup_s=time.perf_counter() - t0)
+                    order=insertion_order(aug, len(plc.points), len(pts), seed), setup_s=time.perf_counter() - t0)
 
 
 def facet_keep(plc: PLC) -> np.ndarray:

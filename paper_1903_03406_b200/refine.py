@@ -38,7 +38,7 @@ def default_device() -> int:
     return int(os.environ.get("GQM3D_DEVICE", os.environ.get("LOCAL_RANK", "0")))
 
 
-def refine(plc: PLC, cfg: RefineConfig = None, device: int = None):
+def refine(plc: PLC, cfg: RefineConfig = None, device: int = None, context: _native.Context = None):
     """Refine ``plc`` into a conforming tetrahedral mesh whose tets have
     radius-edge ratio <= cfg.B (up to the reference's skip rules).
     Returns ``(Mesh, QualityReport)``.  ``cfg`` may also be a bare float B."""
@@ -50,7 +50,7 @@ def refine(plc: PLC, cfg: RefineConfig = None, device: int = None):
     prep = prepare(plc, seed=cfg.seed)
     keep = facet_keep(prep.plc)
     t_prep = time.perf_counter() - t0
-    ctx = _context(default_device() if device is None else device)
+    ctx = context if context is not None else _context(default_device() if device is None else device)
     cnt = ctx.refine(prep, keep, cfg.B, cfg.max_rounds, cfg.seed, cfg.verbose, blast=cfg.filter == "blast")
     t_dev = time.perf_counter() - t0 - t_prep
     t1 = time.perf_counter()

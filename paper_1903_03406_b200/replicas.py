@@ -7,6 +7,8 @@ totals (Steiner points, device seconds) at the end (max-over-ranks time).
 from __future__ import annotations
 
 import os
+import queue
+import threading
 import time
 
 
@@ -54,3 +56,50 @@ def run_replicas(plcs, B: float, worker=None, group=None):
     else:
         n = len(mine)
     return {"steiner": steiner, "seconds": secs, "plcs": n, "world": world}
+
+
+def refine_batch(plcs, cfg, device: int = None, streams: int = 4, prepared=None):
+    """Refine independent PLCs on one GPU, ``streams`` at a time: each host
+    thread drives its own context (own CUDA stream, caching allocator and
+    counters), so the rounds of several PLCs overlap on the device -- one PLC
+    of C5 keeps only a few SMs busy per round.  Returns the per-PLC
+    (Mesh, QualityReport) pairs in input order (or GqCounts with
+    ``prepared=(preps, keeps)``: the device-resident path)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from . import _native
+    from .refine import default_device, refine
+
+    dev = default_device() if device is None else device
+    streams = max(1, min(streams, len(plcs) if prepared is None else len(prepared[0])))
+    pool = _contexts(dev, streams)
+    free = queue.Queue()
+    for c in pool:
+        free.put(c)
+
+    def one(i):
+        ctx = free.get()
+        try:
+            if prepared is not None:
+                prep, keep = prepared[0][i], prepared[1][i]
+                return ctx.refine(prep, keep, cfg.B, cfg.max_rounds, cfg.seed)
+            return refine(plcs[i], cfg, context=ctx)
+        finally:
+            free.put(ctx)
+
+    n = len(plcs) if prepared is None else len(prepared[0])
+    with ThreadPoolExecutor(max_workers=streams) as ex:
+        return list(ex.map(one, range(n)))
+
+
+_POOLS = {}
+_POOL_LOCK = threading.Lock()
+
+
+def _contexts(device: int, k: int):
+    from . import _native
+    with _POOL_LOCK:
+        pool = _POOLS.setdefault(device, [])
+        while len(pool) < k:
+            pool.append(_native.Context(device))
+        return pool[:k]
