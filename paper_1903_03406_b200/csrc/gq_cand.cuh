@@ -162,6 +162,56 @@ __device__ __noinline__ void seg_split_point(const Dev& D, int r, double* p) {
   for (int k = 0; k < 3; ++k) p[k] = a[k] + d[k] * f;
 }
 
+// Convex-hull guard for constraint splits on an oblique hull (a PLC whose
+// polygons tile a curved convex hull, C4's outer sphere: no box is added
+// then, refine.py:462-475).  The ghost tets that close the mesh assume the
+// hull stays convex; a midpoint / circumcentre rounded a few ulps INSIDE the
+// hull faces it splits would leave a reflex hull edge, after which hull
+// cavities stop starring and the hull subsegments split down to rounding
+// level.  Such a point is pushed outward along the faces' normals by the
+// smallest power-of-two step that puts it on or outside every hull face it
+// splits (exact orient3d >= 0), so it becomes a hull vertex.  Axis-aligned
+// hulls never need it: their split points round exactly onto the facet planes.
+__device__ inline void hull_nudge(const Dev& D, double* p, const int4* hf, int nh) {
+  bool ok = true;
+  for (int k = 0; k < nh && ok; ++k) ok = orient3d(PT(D, hf[k].x), PT(D, hf[k].y), PT(D, hf[k].z), p) >= 0;
+  if (ok) return;
+  double N[3] = {0, 0, 0};
+  for (int k = 0; k < nh; ++k) {
+    const double *x = PT(D, hf[k].x), *y = PT(D, hf[k].y), *z = PT(D, hf[k].z);
+    double u[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]}, v[3] = {z[0] - x[0], z[1] - x[1], z[2] - x[2]};
+    double n[3] = {u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2], u[0] * v[1] - u[1] * v[0]};
+    double l = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+    if (l > 0) for (int a = 0; a < 3; ++a) N[a] += n[a] / l;
+  }
+  double scale = fmax(fabs(p[0]), fmax(fabs(p[1]), fabs(p[2])));
+  for (int e = -52; e < 8 - 52 + 40; ++e) {
+    double step = scale * ldexp(1.0, e);
+    double q[3] = {p[0] + N[0] * step, p[1] + N[1] * step, p[2] + N[2] * step};
+    bool good = true;
+    for (int k = 0; k < nh && good; ++k) good = orient3d(PT(D, hf[k].x), PT(D, hf[k].y), PT(D, hf[k].z), q) >= 0;
+    if (good) { p[0] = q[0]; p[1] = q[1]; p[2] = q[2]; return; }
+  }
+}
+__device__ __noinline__ void hull_guard_seg(const Dev& D, int a, int b, double* p, Scratch& S) {
+  int4 hf[8]; int nh = 0;
+  around_vertex(D, a, S.tset, S.stack, 2 * S.cap, [&](int t) {
+    int4 q = D.tv[t];
+    if (q.w == GHOST && has_v(q, b) && nh < 8) hf[nh++] = q;
+    return false;
+  }, [&] { nh = 0; });
+  if (nh) hull_nudge(D, p, hf, nh);
+}
+__device__ __noinline__ void hull_guard_face(const Dev& D, int slot, double* p) {
+  if (slot < 0) return;
+  int t = slot >> 2, u = tnk(D, t, slot & 3) >> 2;
+  int4 hf[1];
+  if (D.tv[t].w == GHOST) hf[0] = D.tv[t];
+  else if (u >= 0 && D.tv[u].w == GHOST) hf[0] = D.tv[u];
+  else return;
+  hull_nudge(D, p, hf, 1);
+}
+
 // fills point / priority / seed / allowed pids / claim extra for candidate c.
 // Returns false when the element is degenerate (DegenerateTet / DegenerateTri).
 __device__ __noinline__ bool make_cand(const Dev& D, const Cand& C, int c, const CandCtx& X, Scratch& S) {
@@ -180,6 +230,7 @@ __device__ __noinline__ bool make_cand(const Dev& D, const Cand& C, int c, const
     int2 e = D.sg_uv[tgt];
     canon[0] = e.x; canon[1] = e.y; nc = 2;
     seg_split_point(D, tgt, p);
+    if (X.with_facets && D.poly_obl_hull) hull_guard_seg(D, e.x, e.y, p, S);
     if (!edge_exists(D, e.x, e.y, S.tset, S.stack, 2 * S.cap)) C.seed[c] = walk_seed(D, p, e.x);
     if (X.with_facets) {
       int sid = D.sg_sid[tgt];
@@ -202,6 +253,7 @@ __device__ __noinline__ bool make_cand(const Dev& D, const Cand& C, int c, const
     if (!circumcircle_tri(PT(D, f.x), PT(D, f.y), PT(D, f.z), s)) return false;
     p[0] = s.c[0]; p[1] = s.c[1]; p[2] = s.c[2];
     int slot = find_face(D, f.x, f.y, f.z, S.tset, S.stack, 2 * S.cap);
+    if (D.poly_obl_hull && D.poly_obl[f.w]) hull_guard_face(D, slot, p);
     if (slot < 0) C.seed[c] = walk_seed(D, p, f.x);
     C.allow[c] = make_int4(f.w, -1, -1, -1); C.nallow[c] = 1;
     if (slot >= 0) C.extra[c] = min(slot, tnk(D, slot >> 2, slot & 3));

@@ -107,6 +107,7 @@ struct Dev {
   int* segpoly;
   int2* sid_uv;        // original segment endpoints
   uint8_t* vapex;      // input vertex where two input segments meet at < 45 degrees (n_input entries)
+  int poly_obl_hull;   // some oblique polygon lies on the convex hull (hull_guard_*, gq_cand.cuh)
   int nsid, npoly;
   double too_close_sq, lmin2;
   Counters* ctr;
@@ -372,6 +373,56 @@ __device__ inline int walk_cap(const Dev& D, int extra) {
   double nt = D.ctr->nt > 1 ? (double)D.ctr->nt : 1.0;
   return (int)(10.0 * pow(nt, 1.0 / 3.0)) + extra;
 }
+// closed containment of p in real tet t (every face orient3d <= 0)
+__device__ inline bool contains_closed(const Dev& D, int t, const double* p) {
+  int4 q = D.tv[t];
+  for (int i = 0; i < 4; ++i) {
+    int f[3]; face_verts(q, i, f);
+    if (orient3d(PT(D, f[0]), PT(D, f[1]), PT(D, f[2]), p) > 0) return false;
+  }
+  return true;
+}
+// The exhaustive scan below returns the lowest-index real tet containing p
+// (else the lowest-index ghost whose hull face sees p).  Those tets form a
+// face-connected set around the tet a walk ends in (the tets sharing the
+// face / edge / vertex p lies on; the visible part of the convex hull), so a
+// bounded search from there gives the same answer; -1 when the set is larger
+// than the search's arena.
+__device__ __noinline__ int lowest_equivalent(const Dev& D, const double* p, int t0) {
+  const int CAP = 96;
+  int found[CAP];
+  int n = 0, head = 0;
+  bool ghost = D.tv[t0].w == GHOST;
+  found[n++] = t0;
+  int best = t0;
+  while (head < n) {
+    int cur = found[head++];
+    int4 q = D.tv[cur];
+    for (int i = 0; i < 4; ++i) {
+      int u = tnk(D, cur, i) >> 2;
+      if (u < 0 || !D.alive[u]) continue;
+      int4 qu = D.tv[u];
+      bool member;
+      if (ghost) {
+        if (qu.w != GHOST) continue;
+        member = orient3d(PT(D, qu.x), PT(D, qu.y), PT(D, qu.z), p) > 0;
+      } else {
+        if (qu.w == GHOST) continue;
+        int f[3]; face_verts(q, i, f);
+        if (orient3d(PT(D, f[0]), PT(D, f[1]), PT(D, f[2]), p) != 0) continue;   // p not on the shared face
+        member = contains_closed(D, u, p);
+      }
+      if (!member) continue;
+      bool seen = false;
+      for (int k = 0; k < n && !seen; ++k) seen = found[k] == u;
+      if (seen) continue;
+      if (n >= CAP) return -1;
+      found[n++] = u;
+      if (u < best) best = u;
+    }
+  }
+  return best;
+}
 __device__ __noinline__ int walk(const Dev& D, const double* p, int hint) {
   int t = hint_tet(D, hint);
   int max_steps = walk_cap(D, 32);
@@ -389,6 +440,42 @@ __device__ __noinline__ int walk(const Dev& D, const double* p, int hint) {
       if (orient3d(PT(D, f[0]), PT(D, f[1]), PT(D, f[2]), p) > 0) { prev = t; t = u; moved = true; break; }
     }
     if (!moved) return t;
+  }
+  {
+    // The deterministic walk cycled (it can on a constrained mesh).  Where
+    // the reference scans every tet (mesh.py:362-371), first finish with a
+    // randomised remembering walk, which leaves any cycle, and resolve the
+    // scan's tie rule locally (lowest_equivalent): same tet, no O(nt) pass.
+    unsigned long long r = 0x9E3779B97F4A7C15ull ^ (unsigned long long)t;
+    prev = -1;
+    for (int s2 = 0; s2 < 16 * max_steps; ++s2) {
+      int4 q = D.tv[t];
+      if (q.w == GHOST) break;
+      r = r * 6364136223846793005ull + 1442695040888963407ull;
+      int off = (int)(r >> 62);
+      bool moved = false;
+      for (int k = 0; k < 4; ++k) {
+        int i = (k + off) & 3;
+        int u = tnk(D, t, i) >> 2;
+        if (u == prev) continue;
+        int f[3]; face_verts(q, i, f);
+        if (orient3d(PT(D, f[0]), PT(D, f[1]), PT(D, f[2]), p) > 0) { prev = t; t = u; moved = true; break; }
+      }
+      if (!moved) {
+        int b = lowest_equivalent(D, p, t);
+        if (b >= 0) return b;
+        break;
+      }
+    }
+    if (D.tv[t].w == GHOST) {
+      int4 q = D.tv[t];
+      if (orient3d(PT(D, q.x), PT(D, q.y), PT(D, q.z), p) > 0) {
+        // outside the hull: the reference returns the lowest ghost seeing p, but only when
+        // no real tet contains p -- true here, since the walk left the hull through a visible face
+        int b = lowest_equivalent(D, p, t);
+        if (b >= 0) return b;
+      }
+    }
   }
   int nt = D.ctr->nt;
   for (int s = 0; s < nt; ++s) {

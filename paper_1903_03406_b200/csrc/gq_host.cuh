@@ -363,6 +363,7 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   D.segpoly = dmalloc<int>(std::max(npidx, 1));
   D.sid_uv = dmalloc<int2>(std::max(m, 1));
   D.vapex = nullptr;   // set by refine_impl
+  D.poly_obl_hull = 0;
   D.nsid = m; D.npoly = f;
   c->dctr = dmalloc<Counters>(1);
   D.ctr = c->dctr;
@@ -1449,6 +1450,8 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
         if (same) obl[pid] = 0;
       }
     CK(cudaMemcpyAsync(D.poly_obl, obl.data(), f, cudaMemcpyHostToDevice, c->st));
+    D.poly_obl_hull = 0;   // the hull guards act only where a ghost tet touches the split element
+    for (int pid = 0; pid < f && !D.poly_obl_hull; ++pid) D.poly_obl_hull = obl[pid];
     if (!sp.empty()) CK(cudaMemcpyAsync(D.segpoly, sp.data(), 4 * sp.size(), cudaMemcpyHostToDevice, c->st));
   }
   CK(cudaMemcpyAsync(D.segpoly_off, spo.data(), 4 * (size_t)(m + 1), cudaMemcpyHostToDevice, c->st));
