@@ -184,10 +184,14 @@ __device__ inline void hull_nudge(const Dev& D, double* p, const int4* hf, int n
     double l = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
     if (l > 0) for (int a = 0; a < 3; ++a) N[a] += n[a] / l;
   }
+  // steps are whole multiples of u = ulp(max |coordinate|): a coordinate moves
+  // by 0 or by >= u, so no tiny coordinates appear (the exact predicates'
+  // fixed-width integers size themselves by the exponent spread)
   double scale = fmax(fabs(p[0]), fmax(fabs(p[1]), fabs(p[2])));
-  for (int e = -52; e < 8 - 52 + 40; ++e) {
-    double step = scale * ldexp(1.0, e);
-    double q[3] = {p[0] + N[0] * step, p[1] + N[1] * step, p[2] + N[2] * step};
+  double u = ldexp(1.0, ilogb(scale) - 52);
+  for (int e = 0; e < 40; ++e) {
+    double step = ldexp(1.0, e);
+    double q[3] = {p[0] + rint(N[0] * step) * u, p[1] + rint(N[1] * step) * u, p[2] + rint(N[2] * step) * u};
     bool good = true;
     for (int k = 0; k < nh && good; ++k) good = orient3d(PT(D, hf[k].x), PT(D, hf[k].y), PT(D, hf[k].z), q) >= 0;
     if (good) { p[0] = q[0]; p[1] = q[1]; p[2] = q[2]; return; }

@@ -49,6 +49,10 @@ struct Counters {
   // [4] encroached by an off-plane apex, [5] encroached by a (near-)coplanar apex
   unsigned int chk[8];
   unsigned int skipr[12];            // skipped elements by kind * 4 + reason (diagnostics)
+  unsigned int fail[8];              // failed-region causes (diagnostics): 0 no seed, 1 seed peeled,
+                                     // 2 swallows a vertex, 3 pinched ghost boundary, 4 star check,
+                                     // 5 sequential-path overflow, 6 membrane
+  int first_real;                    // no alive real tet has a lower index (hint_tet; 0 after compaction)
 };
 
 // A tet is one 32-byte record {tv, tn} (vertices, then packed neighbour
@@ -362,10 +366,15 @@ __device__ inline int find_face(const Dev& D, int a, int b, int c, ISet& seen, i
 
 // ---------------------------------------------------------------------------
 // walks (mesh.py:307-371)
+// mesh.py:307-320: the hint, else the lowest-index alive real tet.  Tet slots
+// only die or are appended between compactions, so that index never
+// decreases: the scan starts at the last one found (D.ctr->first_real) and
+// returns exactly what a scan from slot 0 would.
 __device__ __noinline__ int hint_tet(const Dev& D, int hint) {
   int nt = D.ctr->nt;
   if (hint >= 0 && hint < nt && D.alive[hint] && D.tv[hint].w != GHOST) return hint;
-  for (int t = 0; t < nt; ++t) if (D.alive[t] && D.tv[t].w != GHOST) return t;
+  for (int t = max(D.ctr->first_real, 0); t < nt; ++t)
+    if (D.alive[t] && D.tv[t].w != GHOST) { atomicMax(&D.ctr->first_real, t); return t; }
   raise_err(GQ_ERR_WALK);
   return 0;
 }

@@ -192,6 +192,7 @@ __global__ void k_fallback(Dev D, Cand C, Scr SCB, FallbackIO F, T2Items T, Skip
       if (kind == K_SEG) D.sg_fl[tgt] |= RF_BLOCK;
       else if (kind == K_FACE) D.sf_fl[tgt] |= RF_BLOCK;
     } else {
+      if (st == RS_OVERFLOW) atomicAdd(&D.ctr->fail[5], 1u);
       // not star-shaped, or a cavity beyond the sequential path's arena
       // (8192 tets): skipped like the reference's CavityNotStarShaped
       skip_cand(D, C, c, 3, F.round_no, L);
@@ -442,6 +443,7 @@ __global__ void __launch_bounds__(32 * WS_WARPS) k_star_check(Dev D, Cand C, con
     else if (C.bigi[c] >= HUGE_BASE) ok = star_pairs_ok(D, v.bf, nbf, huge_star_hash(C, c, &X.flag));
     else ok = star_pairs_ok(D, v.bf, nbf, big_star_hash(SB, gw, &X.flag));
     if (!ok && lane == 0) {
+      atomicAdd(&D.ctr->fail[4], 1u);
       insflag[k] = 0;
       skip_cand(D, C, c, 3, round_no, L);
     }

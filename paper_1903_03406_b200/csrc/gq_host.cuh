@@ -797,6 +797,7 @@ static void compact_tets(gq_ctx* c) {
   std::swap(D.ratio, c->ratio2); std::swap(D.skip, c->skip2);
   CK(cudaMemsetAsync(D.alive, 0, nt, c->st));
   CK(cudaMemsetAsync(D.alive, 1, na, c->st));
+  CK(cudaMemsetAsync(&c->dctr->first_real, 0, sizeof(int), c->st));   // ids renumbered
   c->hc.nt = na;
   push(c);
 }
@@ -1232,6 +1233,7 @@ static void fine(gq_ctx* c, int k) {
 static RoundOut run_round(gq_ctx* c, int round_no) {
   RoundOut R;
   c->big_used = 0;
+  if (getenv("GQ_TRACE_FROM")) g_trace = round_no >= atoi(getenv("GQ_TRACE_FROM"));   // stage trace from a round on
   pull(c);
   maintain_capacity(c);
   ensure_q(c, (size_t)std::max(std::max(c->hc.nt, c->hc.nsegrec + c->hc.nfacerec), c->C.cap) * 2 + 4096);
@@ -1543,11 +1545,12 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
       const unsigned int* k = c->hc.chk;
       std::fprintf(stderr, "round %d phase=%d candidates=%lld accepted=%lld blasted=%lld failed=%lld inserted=%lld time=%.4f"
                    " | nv %d nt %d segs %d faces %d skipped %d | check: seg miss %u enc %u (collinear %u) face miss %u enc %u (coplanar %u)"
-                   " | skips seg %u/%u/%u/%u face %u/%u/%u/%u tet %u/%u/%u/%u\n",
+                   " | skips seg %u/%u/%u/%u face %u/%u/%u/%u tet %u/%u/%u/%u | fails %u/%u/%u/%u/%u/%u/%u\n",
                    round_no, R.phase, R.ncand, R.acc, R.rej, R.failed, R.inserted, dt, c->hc.nv, c->hc.nt, c->hc.nsegrec,
                    c->hc.nfacerec, c->hc.nskip, k[0], k[1], k[2], k[3], k[4], k[5], c->hc.skipr[0], c->hc.skipr[1],
                    c->hc.skipr[2], c->hc.skipr[3], c->hc.skipr[4], c->hc.skipr[5], c->hc.skipr[6], c->hc.skipr[7],
-                   c->hc.skipr[8], c->hc.skipr[9], c->hc.skipr[10], c->hc.skipr[11]);
+                   c->hc.skipr[8], c->hc.skipr[9], c->hc.skipr[10], c->hc.skipr[11], c->hc.fail[0], c->hc.fail[1],
+                   c->hc.fail[2], c->hc.fail[3], c->hc.fail[4], c->hc.fail[5], c->hc.fail[6]);
     }
     round_no += 1;
   }

@@ -110,7 +110,7 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
     __syncwarp();
     seed = W.seed;
     WMARK(50);
-    if (seed < 0) return RS_CNSS;
+    if (seed < 0) { if (lane == 0) atomicAdd(&D.ctr->fail[0], 1u); return RS_CNSS; }
   }
   O.seed = seed;
   WSTOP(1);
@@ -188,7 +188,7 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
     WMARK(50);
     const bool shrunk = !W.in[0];
     __syncwarp();
-    if (shrunk) return RS_CNSS;          // seed shrunk away
+    if (shrunk) { if (lane == 0) atomicAdd(&D.ctr->fail[1], 1u); return RS_CNSS; }   // seed shrunk away
     for (int k = lane; k < n; k += 32) W.comp[k] = 0;
     __syncwarp();
     if (lane == 0) { W.comp[0] = 1; W.f0[0] = 0; W.cnt = 1; }
@@ -272,7 +272,11 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
   }
   __syncwarp();
   DCHK(W.memb == INT_MAX || (W.memb >> 2) < m);
-  if (W.memb != INT_MAX) { O.memb = 4 * O.tets[W.memb >> 2] + (W.memb & 3); return RS_MEMBRANE; }
+  if (W.memb != INT_MAX) {
+    O.memb = 4 * O.tets[W.memb >> 2] + (W.memb & 3);
+    if (lane == 0) atomicAdd(&D.ctr->fail[6], 1u);
+    return RS_MEMBRANE;
+  }
   int incl = mycnt;
   for (int o = 1; o < 32; o <<= 1) { int v = __shfl_up_sync(FULL, incl, o); if (lane >= o) incl += v; }
   const int nbf = __shfl_sync(FULL, incl, 31);
@@ -293,8 +297,10 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
   }
   __syncwarp();
   if (__any_sync(FULL, bf_has_ghost_part(D, O.bf, nbf, lane, 32)) &&
-      __any_sync(FULL, bf_open_part(D, O.bf, nbf, lane, 32)))
+      __any_sync(FULL, bf_open_part(D, O.bf, nbf, lane, 32))) {
+    if (lane == 0) atomicAdd(&D.ctr->fail[3], 1u);
     return RS_BADSTAR;
+  }
   WSTOP(5);
   WMARK(15);
   // boundary vertices: min distance and the swallow check (hash reused)
@@ -331,7 +337,7 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
     }
   }
   WMARK(50);
-  if (__any_sync(FULL, swallow)) return RS_CNSS;
+  if (__any_sync(FULL, swallow)) { if (lane == 0) atomicAdd(&D.ctr->fail[2], 1u); return RS_CNSS; }
   WSTOP(6);
   WMARK(16);
   O.ntet = m; O.nbf = nbf; O.mind = mymin;

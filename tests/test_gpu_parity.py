@@ -79,6 +79,11 @@ def test_refine_matches_reference(gq, golden_dir, name):
                      for r in rep.per_round], dtype=np.int64).reshape(-1, 9)
     assert np.array_equal(rows, g["per_round"])
     assert sorted(mesh.subfaces) == sorted(tuple(r[:3]) for r in g["subfaces"].tolist())
+    # report fields: the device quality scan's 36-bin dihedral histogram and
+    # the skip list equal the reference's (stats.py:26-99, refine.py:669-675)
+    assert list(rep.dihedral_histogram) == g["hist"].tolist()
+    import json
+    assert rep.skipped == json.loads(str(g["skipped"]))
 
 
 @pytest.mark.parametrize("seed,rounds", [(1, 500), (2, 500), (0, 7)])
@@ -101,6 +106,19 @@ def test_refine_c2_scaled_vs_oracle(gq):
     ref = oracle.refine(plc, B=1.6)
     assert np.array_equal(mesh.points, ref["points"])
     assert rep.bad_tet_count == int(((ref["alive"] == 1) & (ref["tv"][:, 3] >= 0) & (ref["ratio"] > 1.6)).sum())
+    _same_report(mesh, rep, ref)
+
+
+def _same_report(mesh, rep, ref):
+    """Beyond the point set: same tets in the same slots, bit-identical
+    radius-edge ratios, the same skip list and per-round rows."""
+    assert np.array_equal(mesh.alive, ref["alive"])
+    live = ref["alive"] == 1
+    assert np.array_equal(mesh.tv[live], ref["tv"][live])
+    assert np.array_equal(mesh.ratio[live].view(np.int64), ref["ratio"][live].view(np.int64))
+    assert rep.skipped == ref["skipped"]
+    key = ("round", "phase", "candidates", "accepted", "blasted", "failed", "inserted", "pending_segments", "pending_faces")
+    assert [tuple(r[k] for k in key) for r in rep.per_round] == [tuple(r[k] for k in key) for r in ref["per_round"]]
 
 
 @pytest.mark.parametrize("cfg,scale,B", [("C3", 0.02, 1.4), ("C5", 0.05, 1.5), ("C1", 1.0, 2.0)])
@@ -116,6 +134,20 @@ def test_refine_other_configs_vs_oracle(gq, cfg, scale, B):
     assert np.array_equal(mesh.points, ref["points"])
     assert len(rep.per_round) == len(ref["per_round"])
     mesh.audit()
+
+
+@pytest.mark.parametrize("cfg,scale,B", [("C3", 0.2, 1.4), ("C5", 1.0, 1.5)])
+def test_refine_at_scale_vs_oracle(gq, cfg, scale, B):
+    """Parity at scale: C3 (parity variant) at 1/5 -- 50k points, 400
+    triangles -- and one full PLC of the C5 batch (cube + 50k points):
+    bit-identical points, tets, ratios, skip lists and per-round rows."""
+    import oracle
+    from paper_1903_03406_b200 import synth
+    plc = synth.config_plc(cfg, scale=scale)
+    mesh, rep = _refine(plc, B)
+    ref = oracle.refine(plc, B=B)
+    assert np.array_equal(mesh.points, ref["points"])
+    _same_report(mesh, rep, ref)
 
 
 def test_paper_literal_blast_mode_within_two_percent(gq, golden_dir):
@@ -165,3 +197,20 @@ def test_no_cpu_fallback_library_loaded(gq):
     import paper_1903_03406_b200._native as nat
     assert os.path.basename(nat.lib_path()) in ("libgqm3d.so",) or "GQM3D_LIB" in os.environ
     assert nat._LIB is not None
+
+
+def test_concurrent_contexts_match_sequential(gq):
+    """C5's batch path: several PLCs in flight on one GPU (one context, stream
+    and host thread each) give exactly the single-context results."""
+    from paper_1903_03406_b200 import RefineConfig, synth
+    from paper_1903_03406_b200.replicas import refine_batch
+    plcs = [synth.cube_points(800 + 100 * k, k) for k in range(5)]
+    cfg = RefineConfig(B=1.5)
+    seq = [_refine(p, 1.5) for p in plcs]
+    par = refine_batch(plcs, cfg, streams=3)
+    for (m0, r0), (m1, r1) in zip(seq, par):
+        assert np.array_equal(m0.points, m1.points)
+        assert r0.per_round == r1.per_round or [
+            {k: v for k, v in r.items() if k != "time"} for r in r0.per_round] == [
+            {k: v for k, v in r.items() if k != "time"} for r in r1.per_round]
+        assert r0.dihedral_histogram == r1.dihedral_histogram
