@@ -108,6 +108,10 @@ int gq_write_mesh(const char* node_path, const char* ele_path, const char* face_
 int gq_certify_pairs(int device, const double* xyz, int32_t n, const int32_t* seg, int32_t m, const int32_t* tri,
                      int32_t f, int32_t* status, int32_t* pairs, int64_t pair_cap, int64_t* n_pairs);
 
+/* FP64 FMA throughput of the device in TFLOP/s (2 flops per FMA, best of 5;
+ * the secondary roofline of the predicate filters). */
+int gq_probe_fp64(int device, double* tflops);
+
 /* batched exact predicates / constructions on the device, for parity tests:
  * which 0 orient3d(12) 1 insphere(15) 2 orient2d(6) 3 incircle2d(8)
  * 4 incircle3d(12) 5 encroaches_segment(9) 6 encroaches_face(12) -> out8;

@@ -35,7 +35,8 @@ class GqCounts(ctypes.Structure):
 
 
 EXPORTS = ("gq_create", "gq_destroy", "gq_last_error", "gq_refine", "gq_export_mesh", "gq_export_constraints",
-           "gq_export_rounds", "gq_export_skipped", "gq_quality", "gq_batch", "gq_write_mesh", "gq_certify_pairs")
+           "gq_export_rounds", "gq_export_skipped", "gq_quality", "gq_batch", "gq_write_mesh", "gq_certify_pairs",
+           "gq_probe_fp64")
 
 
 def lib_path() -> str:
@@ -63,6 +64,7 @@ def lib():
         L.gq_quality.argtypes = [vp, ctypes.c_double, vp, vp]
         L.gq_batch.argtypes = [ctypes.c_int, vp, i32, i32, vp, vp]
         L.gq_write_mesh.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, vp, vp, i32, vp, vp, i32, vp, i32]
+        L.gq_probe_fp64.argtypes = [ctypes.c_int, vp]
         L.gq_certify_pairs.argtypes = [ctypes.c_int, vp, i32, vp, i32, vp, i32, vp, vp, ctypes.c_int64, vp]
         for name in EXPORTS:
             if name not in ("gq_last_error",):
@@ -185,3 +187,12 @@ def certify_pairs(points: np.ndarray, segments: np.ndarray, triangles: np.ndarra
     if rc != 0:
         raise NativeError(rc, "gq_certify_pairs failed")
     return int(st[0]), pairs[:int(npairs[0])]
+
+
+def probe_fp64(device: int = 0) -> float:
+    """Measured FP64 FMA peak of the device in TFLOP/s (gq_probe_fp64)."""
+    out = np.zeros(1)
+    rc = lib().gq_probe_fp64(int(device), _p(out))
+    if rc != 0:
+        raise NativeError(rc, "gq_probe_fp64 failed")
+    return float(out[0])

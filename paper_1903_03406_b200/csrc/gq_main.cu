@@ -295,6 +295,48 @@ int gq_certify_pairs(int device, const double* xyz, int32_t n, const int32_t* se
   return GQ_OK;
 }
 
+// FP64 FMA throughput probe (the secondary roofline of SURVEY 8(d): the
+// predicate filters are FP64 chains).  8 independent FMA chains per thread,
+// grid = 148 SMs x 8 blocks x 256 threads; CUDA events around the kernel.
+__global__ void k_fp64_fma(double* out, int iters, double a, double b) {
+  double x[8];
+  for (int k = 0; k < 8; ++k) x[k] = (double)(threadIdx.x + k) * 1e-3;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0;
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;   // keep the chains alive
+}
+int gq_probe_fp64(int device, double* tflops) {
+  if (!tflops) return GQ_EINVAL;
+  try {
+    CK(cudaSetDevice(device));
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    double* d = dmalloc<double>(1);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+    const int blocks = nsm * 8, threads = 256, iters = 1 << 14;
+    k_fp64_fma<<<blocks, threads>>>(d, 16, 0.999, 1e-3);   // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+      CK(cudaEventRecord(e0));
+      k_fp64_fma<<<blocks, threads>>>(d, iters, 0.999, 1e-3);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0; CK(cudaEventElapsedTime(&ms, e0, e1));
+      best = std::min(best, ms);
+    }
+    double flops = 2.0 * 8 * (double)iters * blocks * threads;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    dfree(d);
+  } catch (std::exception&) { return GQ_ECUDA; }
+  return GQ_OK;
+}
+
 int gq_batch(int which, const double* in, int32_t n, int32_t width, int8_t* out8, double* outd) {
   try {
     double* din = dmalloc<double>((size_t)n * width);

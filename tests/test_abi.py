@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared():
     src = open(os.path.join(ROOT, "include", "gqm3d.h")).read()
-    return sorted(set(re.findall(r"\b(gq_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(gq_[a-z_0-9]+)\s*\(", src)))
 
 
 def test_header_declares_the_boundary():
