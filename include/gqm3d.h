@@ -86,8 +86,12 @@ int gq_export_rounds(gq_ctx* ctx, int64_t* rows, double* seconds);
  * 2 too_close,3 cavity_not_star_shaped), nverts, v0..v3 */
 int gq_export_skipped(gq_ctx* ctx, int32_t* rows);
 /* radius-edge ratio > B count and the 36-bin dihedral histogram of the real
- * tets (stats.py:26-99), computed on the device */
-int gq_quality(gq_ctx* ctx, double B, int64_t* bad_count, int64_t* hist36);
+ * tets (stats.py:26-99), computed on the device.  Tets with a dihedral angle
+ * within rounding of a 5-degree bin edge are left out of hist36 and listed in
+ * edge_tets (capacity edge_cap, count n_edge) for the caller to bin with the
+ * reference's own expression (the last bit of acos differs between libraries). */
+int gq_quality(gq_ctx* ctx, double B, int64_t* bad_count, int64_t* hist36, int32_t* edge_tets, int64_t edge_cap,
+               int64_t* n_edge);
 
 /* .node / .ele / .face files of a refined mesh (host only; formats.py:210-263 of
  * the reference: 1-based ids, "%.17g" coordinates, origin attribute, alive

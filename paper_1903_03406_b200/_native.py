@@ -61,7 +61,7 @@ def lib():
         L.gq_export_constraints.argtypes = [vp, vp, vp]
         L.gq_export_rounds.argtypes = [vp, vp, vp]
         L.gq_export_skipped.argtypes = [vp, vp]
-        L.gq_quality.argtypes = [vp, ctypes.c_double, vp, vp]
+        L.gq_quality.argtypes = [vp, ctypes.c_double, vp, vp, vp, ctypes.c_int64, vp]
         L.gq_batch.argtypes = [ctypes.c_int, vp, i32, i32, vp, vp]
         L.gq_write_mesh.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, vp, vp, i32, vp, vp, i32, vp, i32]
         L.gq_probe_fp64.argtypes = [ctypes.c_int, vp]
@@ -144,11 +144,15 @@ class Context:
         self._check(self._L.gq_export_skipped(self._h, _p(rows)))
         return rows
 
-    def quality(self, B: float):
+    def quality(self, B: float, edge_cap: int = 1 << 22):
+        """(bad count, device histogram, tets whose dihedral angles sit on a
+        bin edge -- to be binned by the caller with the reference's formula)."""
         bad = np.zeros(1, np.int64)
         hist = np.zeros(36, np.int64)
-        self._check(self._L.gq_quality(self._h, float(B), _p(bad), _p(hist)))
-        return int(bad[0]), hist
+        edges = np.zeros(edge_cap, np.int32)
+        ne = np.zeros(1, np.int64)
+        self._check(self._L.gq_quality(self._h, float(B), _p(bad), _p(hist), _p(edges), int(edge_cap), _p(ne)))
+        return int(bad[0]), hist, edges[:int(ne[0])]
 
 
 _BATCH = {"orient3d": (0, 12), "insphere": (1, 15), "orient2d": (2, 6), "incircle2d": (3, 8),

@@ -60,6 +60,7 @@ struct Cand {          // candidate arrays (capacity cap)
   int* htets; int* hbf; int* hcr; int* hcrf; int* hbsub; int* hbseg; int* heseg;
   unsigned long long* hskey; int* hsv0; int* hsv1;
   int nhugecap, ht, hf, hc, hs;
+  const int* segpoly;    // D.segpoly (allowed polygons of a segment shared by more than 4)
 };
 #define HUGE_BASE (1 << 28)
 struct SlabView { int* tets; int* bf; int* cr; int* crf; int* bsub; int* bseg; int* eseg; int ct, cf, cc; };
@@ -241,12 +242,15 @@ __device__ __noinline__ bool make_cand(const Dev& D, const Cand& C, int c, const
       int o0 = D.segpoly_off[sid], o1 = D.segpoly_off[sid + 1];
       int na = 0;
       int4 al = make_int4(-1, -1, -1, -1);
-      for (int o = o0; o < o1 && na < 4; ++o) {
-        int pid = D.segpoly[o];
-        if (na == 0) al.x = pid; else if (na == 1) al.y = pid; else if (na == 2) al.z = pid; else al.w = pid;
-        ++na;
+      if (o1 - o0 > 4) {          // more polygons than fit inline: refer to the segment's list
+        al.x = o0; na = o1 - o0;
+      } else {
+        for (int o = o0; o < o1; ++o) {
+          int pid = D.segpoly[o];
+          if (na == 0) al.x = pid; else if (na == 1) al.y = pid; else if (na == 2) al.z = pid; else al.w = pid;
+          ++na;
+        }
       }
-      if (o1 - o0 > 4) raise_err(GQ_ERR_CAP);
       C.allow[c] = al; C.nallow[c] = na;
       C.extra[c] = tgt;
     }
@@ -274,6 +278,7 @@ __device__ inline Allow allow_of(const Cand& C, int c) {
   A.n = C.nallow[c];
   int4 a = C.allow[c];
   A.pid[0] = a.x; A.pid[1] = a.y; A.pid[2] = a.z; A.pid[3] = a.w;
+  A.many = A.n > 4 ? C.segpoly + a.x : nullptr;   // a.x holds the offset into the segment's polygon list
   return A;
 }
 

@@ -112,6 +112,9 @@ struct Dev {
   int2* sid_uv;        // original segment endpoints
   uint8_t* vapex;      // input vertex where two input segments meet at < 45 degrees (n_input entries)
   int poly_obl_hull;   // some oblique polygon lies on the convex hull (hull_guard_*, gq_cand.cuh)
+  const int* poly_off; // polygon vertex cycles (CSR), resident for the inside test of non-convex ones
+  const int* poly_idx;
+  uint8_t* poly_convex; // 1: every 2D triangle of the polygon is inside it (no centroid test needed)
   int nsid, npoly;
   double too_close_sq, lmin2;
   Counters* ctr;
@@ -513,7 +516,9 @@ __device__ __noinline__ int walk(const Dev& D, const double* p, int hint) {
 struct Allow {
   int pid[4];
   int n;
+  const int* many;   // n > 4: the segment's polygon list (D.segpoly), pid[] unused
   __device__ bool any() const { return n > 0; }
+  __device__ int at(int k) const { return n <= 4 ? pid[k] : many[k]; }
 };
 __device__ __noinline__ bool allowed_face(const Dev& D, const Allow& A, int a, int b, int c) {
   if (A.n == 0) return false;
@@ -521,7 +526,7 @@ __device__ __noinline__ bool allowed_face(const Dev& D, const Allow& A, int a, i
   int r = face_lookup(D, a, b, c);
   if (r < 0) return false;
   int pid = D.sf_v[r].w;
-  for (int k = 0; k < A.n; ++k) if (A.pid[k] == pid) return true;
+  for (int k = 0; k < A.n; ++k) if (A.at(k) == pid) return true;
   return false;
 }
 __device__ inline bool blocked(const Dev& D, const Allow& A, int t, int i) {

@@ -42,14 +42,16 @@ __device__ __noinline__ void insert_one(const Dev& D, const Cand& C, int c, Scra
   D.vsid[vid] = C.kind[c] == K_SEG ? D.sg_sid[C.tgt[c]] : -1;
   int nitems = 0;
   if (C.kind[c] != K_TET && D.npoly > 0) {
-    int pids[8]; int np = 0;
+    // polygons of the split element: every polygon of the segment (any number), or the subface's
+    int o0 = 0, np = 1, fpid = -1;
     if (C.kind[c] == K_SEG) {
       int sid = D.sg_sid[C.tgt[c]];
-      for (int o = D.segpoly_off[sid]; o < D.segpoly_off[sid + 1] && np < 8; ++o) pids[np++] = D.segpoly[o];
-    } else pids[np++] = D.sf_v[C.tgt[c]].w;
+      o0 = D.segpoly_off[sid]; np = D.segpoly_off[sid + 1] - o0;
+    } else fpid = D.sf_v[C.tgt[c]].w;
+    if (item0 + np > T.icap) { raise_err(GQ_ERR_CAP); np = T.icap - item0; }
     for (int k = 0; k < np; ++k) {
       int w = item0 + k;
-      int pid = pids[k];
+      int pid = fpid >= 0 ? fpid : D.segpoly[o0 + k];
       Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = vid; X.follow3d = D.poly_obl[pid];
       proj2(D, pid, p, X.p);
       int forced[CC + 2]; int nf;
@@ -78,6 +80,7 @@ __device__ __noinline__ void insert_one(const Dev& D, const Cand& C, int c, Scra
         },
         [&](int a, int b, int cc, int) {
           if (collinear_sliver(D, a, b, cc)) return;
+          if (!tri_in_polygon(D, pid, a, b, cc)) return;
           int a0 = a, b0 = b, c0 = cc; sort3(a0, b0, c0);
           if (face_lookup(D, a0, b0, c0) >= 0) return;
           new_face_record(D, a0, b0, c0, pid, RF_LIVE | RF_CHECK);
@@ -254,7 +257,16 @@ __global__ void k_compact_vt(Dev D, const int* remap, const int* flags, int nv) 
 }
 
 // quality (stats.py:35-99): bad count + dihedral histogram of real tets
-__global__ void k_quality(Dev D, double B, unsigned long long* bad, unsigned long long* hist) {
+// Dihedral angles within 1e-11 of a 5-degree bin edge depend on the last bit
+// of acos (CUDA's vs the C library's numpy calls): such tets are listed for the
+// host, which bins them with the reference's own numpy expression
+// (stats.py:64-86), and left out of the device histogram.
+__device__ inline bool bin_edge(double ang) {
+  double x = ang / 5.0;
+  return fabs(x - rint(x)) < 1e-11 * fmax(1.0, x);
+}
+__global__ void k_quality(Dev D, double B, unsigned long long* bad, unsigned long long* hist, int* edge_list,
+                          int edge_cap, int* n_edge) {
   int nt = D.ctr->nt;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
     if (!D.alive[t] || D.tv[t].w == GHOST) continue;
@@ -281,6 +293,8 @@ __global__ void k_quality(Dev D, double B, unsigned long long* bad, unsigned lon
     double ratio = sqrt(r2 / sh);
     if (!isfinite(ratio)) ratio = INFINITY;
     if (ratio > B) atomicAdd(bad, 1ull);
+    int bins[6];
+    bool edge = false;
     for (int e = 0; e < 6; ++e) {
       int i = pr[e][0], j = pr[e][1];
       int kk = -1, ll = -1;
@@ -297,8 +311,14 @@ __global__ void k_quality(Dev D, double B, unsigned long long* bad, unsigned lon
       int bin = (int)(ang / 5.0);
       bin = bin < 0 ? 0 : (bin > 35 ? 35 : bin);
       if (!(ang == ang)) bin = 0;
-      atomicAdd(hist + bin, 1ull);
+      else if (bin_edge(ang)) edge = true;
+      bins[e] = bin;
     }
+    if (edge) {
+      int k = atomicAdd(n_edge, 1);
+      if (k < edge_cap) { edge_list[k] = t; continue; }
+    }
+    for (int e = 0; e < 6; ++e) atomicAdd(hist + bins[e], 1ull);
   }
 }
 

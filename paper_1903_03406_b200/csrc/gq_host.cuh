@@ -226,6 +226,7 @@ static void alloc_scratch(Scr& s, int nthreads, int cap, int tcap, int fcap, cud
 static void alloc_cands(gq_ctx* c, int cap, int bigcap) {
   Cand& C = c->C;
   C.cap = cap;
+  C.segpoly = c->D.segpoly;
   C.kind = dmalloc<int>(cap); C.tgt = dmalloc<int>(cap); C.seed = dmalloc<int>(cap); C.status = dmalloc<int>(cap);
   C.memb = dmalloc<int>(cap); C.pool = dmalloc<int>(cap); C.rank = dmalloc<int>(cap);
   C.allow = dmalloc<int4>(cap); C.nallow = dmalloc<int>(cap); C.extra = dmalloc<int>(cap);
@@ -357,6 +358,9 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   CK(cudaMemsetAsync(D.t2count, 0, std::max(f, 1) * 4, c->st));
   D.poly_keep = dmalloc<int2>(std::max(f, 1));
   D.poly_obl = dmalloc<uint8_t>(std::max(f, 1));
+  D.poly_convex = dmalloc<uint8_t>(std::max(f, 1));
+  CK(cudaMemsetAsync(D.poly_convex, 1, std::max(f, 1), c->st));
+  D.poly_off = nullptr; D.poly_idx = nullptr;
   D.t2last = dmalloc<int>(std::max(f, 1));
   CK(cudaMemsetAsync(D.t2last, 0xff, 4 * (size_t)std::max(f, 1), c->st));
   D.segpoly_off = dmalloc<int>(m + 1);
@@ -423,7 +427,7 @@ static void free_all(gq_ctx* c) {
   Dev& D = c->D;
   void* ps[] = {D.P, D.vorigin, D.vert_tet, D.vsid, D.tv.p, D.alive, D.sub, D.seg, D.skip, D.ratio, D.sg_uv,
                 D.sg_sid, D.sg_fl, D.sg_hk, D.sg_hv, D.sf_v, D.sf_fl, D.sf_hk, D.sf_hv, D.t2v, D.t2alive, D.he_hk,
-                D.he_hv, D.t2count, D.poly_keep, D.poly_obl, D.t2last, D.segpoly_off, D.segpoly, D.sid_uv, D.vapex, D.vp_key, D.vp_val, D.vp_ep, D.vp_stack, D.vp_epoch, D.vp_lock, c->dctr, c->W.own, c->T.cand,
+                D.he_hv, D.t2count, D.poly_keep, D.poly_obl, D.t2last, D.segpoly_off, D.segpoly, D.sid_uv, D.vapex, D.poly_convex, (void*)D.poly_off, (void*)D.poly_idx, D.vp_key, D.vp_val, D.vp_ep, D.vp_stack, D.vp_epoch, D.vp_lock, c->dctr, c->W.own, c->T.cand,
                 c->T.pid, c->T.state, c->T.cav, c->T.ncav, c->T.rem, c->T.nrem, c->T.own, c->L.rows, c->d_int,
                 c->S.tkey, c->S.tval, c->S.tep, c->S.fkey, c->S.fep, c->S.epoch, c->S.list, c->S.stack, c->S.in,
                 c->S.comp, c->SB.tkey, c->SB.tval, c->SB.tep, c->SB.fkey, c->SB.fep, c->SB.epoch, c->SB.list,
@@ -1442,7 +1446,6 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
       }
     }
     for (int s = 0; s < m; ++s) { spo[s + 1] = spo[s] + (int)c->polys[s].size(); for (int p : c->polys[s]) sp.push_back(p); }
-    for (int s = 0; s < m; ++s) if (c->polys[s].size() > 4) throw std::runtime_error("segment shared by more than 4 polygons");
     CK(cudaMemcpyAsync(D.poly_keep, keep, 8 * (size_t)f, cudaMemcpyHostToDevice, c->st));
     std::vector<uint8_t> obl(f, 1);
     for (int pid = 0; pid < f; ++pid)
@@ -1505,12 +1508,13 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
     int* dpo = dmalloc<int>(f + 1); int* dpi = dmalloc<int>(std::max(npidx, 1));
     CK(cudaMemcpyAsync(dpo, poff, 4 * (size_t)(f + 1), cudaMemcpyHostToDevice, c->st));
     CK(cudaMemcpyAsync(dpi, pidx, 4 * (size_t)npidx, cudaMemcpyHostToDevice, c->st));
+    D.poly_off = dpo; D.poly_idx = dpi;        // resident: non-convex polygons' inside test
+    LAUNCH(k_poly_convex, f, D, f);
     LAUNCH_S(k_facets_init, f, D, dpo, dpi, f, c->S, (int*)nullptr);
     sync(c);
     pull(c);
     LAUNCH(k_facets_records, c->hc.nt2, D, c->hc.nt2);
     sync(c);
-    dfree(dpo); dfree(dpi);
   }
   LAUNCH(k_refresh_all, c->hc.nt, D);
   sync(c);

@@ -313,6 +313,7 @@ __global__ void k_facets_records(Dev D, int nt2) {
     if (!D.t2alive[t]) continue;
     int4 q = D.t2v[t];
     if (q.z == GHOST) continue;
+    if (!tri_in_polygon(D, q.w, q.x, q.y, q.z)) continue;   // facets.py:278-291 (non-convex polygons)
     new_face_record(D, q.x, q.y, q.z, q.w, RF_LIVE);
   }
 }

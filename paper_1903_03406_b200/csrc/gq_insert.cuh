@@ -40,6 +40,83 @@ __device__ inline int new_face_record(const Dev& D, int a, int b, int c, int pid
   return r;
 }
 
+// facets.py:278-291 Facet._tri_inside: a 2D triangle of the polygon's
+// triangulation (which covers the convex hull of its vertices) is a subface
+// iff its centroid lies inside or on the polygon (plc.py _point_in_polygon_2d),
+// decided exactly: all coordinates as integers on a common power-of-two
+// scale, the centroid kept as S/3 (S = a + b + c) by multiplying through by 3.
+__device__ __noinline__ bool tri_in_polygon(const Dev& D, int pid, int a, int b, int c) {
+  if (D.poly_convex[pid]) return true;
+  const int o0 = D.poly_off[pid], n = D.poly_off[pid + 1] - o0;
+  int2 kp = D.poly_keep[pid];
+  auto X = [&](int v, int k) { return PT(D, v)[k == 0 ? kp.x : kp.y]; };
+  int emin = 1 << 30;
+  auto upd = [&](double x) { if (x != 0.0) { int e; frexp(x, &e); emin = e < emin ? e : emin; } };
+  for (int k = 0; k < 2; ++k) { upd(X(a, k)); upd(X(b, k)); upd(X(c, k)); }
+  for (int j = 0; j < n; ++j) for (int k = 0; k < 2; ++k) upd(X(D.poly_idx[o0 + j], k));
+  if (emin == (1 << 30)) emin = 0;
+  auto toBI = [&](double x, BI& r) {
+    if (x == 0.0) { bi_zero(r); return; }
+    int e; double m = frexp(x, &e);
+    bi_set(r, (long long)(m * 9007199254740992.0), e - emin);
+  };
+  BI S[2], t, u, three;
+  bi_set(three, 3, 0);
+  for (int k = 0; k < 2; ++k) {
+    BI pa, pb, pc;
+    toBI(X(a, k), pa); toBI(X(b, k), pb); toBI(X(c, k), pc);
+    bi_add(t, pa, pb); bi_add(S[k], t, pc);
+  }
+  bool inside = false;
+  for (int j = 0; j < n; ++j) {
+    int va = D.poly_idx[o0 + j], vb = D.poly_idx[o0 + (j + 1) % n];
+    BI A[2], B[2], A3[2], d[2], w[2];
+    for (int k = 0; k < 2; ++k) {
+      toBI(X(va, k), A[k]); toBI(X(vb, k), B[k]);
+      bi_mul(A3[k], A[k], three);
+      bi_sub(d[k], B[k], A[k]);            // B - A
+      bi_sub(w[k], S[k], A3[k]);           // 3 (q - A)
+    }
+    // on the edge: orient2d(A, B, q) == 0 and 0 <= (q-A).(B-A) <= |B-A|^2 (ends included)
+    BI o1, o2, orr;
+    bi_mul(o1, d[0], w[1]); bi_mul(o2, d[1], w[0]); bi_sub(orr, o1, o2);
+    if (orr.s == 0) {
+      BI dot, l2, p0, p1, l2x3;
+      bi_mul(p0, w[0], d[0]); bi_mul(p1, w[1], d[1]); bi_add(dot, p0, p1);
+      bi_mul(p0, d[0], d[0]); bi_mul(p1, d[1], d[1]); bi_add(l2, p0, p1);
+      bi_mul(l2x3, l2, three);
+      BI diff; bi_sub(diff, l2x3, dot);
+      if (dot.s >= 0 && diff.s >= 0) return true;
+    }
+    // crossing number (ray towards +x): (A.y > q.y) != (B.y > q.y), then xcross > q.x
+    BI B3y; bi_mul(B3y, B[1], three);
+    BI da, db; bi_sub(da, A3[1], S[1]); bi_sub(db, B3y, S[1]);
+    if ((da.s > 0) != (db.s > 0)) {
+      BI m0, m1, N, ax3;
+      bi_sub(ax3, A3[0], S[0]);            // 3 A.x - S.x
+      bi_mul(m0, ax3, d[1]);               // (3Ax - Sx)(By - Ay)
+      bi_mul(m1, w[1], d[0]);              // (Sy - 3Ay)(Bx - Ax)
+      bi_add(N, m0, m1);
+      if (N.s != 0 && N.s == d[1].s) inside = !inside;
+    }
+  }
+  return inside;
+}
+__global__ void k_poly_convex(Dev D, int f) {
+  for (int pid = blockIdx.x * blockDim.x + threadIdx.x; pid < f; pid += gridDim.x * blockDim.x) {
+    const int o0 = D.poly_off[pid], n = D.poly_off[pid + 1] - o0;
+    int2 kp = D.poly_keep[pid];
+    bool convex = true;
+    for (int j = 0; j < n && convex; ++j) {
+      const double *p0 = PT(D, D.poly_idx[o0 + j]), *p1 = PT(D, D.poly_idx[o0 + (j + 1) % n]),
+                   *p2 = PT(D, D.poly_idx[o0 + (j + 2) % n]);
+      double a2[2] = {p0[kp.x], p0[kp.y]}, b2[2] = {p1[kp.x], p1[kp.y]}, c2[2] = {p2[kp.x], p2[kp.y]};
+      convex = orient2d(a2, b2, c2) >= 0;   // counterclockwise in the kept axes (facets.py:262-268)
+    }
+    D.poly_convex[pid] = convex ? 1 : 0;
+  }
+}
+
 __global__ void k_ins_segsplit(Dev D, Cand C, Ins I) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < I.n; k += gridDim.x * blockDim.x) {
     int c = I.list[k];
@@ -187,8 +264,9 @@ __device__ void t2_commit_body(const Dev& D, const Cand& C, const T2Items& T, Sc
           if (nrem < T.rcap) rem[nrem++] = rec; else raise_err(GQ_ERR_CAP);
         }
       },
-      [&](int a, int b, int cc, int t2) {  // added, unless a collinear sliver
+      [&](int a, int b, int cc, int t2) {  // added, unless a collinear sliver or outside the polygon
         if (collinear_sliver(D, a, b, cc)) return;
+        if (!tri_in_polygon(D, pid, a, b, cc)) return;
         int a0 = a, b0 = b, c0 = cc; sort3(a0, b0, c0);
         if (face_lookup(D, a0, b0, c0) >= 0) return;   // never add a key twice
         new_face_record(D, a0, b0, c0, pid, RF_LIVE | RF_CHECK);

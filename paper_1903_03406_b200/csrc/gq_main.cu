@@ -205,21 +205,28 @@ int gq_export_skipped(gq_ctx* c, int32_t* rows) {
   return GQ_OK;
 }
 
-int gq_quality(gq_ctx* c, double B, int64_t* bad_count, int64_t* hist36) {
+int gq_quality(gq_ctx* c, double B, int64_t* bad_count, int64_t* hist36, int32_t* edge_tets, int64_t edge_cap,
+               int64_t* n_edge) {
   if (!c || !c->allocated) return GQ_EINVAL;
   CtxScope scope(c);
   try {
-    unsigned long long* d = dmalloc<unsigned long long>(37);
-    CK(cudaMemsetAsync(d, 0, 37 * 8, c->st));
+    unsigned long long* d = dmalloc<unsigned long long>(38);
+    int cap = (int)std::max<int64_t>(0, std::min<int64_t>(edge_cap, 1 << 28));
+    int* dl = dmalloc<int>(std::max(cap, 1));
+    CK(cudaMemsetAsync(d, 0, 38 * 8, c->st));
     pull(c);
-    k_quality<<<grid_for(c->hc.nt), 128, 0, c->st>>>(c->D, B, d, d + 1);
+    k_quality<<<grid_for(c->hc.nt), 128, 0, c->st>>>(c->D, B, d, d + 1, dl, cap, reinterpret_cast<int*>(d + 37));
     CK(cudaGetLastError());
     sync(c);
-    unsigned long long h[37];
-    d2h(c, h, d, 37 * 8);
-    dfree(d);
+    unsigned long long h[38];
+    d2h(c, h, d, 38 * 8);
+    int ne = (int)(h[37] & 0xffffffffull);
+    if (ne > cap) throw std::runtime_error("quality: bin-edge list overflow");
+    if (edge_tets && ne) d2h(c, edge_tets, dl, 4 * (size_t)ne);
+    dfree(d); dfree(dl);
     if (bad_count) *bad_count = (int64_t)h[0];
     if (hist36) for (int k = 0; k < 36; ++k) hist36[k] = (int64_t)h[1 + k];
+    if (n_edge) *n_edge = ne;
   } catch (std::exception& e) { c->err = e.what(); return GQ_ECUDA; }
   return GQ_OK;
 }

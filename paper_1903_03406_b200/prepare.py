@@ -106,13 +106,7 @@ def facet_keep(plc: PLC) -> np.ndarray:
         if tot < 0:
             i, j = j, i
         out[pid] = (i, j)
-        # the device facet code treats every 2D triangle as inside its polygon,
-        # which holds for convex polygons only (facets.py:278-291): reject others
-        q = [(Fraction(pt[i]), Fraction(pt[j])) for pt in pts]
-        for k in range(n):
-            (ax, ay), (bx, by), (cx, cy) = q[k], q[(k + 1) % n], q[(k + 2) % n]
-            if (bx - ax) * (cy - ay) - (by - ay) * (cx - ax) < 0:
-                from .errors import TetrefineError
-                raise TetrefineError(f"polygon {pid} is not convex (unsupported by the GPU facet path)")
+        # (non-convex polygons: the device keeps a 2D triangle as a subface only
+        # when its centroid is inside the polygon, facets.py:278-291)
     del cache
     return out

@@ -58,7 +58,7 @@ def refine(plc: PLC, cfg: RefineConfig = None, device: int = None, context: _nat
     segs, faces = ctx.export_constraints(cnt)
     rows, secs = ctx.export_rounds(cnt)
     sk = ctx.export_skipped(cnt)
-    bad, hist = ctx.quality(cfg.B)
+    bad, hist, edge_tets = ctx.quality(cfg.B)
     mesh = Mesh(arrays, {(int(u), int(v)): int(s) for u, v, s in segs},
                 {(int(a), int(b), int(c)): int(p) for a, b, c, p in faces}, bbox_diag_of(prep.points))
     rep = QualityReport()
@@ -67,6 +67,9 @@ def refine(plc: PLC, cfg: RefineConfig = None, device: int = None, context: _nat
     rep.steiner_points = int(np.count_nonzero(org == 1))
     rep.tet_count = mesh.n_real_tets()
     rep.bad_tet_count = bad
+    if len(edge_tets):   # bin-edge angles: the reference's own numpy expression (stats.py:64-86)
+        from .stats import dihedral_histogram_of
+        hist = hist + dihedral_histogram_of(mesh.points, mesh.tv[edge_tets])
     rep.dihedral_histogram = [int(x) for x in hist]
     rep.skipped = [{"kind": _KINDS[int(r[0])], "vertices": [int(x) for x in r[3:3 + r[2]]],
                     "reason": _REASONS[int(r[1])]} for r in sk]

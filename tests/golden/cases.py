@@ -5,6 +5,18 @@ import json
 
 from paper_1903_03406_b200 import synth
 
+def _lshape(n: int, seed: int):
+    """Unit cube + n points + one non-convex (L-shaped) hexagon in z = 0.5:
+    the reference keeps only 2D triangles whose centroid is inside it."""
+    from paper_1903_03406_b200 import PLC
+    base = synth.cube_points(n, seed)
+    k = len(base.points)
+    L = [(0.2, 0.2, 0.5), (0.8, 0.2, 0.5), (0.8, 0.5, 0.5), (0.5, 0.5, 0.5), (0.5, 0.8, 0.5), (0.2, 0.8, 0.5)]
+    segs = [(k + i, k + (i + 1) % 6) for i in range(6)]
+    return PLC(points=list(base.points) + L, segments=list(base.segments) + segs,
+               polygons=list(base.polygons) + [tuple(range(k, k + 6))])
+
+
 CASES = {
     # name: (builder, B)
     "cube0": (lambda: synth.cube_points(0, 0), 2.0),
@@ -15,6 +27,7 @@ CASES = {
     "rect600": (lambda: synth.generate(synth.SynthSpec(600, 0.01, "cube", 0)), 1.6),
     "tri500": (lambda: synth.triangles_cloud(500, 5, 0), 1.4),
     "oblique500": (lambda: synth.triangles_cloud(500, 5, 0, snapped=False), 1.6),
+    "lshape400": (lambda: _lshape(400, 5), 1.8),
 }
 
 

@@ -60,7 +60,7 @@ def _refine(plc, B, **kw):
     return refine(plc, RefineConfig(B=B, **kw))
 
 
-@pytest.mark.parametrize("name", ["cube0", "cube100", "cube300", "c1", "seg1000", "rect600", "tri500", "oblique500"])
+@pytest.mark.parametrize("name", ["cube0", "cube100", "cube300", "c1", "seg1000", "rect600", "tri500", "oblique500", "lshape400"])
 def test_refine_matches_reference(gq, golden_dir, name):
     g = np.load(os.path.join(golden_dir, f"refine_{name}.npz"))
     build, B = CASES[name]
