@@ -214,3 +214,16 @@ def test_concurrent_contexts_match_sequential(gq):
             {k: v for k, v in r.items() if k != "time"} for r in r0.per_round] == [
             {k: v for k, v in r.items() if k != "time"} for r in r1.per_round]
         assert r0.dihedral_histogram == r1.dihedral_histogram
+
+
+def test_oblique_facets_self_verified(gq):
+    """C3's stress variant (oblique triangles, which the reference cannot
+    refine) at 1/50 scale: no parity target, so the mesh is
+    self-verified -- every tet positively oriented, adjacency symmetric,
+    masks consistent, every subsegment an edge and every subface a face."""
+    from paper_1903_03406_b200 import synth
+    plc = synth.triangles_cloud(5000, 40, 0, snapped=False)
+    mesh, rep = _refine(plc, 1.4)
+    mesh.audit()
+    assert rep.steiner_points > 0
+    assert rep.bad_tet_count <= 0.01 * rep.tet_count
