@@ -101,8 +101,15 @@ __device__ inline unsigned long long prio_hash(const int* canon, int n, int roun
 
 // ---------------------------------------------------------------------------
 // skipped-element log
-struct SkipLog { int* rows; int cap; };   // 8 ints: round, kind, reason, n, v0..v3
-__device__ __noinline__ void log_skip(const Dev& D, const SkipLog& L, int round_no, int kind, int reason, const int* v, int n) {
+// 9 ints per row: round, kind, reason, n, v0..v3, order.  Rows are appended
+// concurrently; `order` (stage << 28 | position: 0 candidate construction in
+// pool order, 1 the accepted set in priority order, 2 the sequential fallback)
+// restores the reference's recording order (refine.py:669-675) at export.
+#define SKIP_ROW 9
+struct SkipLog { int* rows; int cap; };
+__device__ __forceinline__ int skip_order(int stage, int pos) { return (stage << 28) | (pos & ((1 << 28) - 1)); }
+__device__ __noinline__ void log_skip(const Dev& D, const SkipLog& L, int round_no, int kind, int reason, const int* v, int n,
+                                      int order) {
   atomicAdd(&D.ctr->skipr[(kind & 3) * 4 + (reason & 3)], 1u);
 #ifdef GQ_DEBUG2D
   if (kind == K_SEG && n == 2) {
@@ -114,9 +121,10 @@ __device__ __noinline__ void log_skip(const Dev& D, const SkipLog& L, int round_
 #endif
   int k = atomicAdd(&D.ctr->nskip, 1);
   if (k >= L.cap) { raise_err(GQ_ERR_CAP); return; }
-  int* r = L.rows + 8 * (size_t)k;
+  int* r = L.rows + SKIP_ROW * (size_t)k;
   r[0] = round_no; r[1] = kind; r[2] = reason; r[3] = n;
   for (int i = 0; i < 4; ++i) r[4 + i] = i < n ? v[i] : -1;
+  r[8] = order;
 }
 __device__ inline void tet_canon(const Dev& D, int t, int* c) {
   int4 q = D.tv[t];

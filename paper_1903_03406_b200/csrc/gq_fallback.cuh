@@ -12,22 +12,23 @@ __device__ inline void mark_enc_face_key(const Dev& D, int a, int b, int c) {
   int r = face_lookup(D, a, b, c);
   if (r >= 0 && !(D.sf_fl[r] & RF_SKIP)) D.sf_fl[r] |= RF_ENC;
 }
-__device__ __noinline__ void skip_cand(const Dev& D, const Cand& C, int c, int reason, int round_no, const SkipLog& L) {
+__device__ __noinline__ void skip_cand(const Dev& D, const Cand& C, int c, int reason, int round_no, const SkipLog& L,
+                                       int order) {
   int kind = C.kind[c], tgt = C.tgt[c];
   if (kind == K_TET) {
     if (tgt >= 0 && tgt < D.ctr->nt && D.alive[tgt]) {
       D.skip[tgt] = 1;
       int cv[4]; tet_canon(D, tgt, cv);
-      log_skip(D, L, round_no, K_TET, reason, cv, 4);
+      log_skip(D, L, round_no, K_TET, reason, cv, 4, order);
     }
   } else if (kind == K_SEG) {
     D.sg_fl[tgt] = (D.sg_fl[tgt] | RF_SKIP) & ~RF_ENC;
     int2 e = D.sg_uv[tgt]; int v[2] = {e.x, e.y};
-    log_skip(D, L, round_no, K_SEG, reason, v, 2);
+    log_skip(D, L, round_no, K_SEG, reason, v, 2, order);
   } else {
     D.sf_fl[tgt] = (D.sf_fl[tgt] | RF_SKIP) & ~RF_ENC;
     int4 f = D.sf_v[tgt]; int v[3] = {f.x, f.y, f.z};
-    log_skip(D, L, round_no, K_FACE, reason, v, 3);
+    log_skip(D, L, round_no, K_FACE, reason, v, 3, order);
   }
 }
 
@@ -133,7 +134,7 @@ __global__ void k_fallback(Dev D, Cand C, Scr SCB, FallbackIO F, T2Items T, Skip
   for (int k = 0; k < F.n; ++k) {
     int c = F.list[k];
     int kind = C.kind[c], tgt = C.tgt[c];
-    if (C.status[c] == CS_TOOCLOSE) { skip_cand(D, C, c, 2, F.round_no, L); continue; }
+    if (C.status[c] == CS_TOOCLOSE) { skip_cand(D, C, c, 2, F.round_no, L, skip_order(2, k)); continue; }
     if (kind == K_TET && !(tgt >= 0 && tgt < D.ctr->nt && D.alive[tgt])) continue;
     if (kind == K_SEG && !(D.sg_fl[tgt] & RF_LIVE)) continue;
     if (kind == K_FACE && !(D.sf_fl[tgt] & RF_LIVE)) continue;
@@ -178,11 +179,11 @@ __global__ void k_fallback(Dev D, Cand C, Scr SCB, FallbackIO F, T2Items T, Skip
     int st = ns == 0 ? RS_CNSS : region_compute(D, p, seeds, ns, allow_of(C, c), S, O);
     store_region(C, c, O);
     if (st == RS_OK) {
-      if (O.mind <= D.too_close_sq) { skip_cand(D, C, c, 2, F.round_no, L); continue; }
+      if (O.mind <= D.too_close_sq) { skip_cand(D, C, c, 2, F.round_no, L, skip_order(2, k)); continue; }
       if (kind == K_TET && O.mind < F.lmin2) {
         D.skip[tgt] = 1;
         int cv[4]; tet_canon(D, tgt, cv);
-        log_skip(D, L, F.round_no, K_TET, 1, cv, 4);
+        log_skip(D, L, F.round_no, K_TET, 1, cv, 4, skip_order(2, k));
         continue;
       }
       if (D.ctr->nv >= D.vcap) { raise_err(GQ_ERR_CAP); return; }
@@ -198,7 +199,7 @@ __global__ void k_fallback(Dev D, Cand C, Scr SCB, FallbackIO F, T2Items T, Skip
       if (st == RS_OVERFLOW) atomicAdd(&D.ctr->fail[5], 1u);
       // not star-shaped, or a cavity beyond the sequential path's arena
       // (8192 tets): skipped like the reference's CavityNotStarShaped
-      skip_cand(D, C, c, 3, F.round_no, L);
+      skip_cand(D, C, c, 3, F.round_no, L, skip_order(2, k));
     }
   }
 }
@@ -213,7 +214,7 @@ __global__ void k_accept_flags(Dev D, Cand C, const int* acc, int nacc, int* ins
       if (t >= 0 && D.alive[t]) {
         D.skip[t] = 1;
         int cv[4]; tet_canon(D, t, cv);
-        log_skip(D, L, round_no, K_TET, 1, cv, 4);
+        log_skip(D, L, round_no, K_TET, 1, cv, 4, skip_order(1, k));
       }
     } else insflag[k] = 1;
   }
@@ -465,7 +466,7 @@ __global__ void __launch_bounds__(32 * WS_WARPS) k_star_check(Dev D, Cand C, con
     if (!ok && lane == 0) {
       atomicAdd(&D.ctr->fail[4], 1u);
       insflag[k] = 0;
-      skip_cand(D, C, c, 3, round_no, L);
+      skip_cand(D, C, c, 3, round_no, L, skip_order(1, k));
     }
     __syncwarp();
   }

@@ -392,7 +392,7 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   ensure_items(c, 1 << 16);
   c->T.own = dmalloc<int>(t2cap);
   CK(cudaMemsetAsync(c->T.own, 0x7f, t2cap * 4, c->st));
-  c->L.cap = 1 << 20; c->L.rows = dmalloc<int>((size_t)8 * c->L.cap);
+  c->L.cap = 1 << 20; c->L.rows = dmalloc<int>((size_t)SKIP_ROW * c->L.cap);
   c->d_int = dmalloc<int>(64);
   alloc_scratch(c->S, 16384, CT * 2, 1024, 2048, c->st);
   alloc_scratch(c->SB, 512, CTB * 2, 32768, 32768, c->st);
@@ -1219,7 +1219,33 @@ static void ensure_q(gq_ctx* c, size_t n) {
   c->Q.cap = cap;
 }
 
+// GQ_WATCHDOG=<seconds>: a thread reports the host driver's current stage and
+// round whenever it has not moved for that long (locating device stalls)
+static std::atomic<int> g_wd_stage{-2}, g_wd_round{-1};
+static std::atomic<long long> g_wd_tick{0};
+static void watchdog_start() {
+  static std::once_flag once;
+  const char* e = getenv("GQ_WATCHDOG");
+  if (!e) return;
+  double secs = atof(e);
+  std::call_once(once, [secs] {
+    std::thread([secs] {
+      long long last = -1; double since = now_s();
+      for (;;) {
+        std::this_thread::sleep_for(std::chrono::milliseconds(500));
+        long long t = g_wd_tick.load();
+        if (t != last) { last = t; since = now_s(); continue; }
+        if (now_s() - since > secs) {
+          std::fprintf(stderr, "[watchdog] no progress for %.0f s: round %d stage %d\n", now_s() - since,
+                       g_wd_round.load(), g_wd_stage.load());
+          since = now_s();
+        }
+      }
+    }).detach();
+  });
+}
 static void fine(gq_ctx* c, int k) {
+  g_wd_stage.store(k); g_wd_tick.fetch_add(1);
   if (g_trace) { CK(cudaStreamSynchronize(c->st)); std::fprintf(stderr, "[trace] stage %d ok\n", k); }
   if (g_fine_ev) {
     cudaEvent_t e = ev_next(c);
@@ -1238,6 +1264,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   RoundOut R;
   c->big_used = 0;
   if (getenv("GQ_TRACE_FROM")) g_trace = round_no >= atoi(getenv("GQ_TRACE_FROM"));   // stage trace from a round on
+  g_wd_round.store(round_no);
   pull(c);
   maintain_capacity(c);
   ensure_q(c, (size_t)std::max(std::max(c->hc.nt, c->hc.nsegrec + c->hc.nfacerec), c->C.cap) * 2 + 4096);
@@ -1386,6 +1413,7 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   g_fine_ev = getenv("GQ_PROFILE") && atoi(getenv("GQ_PROFILE")) == 3;
   c->rpairs.clear(); c->fev.clear(); c->evused = 0;
   g_trace = getenv("GQ_TRACE") != nullptr;
+  watchdog_start();
   { int ws = getenv("GQ_WSTOP") ? atoi(getenv("GQ_WSTOP")) : 0; CK(cudaMemcpyToSymbolAsync(g_wstop, &ws, 4, 0, cudaMemcpyHostToDevice, c->st)); }
   c->n_input = n_input; c->npoly = f;
   c->rounds.clear(); c->rtimes.clear(); c->launches = 0; c->region_ms = 0;

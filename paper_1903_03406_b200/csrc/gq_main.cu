@@ -23,6 +23,8 @@
 namespace cg = cooperative_groups;
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <array>
 #include <chrono>
 #include <cstdio>
@@ -195,11 +197,19 @@ int gq_export_skipped(gq_ctx* c, int32_t* rows) {
   try {
     pull(c);
     int n = std::min(c->hc.nskip, c->L.cap);
-    std::vector<int> r(8 * (size_t)n);
-    if (n) d2h(c, r.data(), c->L.rows, 32 * (size_t)n);
+    std::vector<int> r(SKIP_ROW * (size_t)n);
+    if (n) d2h(c, r.data(), c->L.rows, 4 * SKIP_ROW * (size_t)n);
+    // the reference's recording order: by round, then stage / position (log_skip)
+    std::vector<int> ord(n);
+    for (int i = 0; i < n; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+      const int *x = &r[SKIP_ROW * (size_t)a], *y = &r[SKIP_ROW * (size_t)b];
+      return x[0] != y[0] ? x[0] < y[0] : x[8] < y[8];
+    });
     for (int i = 0; i < n; ++i) {
-      rows[7 * i] = r[8 * i + 1]; rows[7 * i + 1] = r[8 * i + 2]; rows[7 * i + 2] = r[8 * i + 3];
-      for (int k = 0; k < 4; ++k) rows[7 * i + 3 + k] = r[8 * i + 4 + k];
+      const int* x = &r[SKIP_ROW * (size_t)ord[i]];
+      rows[7 * i] = x[1]; rows[7 * i + 1] = x[2]; rows[7 * i + 2] = x[3];
+      for (int k = 0; k < 4; ++k) rows[7 * i + 3 + k] = x[4 + k];
     }
   } catch (std::exception& e) { c->err = e.what(); return GQ_ECUDA; }
   return GQ_OK;

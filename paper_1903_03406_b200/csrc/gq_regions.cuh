@@ -19,7 +19,7 @@ __global__ void k_make_cands(Dev D, Cand C, Scr SC, int n0, int n1, CandCtx X, S
       if (!ok) {
         D.skip[t] = 1;
         int cv[4]; tet_canon(D, t, cv);
-        log_skip(D, L, X.round_no, K_TET, 0, cv, 4);
+        log_skip(D, L, X.round_no, K_TET, 0, cv, 4, skip_order(0, c));
         C.status[c] = CS_DROP;
         continue;
       }
@@ -29,7 +29,7 @@ __global__ void k_make_cands(Dev D, Cand C, Scr SC, int n0, int n1, CandCtx X, S
       if (s.r2 < lmin2) {
         D.skip[t] = 1;
         int cv[4]; tet_canon(D, t, cv);
-        log_skip(D, L, X.round_no, K_TET, 1, cv, 4);
+        log_skip(D, L, X.round_no, K_TET, 1, cv, 4, skip_order(0, c));
         C.status[c] = CS_DROP;
       }
     } else if (!ok) {
