@@ -624,6 +624,16 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   fine(c, 26);
 }
 
+// Contexts alive on each device.  A cooperative launch needs all its blocks
+// resident at once; with several contexts running concurrently (C5) each one
+// sizes its grid to its share of the device, so the cooperative grids of all
+// of them fit together (their loops are grid-stride, any size is correct).
+static std::atomic<int> g_ctx_count[64];
+static int coop_share(gq_ctx* c, int full) {
+  int k = std::max(1, g_ctx_count[c->device & 63].load());
+  return std::max(1, full / k);
+}
+
 // candidates sorted by priority (class rank, hash, canonical tuple); smaller
 // first (refine.py:45-52).  Two radix passes order by (class, hash); a run of
 // equal (class, hash) -- a 64-bit splitmix collision -- is then put in
@@ -686,7 +696,7 @@ static void run_filter(gq_ctx* c, int n, int* nacc_out) {
       CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
       if (blocks_per_sm < 1) throw std::runtime_error("filter kernel cannot be resident");
     }
-    int blocks = std::min(blocks_per_sm * nsm, (n + 7) / 8);
+    int blocks = std::min(coop_share(c, blocks_per_sm * nsm), (n + 7) / 8);
     int* ctr = c->d_int + 48;
     CK(cudaMemsetAsync(ctr, 0, 12, c->st));
     void* args[] = {&c->D, &c->C, &c->W, &n, &ctr};
@@ -964,7 +974,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
         CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
         if (bps < 1) throw std::runtime_error("init filter kernel cannot be resident");
       }
-      int blocks = std::max(1, std::min(bps * nsm, (W + 7) / 8));
+      int blocks = std::max(1, std::min(coop_share(c, bps * nsm), (W + 7) / 8));
       int* tot = c->d_int + 52;
       void* args[] = {&c->D, &C, &c->W, &d_plist, &W, &nt, &d_acc, &d_plist2, &d_scan, &tot, &d_succ};
       CK(cudaLaunchCooperativeKernel((void*)k_init_filter_coop, dim3(blocks), dim3(256), args, 0, c->st));

@@ -63,6 +63,7 @@ extern "C" {
 int gq_create(int device, gq_ctx** out) {
   if (!out) return GQ_EINVAL;
   gq_ctx* c = new gq_ctx();
+  g_ctx_count[device & 63].fetch_add(1);
   try {
     c->device = device;
     CK(cudaSetDevice(device));
@@ -111,6 +112,7 @@ int gq_destroy(gq_ctx* c) {
     { DevCache& C = dev_cache(); std::lock_guard<std::mutex> g(C.mu); cache_trim(C); }
     if (c->st) cudaStreamDestroy(c->st);
   } catch (...) {}
+  g_ctx_count[c->device & 63].fetch_sub(1);
   delete c;
   return GQ_OK;
 }
