@@ -29,12 +29,14 @@ def up_to_date() -> bool:
 SO_DBG = os.path.join(HERE, "libgqm3d_dbg.so")   # diagnostics build: device error sites printed (GQM3D_LIB=...)
 
 
-def build(force: bool = False, verbose: bool = True, debug: bool = False) -> str:
-    so = SO_DBG if debug else SO
+def build(force: bool = False, verbose: bool = True, debug: bool = False, variant: str = None, defines=()) -> str:
+    """variant/defines: experiment builds (libgqm3d_<variant>.so with -D flags), never the product library."""
+    so = SO_DBG if debug else (os.path.join(HERE, f"libgqm3d_{variant}.so") if variant else SO)
     if not force and os.path.exists(so) and all(os.path.getmtime(d) <= os.path.getmtime(so) for d in DEPS):
         return so
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, *(["-DGQ_DEBUG2D"] if debug else []), "-o", so + ".tmp", SRC, SRC_IO]
+    cmd = [nvcc, *NVCC_FLAGS, *(["-DGQ_DEBUG2D"] if debug else []), *[f"-D{d}" for d in defines],
+           "-o", so + ".tmp", SRC, SRC_IO]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
@@ -43,4 +45,6 @@ def build(force: bool = False, verbose: bool = True, debug: bool = False) -> str
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, debug="--debug" in sys.argv)
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), None)
+    build(force="--force" in sys.argv, debug="--debug" in sys.argv, variant=var, defines=args)

@@ -149,6 +149,17 @@ __device__ __noinline__ int scaled(const double* x, int n, BI* out) {
     if (x[i] != 0.0) { int e; frexp(x[i], &e); emin = e < emin ? e : emin; }
   }
   if (emin == (1 << 30)) emin = 0;
+#ifdef GQ_DEBUG2D
+  {
+    int emax = -(1 << 30);
+    for (int i = 0; i < n; ++i) if (x[i] != 0.0) { int e; frexp(x[i], &e); emax = e > emax ? e : emax; }
+    if (emax - emin > 120) {
+      printf("[bigspread] n %d spread %d:", n, emax - emin);
+      for (int i = 0; i < n; ++i) printf(" %.17g", x[i]);
+      printf("\n");
+    }
+  }
+#endif
   for (int i = 0; i < n; ++i) {
     if (x[i] == 0.0) { bi_zero(out[i]); continue; }
     int e;

@@ -539,7 +539,7 @@ static void run_huge_regions(gq_ctx* c, const std::vector<int>& big) {
     d2h(c, hs.data(), c->tmpA, 4 * (size_t)nh);
     int still = 0;
     for (int k = 0; k < nh; ++k) still += hs[k] == CS_OVF;
-    if (g_trace) std::fprintf(stderr, "[huge] %d cavities, capacity %d tets, %d overflow\n", nh, mcap, still);
+    if (g_trace || c->verbose) std::fprintf(stderr, "[huge] %d cavities, capacity %d tets, %d overflow\n", nh, mcap, still);
     if (still == 0) return;
     if (mcap >= (1 << 22)) {   // give up on these: failed candidates (the fallback skips them)
       LAUNCH(k_set_status, nh, c->C, c->hlist, nh, CS_OVF, CS_CNSS);
@@ -611,6 +611,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
     double tb = now_s();
     run_huge_regions(c, big);
     sync(c);
+    if (c->verbose && now_s() - tb > 0.5) std::fprintf(stderr, "[big] %d oversized cavities took %.2f s\n", nb, now_s() - tb);
     if (g_trace) {
       std::vector<int> nts(nb);
       int mx = 0; long long sm = 0;
