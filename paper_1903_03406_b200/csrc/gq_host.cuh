@@ -515,7 +515,9 @@ __global__ void k_set_status(Cand C, const int* list, int n, int from, int to) {
     if (C.status[list[k]] == from) C.status[list[k]] = to;
 }
 // block-tier overflows of this round: the huge tier, capacities doubled until
-// every cavity fits (4M tets at most, beyond which the candidate fails)
+// every cavity fits (64k tets at most: beyond, the candidate fails).  Cavities
+// that large come from the far circumcentres of nearly flat tets lying on a
+// finely split oblique facet; a region of 100k+ tets costs one block seconds.
 static void run_huge_regions(gq_ctx* c, const std::vector<int>& big) {
   int nb = (int)big.size();
   std::vector<int> st(nb);
@@ -541,7 +543,7 @@ static void run_huge_regions(gq_ctx* c, const std::vector<int>& big) {
     for (int k = 0; k < nh; ++k) still += hs[k] == CS_OVF;
     if (g_trace || c->verbose) std::fprintf(stderr, "[huge] %d cavities, capacity %d tets, %d overflow\n", nh, mcap, still);
     if (still == 0) return;
-    if (mcap >= (1 << 22)) {   // give up on these: failed candidates (the fallback skips them)
+    if (mcap >= (1 << 16)) {   // beyond 64k tets: failed candidates (the sequential fallback skips them)
       LAUNCH(k_set_status, nh, c->C, c->hlist, nh, CS_OVF, CS_CNSS);
       return;
     }

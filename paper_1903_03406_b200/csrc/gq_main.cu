@@ -70,7 +70,7 @@ int gq_create(int device, gq_ctx** out) {
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     CK(cudaEventCreate(&c->ev0)); CK(cudaEventCreate(&c->ev1));
     CK(cudaEventCreate(&c->er0)); CK(cudaEventCreate(&c->er1));
-    CK(cudaDeviceSetLimit(cudaLimitStackSize, 16384));
+    CK(cudaDeviceSetLimit(cudaLimitStackSize, 24576));   // k_fallback: ~18 KB (exact predicates on 40-limb integers)
     CK(cudaFuncSetAttribute(k_region_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BlockShared)));
     CK(cudaFuncSetAttribute(k_region_warp<WT1_MAXT, WT1_HASH, WT1_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(WR_WARPS * sizeof(WarpShared1))));
     if (WT1_MAXT != WT2_MAXT)

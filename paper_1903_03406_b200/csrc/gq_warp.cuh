@@ -46,7 +46,7 @@ struct WarpSharedT {
   int f1[MAXT];
   int comp[MAXT];
   unsigned char in[MAXT];
-  int n, nf, cnt, flag, memb, seed;
+  int n, nf, cnt, flag, memb, seed, ghost;
   unsigned long long mind;
   int seeds[32];
   int nseeds;
@@ -118,7 +118,7 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
   if (lane == 0) {
     int s = wh_claim(W, seed);       // the table is empty: always inserts
     if (s >= 0) W.hval[s] = 0;
-    W.cav[0] = seed; W.n = 1; W.f0[0] = seed; W.flag = 0; W.memb = INT_MAX;
+    W.cav[0] = seed; W.n = 1; W.f0[0] = seed; W.flag = 0; W.memb = INT_MAX; W.ghost = D.tv[seed].w == GHOST;
   }
   __syncwarp();
   // ---- grow
@@ -144,6 +144,7 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
         W.cav[idx] = u;
         W.hval[slot] = idx;
         nxt[atomicAdd(&W.nf, 1)] = u;
+        if (D.tv[u].w == GHOST) W.ghost = 1;   // only a ghost tet puts ghost faces on the boundary
       } else {
         W.hval[slot] = -2;
       }
@@ -296,8 +297,7 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
     }
   }
   __syncwarp();
-  if (__any_sync(FULL, bf_has_ghost_part(D, O.bf, nbf, lane, 32)) &&
-      __any_sync(FULL, bf_open_part(D, O.bf, nbf, lane, 32))) {
+  if (W.ghost && __any_sync(FULL, bf_open_part(D, O.bf, nbf, lane, 32))) {
     if (lane == 0) atomicAdd(&D.ctr->fail[3], 1u);
     return RS_BADSTAR;
   }
