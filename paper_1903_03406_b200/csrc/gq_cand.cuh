@@ -239,6 +239,20 @@ __device__ __noinline__ bool make_cand(const Dev& D, const Cand& C, int c, const
     Sphere s;
     if (circumsphere_tet(PT(D, q.x), PT(D, q.y), PT(D, q.z), PT(D, q.w), s) != 0) return false;
     p[0] = s.c[0]; p[1] = s.c[1]; p[2] = s.c[2];
+    // A nearly flat tet can put its circumcentre at 1e40: far outside the hull,
+    // where only the direction of the hull-exit walk matters (refine.py:378-413),
+    // while the exact predicates' integers grow with the exponent spread.  Such a
+    // point is pulled in along the same ray to 1000 bounding-box diagonals.
+    {
+      double diag = sqrt(D.lmin2) * 1e4, R = 1e3 * diag;
+      const double *a = PT(D, q.x), *b = PT(D, q.y), *c3 = PT(D, q.z), *d = PT(D, q.w);
+      double ctr[3], dv[3], l2 = 0;
+      for (int k = 0; k < 3; ++k) { ctr[k] = 0.25 * (a[k] + b[k] + c3[k] + d[k]); dv[k] = p[k] - ctr[k]; l2 += dv[k] * dv[k]; }
+      if (l2 > R * R) {
+        double f = R / sqrt(l2);
+        for (int k = 0; k < 3; ++k) p[k] = ctr[k] + dv[k] * f;
+      }
+    }
   } else if (kind == K_SEG) {
     int2 e = D.sg_uv[tgt];
     canon[0] = e.x; canon[1] = e.y; nc = 2;

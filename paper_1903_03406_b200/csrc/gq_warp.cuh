@@ -110,7 +110,23 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
     __syncwarp();
     seed = W.seed;
     WMARK(50);
-    if (seed < 0) { if (lane == 0) atomicAdd(&D.ctr->fail[0], 1u); return RS_CNSS; }
+    if (seed < 0) {
+      if (lane == 0) {
+        unsigned k = atomicAdd(&D.ctr->fail[0], 1u);
+#ifdef GQ_DEBUG2D
+        if (k < 40) {
+          int t0s = seeds[0];
+          int4 q = D.tv[t0s];
+          printf("[noseed] k %u nseeds %d p %.17g %.17g %.17g seed0 %d alive %d tv %d %d %d %d walk %d insph %d\n", k, nseeds,
+                 p[0], p[1], p[2], t0s, (int)D.alive[t0s], q.x, q.y, q.z, q.w, W.seed,
+                 q.w == GHOST ? -9 : insphere(PT(D, q.x), PT(D, q.y), PT(D, q.z), PT(D, q.w), p));
+        }
+#else
+        (void)k;
+#endif
+      }
+      return RS_CNSS;
+    }
   }
   O.seed = seed;
   WSTOP(1);
@@ -189,7 +205,21 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
     WMARK(50);
     const bool shrunk = !W.in[0];
     __syncwarp();
-    if (shrunk) { if (lane == 0) atomicAdd(&D.ctr->fail[1], 1u); return RS_CNSS; }   // seed shrunk away
+    if (shrunk) {   // seed shrunk away
+      if (lane == 0) {
+        unsigned k = atomicAdd(&D.ctr->fail[1], 1u);
+#ifdef GQ_DEBUG2D
+        if (k < 40) {
+          int4 q = D.tv[seed];
+          printf("[peeled] k %u n %d p %.17g %.17g %.17g seed %d tv %d %d %d %d nseeds %d\n", k, n, p[0], p[1], p[2], seed,
+                 q.x, q.y, q.z, q.w, nseeds);
+        }
+#else
+        (void)k;
+#endif
+      }
+      return RS_CNSS;
+    }
     for (int k = lane; k < n; k += 32) W.comp[k] = 0;
     __syncwarp();
     if (lane == 0) { W.comp[0] = 1; W.f0[0] = 0; W.cnt = 1; }
