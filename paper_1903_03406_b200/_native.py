@@ -64,10 +64,12 @@ def lib():
         L.gq_quality.argtypes = [vp, ctypes.c_double, vp, vp, vp, ctypes.c_int64, vp]
         L.gq_batch.argtypes = [ctypes.c_int, vp, i32, i32, vp, vp]
         L.gq_write_mesh.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, vp, vp, i32, vp, vp, i32, vp, i32]
-        L.gq_probe_fp64.argtypes = [ctypes.c_int, vp]
-        L.gq_certify_pairs.argtypes = [ctypes.c_int, vp, i32, vp, i32, vp, i32, vp, vp, ctypes.c_int64, vp]
+        if hasattr(L, "gq_probe_fp64"):        # (an older library in GQM3D_LIB may lack the newer entry points)
+            L.gq_probe_fp64.argtypes = [ctypes.c_int, vp]
+        if hasattr(L, "gq_certify_pairs"):
+            L.gq_certify_pairs.argtypes = [ctypes.c_int, vp, i32, vp, i32, vp, i32, vp, vp, ctypes.c_int64, vp]
         for name in EXPORTS:
-            if name not in ("gq_last_error",):
+            if name not in ("gq_last_error",) and hasattr(L, name):
                 getattr(L, name).restype = ctypes.c_int
         _LIB = L
     return _LIB

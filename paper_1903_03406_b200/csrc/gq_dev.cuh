@@ -551,7 +551,8 @@ __device__ __noinline__ bool in_region(const Dev& D, int t, const double* p, con
 
 // ---------------------------------------------------------------------------
 // Delaunay region (mesh.py:450-521, decisions of _kernels.py:392-635)
-enum RegionStatus { RS_OK = 0, RS_CNSS = 1, RS_MEMBRANE = 2, RS_OVERFLOW = 3, RS_TOOCLOSE = 4, RS_BADSTAR = 5 };
+enum RegionStatus { RS_OK = 0, RS_CNSS = 1, RS_MEMBRANE = 2, RS_OVERFLOW = 3, RS_TOOCLOSE = 4, RS_BADSTAR = 5,
+                    RS_SHRUNK = 6 /* internal: seed peeled, retry with the next seed */ };
 
 // Star validation before anything is written.  The peel makes every real
 // boundary face strictly visible from p, so a cavity of real tets always

@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_region_warp(Dev D, Cand
     DCHK(ns >= 0 && ns <= 32);
     SlabView v = slab(C, c);
     RegionOut O = region_view(C, c, v, 0);
-    int st = ns == 0 ? RS_CNSS : region_warp(D, C.p + 3 * (size_t)c, W.seeds, ns, allow_of(C, c), W, S, O);
+    int st = ns == 0 ? RS_CNSS : region_warp_retry(D, C.p + 3 * (size_t)c, W.seeds, ns, allow_of(C, c), W, S, O);
     if (lane == 0) {
       atomicAdd(&D.ctr->region_calls, 1ull);
       store_region(C, c, O);

@@ -46,7 +46,7 @@ struct WarpSharedT {
   int f1[MAXT];
   int comp[MAXT];
   unsigned char in[MAXT];
-  int n, nf, cnt, flag, memb, seed, ghost;
+  int n, nf, cnt, flag, memb, seed, ghost, seedk;
   unsigned long long mind;
   int seeds[32];
   int nseeds;
@@ -87,7 +87,8 @@ __device__ inline int wh_find(const WS& W, int k) {
 // warp's global scratch (lane 0 only: walks and the constraint pass).
 template <int MAXT, int HASH>
 __device__ inline int region_warp(const Dev& D, const double* p, const int* seeds, int nseeds, const Allow& A,
-                                  WarpSharedT<MAXT, HASH>& W, Scratch& S, RegionOut& O, bool walk_on_miss = true) {
+                                  WarpSharedT<MAXT, HASH>& W, Scratch& S, RegionOut& O, bool walk_on_miss = true,
+                                  unsigned excl = 0u, bool may_retry = false) {
   constexpr int WR_MAXT = MAXT, WR_HASH = HASH;
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
@@ -97,9 +98,11 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
   int nc = nseeds < 32 ? nseeds : 32;
   int t0 = lane < nc ? seeds[lane] : -1;
   DCHK(t0 < D.tcap);
-  bool ok = t0 >= 0 && D.alive[t0] && in_region(D, t0, p, A);
+  bool ok = t0 >= 0 && !((excl >> lane) & 1u) && D.alive[t0] && in_region(D, t0, p, A);
   unsigned bal = __ballot_sync(FULL, ok);
   int seed = bal ? __shfl_sync(FULL, t0, __ffs(bal) - 1) : -1;
+  if (lane == 0) W.seedk = bal ? __ffs(bal) - 1 : -1;   // which listed seed (region_warp_retry)
+  if (seed < 0 && excl) return RS_CNSS;                 // a retry with no further seed
   if (seed < 0) {
     WMARK(50);
     if (!walk_on_miss) return RS_CNSS;
@@ -206,6 +209,7 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
     const bool shrunk = !W.in[0];
     __syncwarp();
     if (shrunk) {   // seed shrunk away
+      if (may_retry && W.seedk >= 0 && D.poly_obl_hull) return RS_SHRUNK;   // the caller may retry
       if (lane == 0) {
         unsigned k = atomicAdd(&D.ctr->fail[1], 1u);
 #ifdef GQ_DEBUG2D
@@ -474,6 +478,28 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
   O.ncr = ncr; O.nbsub = nbs; O.nbseg = nbg; O.neseg = neg;
   __syncwarp();
   WMARK(60);
+  return st;
+}
+
+// The peel can remove the seed itself: on a finely split oblique surface the
+// listed seed may be a nearly flat tet spanning two facet triangles whose
+// faces p sees edge-on.  The reference then fails the candidate
+// (_kernels.py region_kernel -> CavityNotStarShaped).  With oblique facets
+// present (none of the parity inputs has one) the next listed seed in region
+// is tried instead, up to three times; the peel is seed-independent, so a
+// surviving seed yields the star-shaped cavity around p.
+template <int MAXT, int HASH>
+__device__ inline int region_warp_retry(const Dev& D, const double* p, const int* seeds, int nseeds, const Allow& A,
+                                        WarpSharedT<MAXT, HASH>& W, Scratch& S, RegionOut& O) {
+  unsigned excl = 0u;
+  int st = RS_CNSS;
+  for (int a = 0; a < 4; ++a) {
+    st = region_warp(D, p, seeds, nseeds, A, W, S, O, true, excl, a < 3);
+    if (st != RS_SHRUNK) break;
+    excl |= 1u << W.seedk;
+    __syncwarp();
+  }
+  if (st == RS_SHRUNK) st = RS_CNSS;
   return st;
 }
 
