@@ -283,7 +283,7 @@ __device__ __noinline__ int first_alive_with(const Dev& D, int v) {
 // Returns 1 done (or stopped by f), 0 no alive tet, -1 the set or the stack
 // overflowed (nothing is lost: the caller reruns with a larger arena).
 template <class F>
-__device__ inline int around_vertex_try(const Dev& D, int v, ISet& seen, int* stack, int cap, F& f) {
+__device__ __noinline__ int around_vertex_try(const Dev& D, int v, ISet& seen, int* stack, int cap, F& f) {
   int start = D.vert_tet[v];
   if (start < 0 || start >= D.ctr->nt || !D.alive[start] || !has_v(D.tv[start], v)) {
     start = first_alive_with(D, v);

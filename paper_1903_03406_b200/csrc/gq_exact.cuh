@@ -17,7 +17,7 @@
 #include <cuda_runtime.h>
 
 #ifndef GQ_BI_LIMBS
-#define GQ_BI_LIMBS 40     // 1280 bits: insphere with a 200-bit exponent spread (far circumcentres)
+#define GQ_BI_LIMBS 30     // 960 bits (far circumcentres are pulled in first, make_cand)
 #endif
 
 namespace gq {

@@ -375,6 +375,14 @@ __global__ void k_redirect(Dev D, Cand C, int n0, int n1, int* nredir) {
         atomicOr(D.sf_fl + hull, RF_REDIR);
         atomicAdd(nredir + 1, 1);
         C.status[c] = CS_DROP;
+      } else if (hull != -2) {
+        // The circumcentre is outside the hull but the hull face it leaves
+        // through is not (yet) a live subface -- a hull subface missing from
+        // the mesh (recovered by the face phase) or skipped.  The reference
+        // would insert the point (refine.py:648-654) and move the domain's
+        // hull outward; it never meets the case on its inputs, whose hull
+        // faces (box / cube) are always present.  Here the candidate waits.
+        C.status[c] = CS_DROP;
       }
     }
   }

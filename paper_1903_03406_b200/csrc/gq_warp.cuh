@@ -493,6 +493,7 @@ __device__ inline int region_warp_retry(const Dev& D, const double* p, const int
                                         WarpSharedT<MAXT, HASH>& W, Scratch& S, RegionOut& O) {
   unsigned excl = 0u;
   int st = RS_CNSS;
+#pragma unroll 1
   for (int a = 0; a < 4; ++a) {
     st = region_warp(D, p, seeds, nseeds, A, W, S, O, true, excl, a < 3);
     if (st != RS_SHRUNK) break;
