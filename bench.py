@@ -3,12 +3,15 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gqm3d|reference]
                     [--config C4|C2|C5|C1|C3] [--scale S]
 
-Workload (default C4, the north-star target of BASELINE.json): outer icosphere
-r=1 + inner icosphere r=0.45 (level 6, 81,920 triangles each) + torus R=0.72
-r=0.12 (40,000 triangles) + 1,000,000 uniform points in the unit ball, B=1.5
-(SURVEY.md 8(d)).  One step = one complete refine of that PLC.  C2 (BASELINE
-configs[1], the largest configuration the reference itself can refine) and the
-others are selectable with --config.
+Workload (default C2, BASELINE configs[1]: the configuration the metric is
+quoted on and the largest one the reference itself refines): 100,000 uniform
+points + 1,000 random segments in the unit cube, B=1.6.  One step = one
+complete refine of that PLC.  The north-star PLC C4 (outer icosphere r=1 +
+inner icosphere r=0.45, level 6, 81,920 triangles each, + torus R=0.72 r=0.12,
+40,000 triangles, + 1,000,000 points in the unit ball, B=1.5) is measured in
+the same run under "north_star" (one refine capped at --north-star-rounds
+rounds, the reference's own max_rounds knob) and selectable as the workload
+with --config C4; C5 (the 64-PLC batch) with --config C5.
 
 * value     Steiner/s with the PLC prepared and uploaded: GPU time of gq_refine
             (CUDA events on the context's stream, bulk Delaunay construction
@@ -217,13 +220,41 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def north_star(ctx, rounds: int, eq_rounds: int):
+    """One C4 refine (the north-star PLC) with a round cap, device-timed, plus
+    the same PLC stopped at the reference arm's equal-rounds cap."""
+    from paper_1903_03406_b200.prepare import facet_keep, prepare
+    from paper_1903_03406_b200 import synth
+    B = CONFIGS["C4"][0]
+    t0 = time.perf_counter()
+    plc = synth.config_plc("C4")
+    prep = prepare(plc, seed=0)
+    keep = facet_keep(prep.plc)
+    setup = time.perf_counter() - t0
+    cnt = ctx.refine(prep, keep, B, rounds, 0)
+    eq = ctx.refine(prep, keep, B, eq_rounds, 0)
+    return {"workload": f"C4: {CONFIGS['C4'][1]}", "B": B, "max_rounds": rounds, "rounds": int(cnt.n_rounds),
+            "steiner": int(cnt.steiner_points), "vertices": int(cnt.nv), "tet_slots": int(cnt.nt),
+            "device_s": cnt.device_ms / 1000.0, "value": int(cnt.steiner_points) / (cnt.device_ms / 1000.0),
+            "unit": "steiner_points/s", "host_setup_s": setup,
+            "equal_rounds": {"rounds": int(eq.n_rounds), "steiner": int(eq.steiner_points),
+                             "device_s": eq.device_ms / 1000.0,
+                             "value": int(eq.steiner_points) / (eq.device_ms / 1000.0),
+                             "reference_port": "34,960 Steiner in 190.8 s over the same 2 rounds on one core of the "
+                                               "build container (183 Steiner/s; profiles/r02_summary.md)"},
+            "note": "one device-timed refine per bench run; the full refine does not reach a fixed point within "
+                    "the reference's default 500 rounds (DESIGN.md section 7)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gqm3d", choices=["gqm3d", "reference"])
-    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--north-star-rounds", type=int, default=60,
+                    help="C2/C5 runs: also refine C4 once with this round cap (0: skip)")
     ap.add_argument("--scale", type=float, default=1.0, help="workload scale (1.0 = the BASELINE config)")
     ap.add_argument("--max-rounds", type=int, default=500)
     ap.add_argument("--e2e-steps", type=int, default=3, help="end-to-end refines timed (<= --steps)")
@@ -402,6 +433,8 @@ def main():
                                     "device_s": cnt.device_ms / 1000.0,
                                     "value": int(cnt.steiner_points) / (cnt.device_ms / 1000.0),
                                     "note": "GPU refine stopped after the reference arm's round cap (--ref-rounds)"}
+        if args.config != "C4" and args.north_star_rounds > 0 and world == 1:
+            line["north_star"] = north_star(ctx, args.north_star_rounds, args.ref_rounds)
         if not args.no_cpu_baseline and world == 1:
             cb = cpu_sample(args.config, args.cpu_budget_s)
             line["cpu_baseline"] = cb if cb else {

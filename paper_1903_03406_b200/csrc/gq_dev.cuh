@@ -36,6 +36,8 @@ struct Counters {
   int nskip;
   int ncand;
   int pad;
+  int line_pad[24];                  // the hot counts above own their 128-byte line (the
+                                     // instrumentation atomics below must not share it)
   // instrumentation (SURVEY 8(d) algorithmic bytes), per context
   unsigned long long region_calls;   // region computations
   unsigned long long tested;         // tets tested for membership (cavity + boundary neighbours)

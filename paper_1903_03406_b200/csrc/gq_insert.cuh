@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(32 * WS_WARPS) k_star_warp(Dev D, Cand C, Ins 
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   StarShared& X = reinterpret_cast<StarShared*>(smem_raw)[wib];
   const int gw = blockIdx.x * WS_WARPS + wib, nw = gridDim.x * WS_WARPS;
+  unsigned long long n_created = 0, n_deleted = 0;
   for (int k = gw; k < I.n; k += nw) {
     int c = I.list[k];
     SlabView v = slab(C, c);
@@ -376,9 +377,10 @@ __global__ void __launch_bounds__(32 * WS_WARPS) k_star_warp(Dev D, Cand C, Ins 
     if (nbf <= WS_MAXF) star_warp(D, C.vid[c], v.bf, nbf, C.nt0[c], true, star_hash_shared(X), nullptr, 0);
     else if (C.bigi[c] >= HUGE_BASE) star_warp(D, C.vid[c], v.bf, nbf, C.nt0[c], true, huge_star_hash(C, c, &X.flag), nullptr, 0);
     else star_warp(D, C.vid[c], v.bf, nbf, C.nt0[c], true, big_star_hash(SB, gw, &X.flag), nullptr, 0);
-    if (lane == 0) { atomicAdd(&D.ctr->created, (unsigned long long)nbf); atomicAdd(&D.ctr->deleted, (unsigned long long)C.ntet[c]); }
+    if (lane == 0) { n_created += nbf; n_deleted += C.ntet[c]; }
     __syncwarp();
   }
+  if (lane == 0 && n_created) { atomicAdd(&D.ctr->created, n_created); atomicAdd(&D.ctr->deleted, n_deleted); }
 }
 __global__ void __launch_bounds__(32 * WS_WARPS) k_init_stars_warp(Dev D, Cand C, const int* pend, const int* plist,
                                                                    const int* acc, int nw_, int* touched, int round, Scr SB) {
@@ -386,6 +388,7 @@ __global__ void __launch_bounds__(32 * WS_WARPS) k_init_stars_warp(Dev D, Cand C
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   StarShared& X = reinterpret_cast<StarShared*>(smem_raw)[wib];
   const int gw = blockIdx.x * WS_WARPS + wib, nw = gridDim.x * WS_WARPS;
+  unsigned long long n_created = 0, n_deleted = 0;
   for (int w = gw; w < nw_; w += nw) {
     if (!acc[w]) continue;
     int c = plist[w];
@@ -393,10 +396,11 @@ __global__ void __launch_bounds__(32 * WS_WARPS) k_init_stars_warp(Dev D, Cand C
     int nbf = C.nbf[c];
     if (nbf <= WS_MAXF) star_warp(D, pend[c], v.bf, nbf, C.nt0[c], true, star_hash_shared(X), touched, round);
     else star_warp(D, pend[c], v.bf, nbf, C.nt0[c], true, big_star_hash(SB, gw, &X.flag), touched, round);
-    if (lane == 0) { atomicAdd(&D.ctr->created, (unsigned long long)nbf); atomicAdd(&D.ctr->deleted, (unsigned long long)C.ntet[c]); }
+    if (lane == 0) { n_created += nbf; n_deleted += C.ntet[c]; }
     __syncwarp();
     if (lane == 0) C.status[c] = CS_DROP;
   }
+  if (lane == 0 && n_created) { atomicAdd(&D.ctr->created, n_created); atomicAdd(&D.ctr->deleted, n_deleted); }
 }
 
 // dirty constraints + survivor mask refresh for subfaces retiled in 2D but

@@ -9,10 +9,11 @@
 __global__ void k_make_cands(Dev D, Cand C, Scr SC, int n0, int n1, CandCtx X, SkipLog L, double lmin2) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   Scratch S = scratch_for(SC, tid);
+  unsigned long long n_cands = 0;
   for (int c = n0 + tid; c < n1; c += gridDim.x * blockDim.x) {
     C.status[c] = CS_OK;
     C.bigi[c] = -1;
-    atomicAdd(&D.ctr->cands, 1ull);
+    ++n_cands;
     bool ok = make_cand(D, C, c, X, S);
     if (C.kind[c] == K_TET) {
       int t = C.tgt[c];
@@ -37,6 +38,7 @@ __global__ void k_make_cands(Dev D, Cand C, Scr SC, int n0, int n1, CandCtx X, S
       C.status[c] = CS_DROP;
     }
   }
+  if (n_cands) atomicAdd(&D.ctr->cands, n_cands);
 }
 
 // region of every candidate in [n0,n1) with status OK (or the listed ones)
@@ -122,6 +124,7 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_region_warp(Dev D, Cand
   WS& W = reinterpret_cast<WS*>(smem_raw)[wib];
   const int gw = blockIdx.x * WR_WARPS + wib, nw = gridDim.x * WR_WARPS;
   Scratch S = scratch_for(SC, gw);
+  unsigned long long n_calls = 0, n_tested = 0;
   for (int k = n0 + gw; k < n1; k += nw) {
     const int c = list ? list[k] : k;
     if (C.status[c] != (list ? CS_OVF : CS_OK)) continue;
@@ -132,12 +135,16 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_region_warp(Dev D, Cand
     DCHK(ns >= 0 && ns <= 32);
     SlabView v = slab(C, c);
     RegionOut O = region_view(C, c, v, 0);
+#ifdef GQ_NO_RETRY
+    int st = ns == 0 ? RS_CNSS : region_warp(D, C.p + 3 * (size_t)c, W.seeds, ns, allow_of(C, c), W, S, O);
+#else
     int st = ns == 0 ? RS_CNSS : region_warp_retry(D, C.p + 3 * (size_t)c, W.seeds, ns, allow_of(C, c), W, S, O);
+#endif
     if (lane == 0) {
-      atomicAdd(&D.ctr->region_calls, 1ull);
+      ++n_calls;
       store_region(C, c, O);
       if (st == RS_OK) {
-        atomicAdd(&D.ctr->tested, (unsigned long long)(O.ntet + O.nbf));
+        n_tested += (unsigned long long)(O.ntet + O.nbf);
         C.status[c] = (O.mind <= D.too_close_sq) ? CS_TOOCLOSE : CS_OK;
       } else if (st == RS_OVERFLOW) C.status[c] = CS_OVF;
       else if (st == RS_MEMBRANE) { C.status[c] = CS_MEMB; C.memb[c] = O.memb; }
@@ -145,6 +152,8 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_region_warp(Dev D, Cand
     }
     __syncwarp();
   }
+  // instrumentation, once per warp (per-candidate atomics on one line serialise)
+  if (lane == 0 && n_calls) { atomicAdd(&D.ctr->region_calls, n_calls); atomicAdd(&D.ctr->tested, n_tested); }
 }
 // bulk construction, warp per pending point (cached cavities re-validated);
 // redo_ovf: the large tier, run on the small tier's overflows
@@ -158,6 +167,7 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_init_region_warp(Dev D,
   WS& W = reinterpret_cast<WS*>(smem_raw)[wib];
   const int gw = blockIdx.x * WR_WARPS + wib, nw = gridDim.x * WR_WARPS;
   Scratch S = scratch_for(SC, gw);
+  unsigned long long n_calls = 0, n_tested = 0;
   for (int w = gw; w < Wn; w += nw) {
     int c = plist[w];
     if (lane == 0 && g_wdbg) { g_wdbg[2 * gw] = c; g_wdbg[2 * gw + 1] = 0; }
@@ -209,15 +219,16 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_init_region_warp(Dev D,
     int r = region_warp(D, p, W.seeds, 1, A, W, S, O, true);
     if (lane == 0 && g_wdbg) g_wdbg[2 * gw + 1] = 99;
     if (lane == 0) {
-      atomicAdd(&D.ctr->region_calls, 1ull);
+      ++n_calls;
       store_region(C, c, O);
       C.extra[c] = -1; C.kind[c] = K_TET; C.rank[c] = c; C.memb[c] = round;
-      if (r == RS_OK) { C.status[c] = CS_OK; atomicAdd(&D.ctr->tested, (unsigned long long)(O.ntet + O.nbf)); }
+      if (r == RS_OK) { C.status[c] = CS_OK; n_tested += (unsigned long long)(O.ntet + O.nbf); }
       else if (r == RS_OVERFLOW) { C.status[c] = CS_OVF; C.memb[c] = -1; }
       else { C.status[c] = CS_CNSS; raise_err(GQ_ERR_DEGEN); }
     }
     __syncwarp();
   }
+  if (lane == 0 && n_calls) { atomicAdd(&D.ctr->region_calls, n_calls); atomicAdd(&D.ctr->tested, n_tested); }
 }
 
 // oversized cavities: one block per candidate (threads in proportion to

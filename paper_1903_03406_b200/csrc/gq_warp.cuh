@@ -331,10 +331,12 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
     }
   }
   __syncwarp();
+#ifndef GQ_NO_GHOSTCHECK
   if (W.ghost && __any_sync(FULL, bf_open_part(D, O.bf, nbf, lane, 32))) {
     if (lane == 0) atomicAdd(&D.ctr->fail[3], 1u);
     return RS_BADSTAR;
   }
+#endif
   WSTOP(5);
   WMARK(15);
   // boundary vertices: min distance and the swallow check (hash reused)
