@@ -387,6 +387,10 @@ def main():
         peak = float(peaks.get("hbm_gbs", 6650.0))
         achieved = (acc["region_bytes"] / (acc["region_ms"] / 1000.0) / 1e9) if acc["region_ms"] > 0 else 0.0
         whole = acc["refine_bytes"] / (acc["dev_ms"] / 1000.0) / 1e9 if acc["dev_ms"] > 0 else 0.0
+        try:   # the secondary roofline (FP64 predicate filters): measured FMA peak of this device
+            fp64 = _native.probe_fp64(local)
+        except Exception:
+            fp64 = None
         traffic, traffic_note = None, None
         try:   # dram bytes of one captured region launch (ncu --set full), committed under profiles/
             with open(os.path.join(ROOT, "profiles", f"region_traffic_{args.config}.json")) as f:
@@ -422,7 +426,8 @@ def main():
                                           "bytes_per_step": acc["refine_bytes"] // args.steps,
                                           "formula": "144 N_cand + 58 T_tested + 8 K_claims + 51 T_created + "
                                                      "1 T_deleted + 29 N_steiner (SURVEY 8(d))"},
-                         "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if not peaks.get("_fallback") else "fallback"},
+                         "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if not peaks.get("_fallback") else "fallback",
+                         "fp64_fma_peak_tflops": fp64},
             "clocks": clk.summary(),
         }
         if args.config == "C4":

@@ -77,8 +77,15 @@ __device__ __forceinline__ void warp_claims(const Dev& D, const Cand& C, const O
     f(key);
   }
 }
+// grid-wide barrier of the cooperative launch, or the block barrier when the
+// kernel runs as one block (small rounds: no cooperative launch, which would
+// serialise against the other contexts' work on the device)
+template <bool ONE>
+__device__ __forceinline__ void gsync() {
+  if (ONE) __syncthreads(); else cg::this_grid().sync();
+}
+template <bool ONE>
 __global__ void __launch_bounds__(256) k_filter_coop(Dev D, Cand C, Owners W, int n, int* ctr) {
-  cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -89,7 +96,7 @@ __global__ void __launch_bounds__(256) k_filter_coop(Dev D, Cand C, Owners W, in
       const int r = C.rank[c];
       warp_claims(D, C, W, c, lane, [&](int k) { atomicMin(W.own + k, r); });
     }
-    grid.sync();
+    gsync<ONE>();
     for (int c = gw; c < n; c += nw) {                       // decide
       if (C.state[c] != 0) continue;
       const int r = C.rank[c];
@@ -98,14 +105,14 @@ __global__ void __launch_bounds__(256) k_filter_coop(Dev D, Cand C, Owners W, in
       win = __all_sync(FULL, win);
       if (win && lane == 0) C.state[c] = 10 + it;
     }
-    grid.sync();
+    gsync<ONE>();
     for (int c = gw; c < n; c += nw) {                       // mark
       if (C.state[c] != 10 + it) continue;
       warp_claims(D, C, W, c, lane, [&](int k) { W.own[k] = -1; });
       __syncwarp();
       if (lane == 0) C.state[c] = 1;
     }
-    grid.sync();
+    gsync<ONE>();
     int und = 0;
     for (int c = gw; c < n; c += nw) {                       // reject
       if (C.state[c] != 0) continue;
@@ -115,7 +122,7 @@ __global__ void __launch_bounds__(256) k_filter_coop(Dev D, Cand C, Owners W, in
       if (lane == 0) { if (hit) C.state[c] = 4; else ++und; }
     }
     if (lane == 0 && und) atomicAdd(ctr + it % 3, und);
-    grid.sync();
+    gsync<ONE>();
     for (int c = gw; c < n; c += nw) {                       // release the claims of losers
       const int st = C.state[c];
       if (st != 0 && st != 4) continue;
@@ -123,7 +130,7 @@ __global__ void __launch_bounds__(256) k_filter_coop(Dev D, Cand C, Owners W, in
       __syncwarp();
       if (st == 4 && lane == 0) C.state[c] = 2;
     }
-    grid.sync();
+    gsync<ONE>();
     if (*(volatile int*)(ctr + it % 3) == 0) break;
     if (it >= 100000) {                 // safety net: the iteration always makes progress
       if (gw == 0 && lane == 0) raise_err(GQ_ERR_CAP);

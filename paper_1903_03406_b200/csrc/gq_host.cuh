@@ -627,6 +627,11 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   fine(c, 26);
 }
 
+// rounds with at most this many candidates run the filter as one block
+#ifndef SMALL_FILTER
+#define SMALL_FILTER 1024
+#endif
+
 // Contexts alive on each device.  A cooperative launch needs all its blocks
 // resident at once; with several contexts running concurrently (C5) each one
 // sizes its grid to its share of the device, so the cooperative grids of all
@@ -695,15 +700,20 @@ static void run_filter(gq_ctx* c, int n, int* nacc_out) {
   if (!getenv("GQ_FILTER_LAUNCHES")) {
     static int blocks_per_sm = 0, nsm = 0;
     if (!blocks_per_sm) {
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_filter_coop, 256, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_filter_coop<false>, 256, 0));
       CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
       if (blocks_per_sm < 1) throw std::runtime_error("filter kernel cannot be resident");
     }
     int blocks = std::min(coop_share(c, blocks_per_sm * nsm), (n + 7) / 8);
     int* ctr = c->d_int + 48;
     CK(cudaMemsetAsync(ctr, 0, 12, c->st));
-    void* args[] = {&c->D, &c->C, &c->W, &n, &ctr};
-    CK(cudaLaunchCooperativeKernel((void*)k_filter_coop, dim3(std::max(blocks, 1)), dim3(256), args, 0, c->st));
+    if (n <= SMALL_FILTER) {   // one block, no cooperative launch (same iterations, same result)
+      k_filter_coop<true><<<1, 256, 0, c->st>>>(c->D, c->C, c->W, n, ctr);
+      CK(cudaGetLastError());
+    } else {
+      void* args[] = {&c->D, &c->C, &c->W, &n, &ctr};
+      CK(cudaLaunchCooperativeKernel((void*)k_filter_coop<false>, dim3(std::max(blocks, 1)), dim3(256), args, 0, c->st));
+    }
     c->launches++;
     return;
   }
@@ -973,14 +983,19 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     if (!getenv("GQ_INIT_LAUNCHES")) {
       static int bps = 0, nsm = 0;
       if (!bps) {
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_init_filter_coop, 256, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_init_filter_coop<false>, 256, 0));
         CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
         if (bps < 1) throw std::runtime_error("init filter kernel cannot be resident");
       }
       int blocks = std::max(1, std::min(coop_share(c, bps * nsm), (W + 7) / 8));
       int* tot = c->d_int + 52;
-      void* args[] = {&c->D, &C, &c->W, &d_plist, &W, &nt, &d_acc, &d_plist2, &d_scan, &tot, &d_succ};
-      CK(cudaLaunchCooperativeKernel((void*)k_init_filter_coop, dim3(blocks), dim3(256), args, 0, c->st));
+      if (W <= SMALL_FILTER) {
+        k_init_filter_coop<true><<<1, 256, 0, c->st>>>(c->D, C, c->W, d_plist, W, nt, d_acc, d_plist2, d_scan, tot, d_succ);
+        CK(cudaGetLastError());
+      } else {
+        void* args[] = {&c->D, &C, &c->W, &d_plist, &W, &nt, &d_acc, &d_plist2, &d_scan, &tot, &d_succ};
+        CK(cudaLaunchCooperativeKernel((void*)k_init_filter_coop<false>, dim3(blocks), dim3(256), args, 0, c->st));
+      }
       c->launches++;
       int h2[4];
       CK(cudaMemcpyAsync(h2, tot, 16, cudaMemcpyDeviceToHost, c->st));

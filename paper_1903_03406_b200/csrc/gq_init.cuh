@@ -130,9 +130,9 @@ __global__ void k_init_unclaim(Dev D, Cand C, Owners W, const int* plist, int nw
 // one cooperative kernel: a warp per window point walks its claims
 // lane-parallel; block 0 scans acceptance and boundary-face counts between the
 // barriers; totals go to tot[0] (accepted) and tot[1] (new tets).
+template <bool ONE>
 __global__ void __launch_bounds__(256) k_init_filter_coop(Dev D, Cand C, Owners W, const int* plist, int nw_in, int nt,
                                                           int* acc, int* accscan, int* nbfscan, int* tot, int* succ) {
-  cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -140,17 +140,17 @@ __global__ void __launch_bounds__(256) k_init_filter_coop(Dev D, Cand C, Owners 
   // kernel (it is computed by the block kernel next round): tot[3] = window,
   // tot[2] = overflowed points in the window
   if (blockIdx.x == 0 && threadIdx.x == 0) { tot[2] = 0; tot[3] = nw_in; }
-  grid.sync();
+  gsync<ONE>();
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw_in; w += gridDim.x * blockDim.x)
     if (C.status[plist[w]] == CS_OVF) { atomicMin(tot + 3, w); atomicAdd(tot + 2, 1); }
-  grid.sync();
+  gsync<ONE>();
   const int nw = *(volatile int*)(tot + 3);
   for (int w = nw + blockIdx.x * blockDim.x + threadIdx.x; w < nw_in; w += gridDim.x * blockDim.x) acc[w] = 0;
   for (int w = gw; w < nw; w += nwarp) {                    // claim: lowest order wins
     const int c = plist[w];
     warp_claims(D, C, W, c, lane, [&](int k) { atomicMin(W.own + k, c); });
   }
-  grid.sync();
+  gsync<ONE>();
   for (int w = gw; w < nw; w += nwarp) {                    // decide
     const int c = plist[w];
     bool win = true;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) k_init_filter_coop(Dev D, Cand C, Owners 
     win = __all_sync(FULL, win);
     if (lane == 0) acc[w] = win;
   }
-  grid.sync();
+  gsync<ONE>();
   for (int w = gw; w < nw; w += nwarp)                      // release
     warp_claims(D, C, W, plist[w], lane, [&](int k) { W.own[k] = INT_MAX; });
   if (blockIdx.x == 0) {                                    // scans in insertion order
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256) k_init_filter_coop(Dev D, Cand C, Owners 
       if (nt + carry[1] > D.tcap) raise_err(GQ_ERR_CAP);
     }
   }
-  grid.sync();
+  gsync<ONE>();
   for (int w = gw; w < nw; w += nwarp) {                    // new tet ids, cavities die
     if (!acc[w]) continue;
     const int c = plist[w];

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_init_region_warp(Dev D,
     RegionOut O = region_view(C, c, sv, 0);
     Allow A; A.n = 0;
     if (lane == 0 && g_wdbg) g_wdbg[2 * gw + 1] = 2;
-    int r = region_warp(D, p, W.seeds, 1, A, W, S, O, true);
+    int r = region_warp(D, p, W.seeds, 1, A, W, S, O, true, 0u, false, false);
     if (lane == 0 && g_wdbg) g_wdbg[2 * gw + 1] = 99;
     if (lane == 0) {
       ++n_calls;

@@ -88,7 +88,7 @@ __device__ inline int wh_find(const WS& W, int k) {
 template <int MAXT, int HASH>
 __device__ inline int region_warp(const Dev& D, const double* p, const int* seeds, int nseeds, const Allow& A,
                                   WarpSharedT<MAXT, HASH>& W, Scratch& S, RegionOut& O, bool walk_on_miss = true,
-                                  unsigned excl = 0u, bool may_retry = false) {
+                                  unsigned excl = 0u, bool may_retry = false, bool check_ghost = true) {
   constexpr int WR_MAXT = MAXT, WR_HASH = HASH;
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
@@ -332,7 +332,8 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
   }
   __syncwarp();
 #ifndef GQ_NO_GHOSTCHECK
-  if (W.ghost && __any_sync(FULL, bf_open_part(D, O.bf, nbf, lane, 32))) {
+  // (bulk construction skips it: its hull is the convex hull of exact input points)
+  if (check_ghost && W.ghost && __any_sync(FULL, bf_open_part(D, O.bf, nbf, lane, 32))) {
     if (lane == 0) atomicAdd(&D.ctr->fail[3], 1u);
     return RS_BADSTAR;
   }
