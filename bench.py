@@ -370,9 +370,8 @@ def main():
     e2e_wall = time.perf_counter() - e0
     for prep in preps:
         h2d += prep.points.nbytes + prep.segments.nbytes + prep.poly_off.nbytes + prep.poly_idx.nbytes + prep.order.nbytes
-    d2h = (mesh.points.nbytes + mesh.vert_origin.nbytes + mesh.vert_tet.nbytes + mesh.tv.nbytes + mesh.tn.nbytes
-           + mesh.alive.nbytes + mesh.sub_mask.nbytes + mesh.seg_mask.nbytes + mesh.ratio.nbytes
-           + mesh.skip_flag.nbytes) * len(plcs)
+    # bytes actually copied by gq_export_mesh (int32 ids on the wire) per PLC
+    d2h = (mesh.nv * (24 + 1 + 4) + mesh.nt * (16 + 16 + 4 * 1 + 8)) * len(plcs)
     t_dev = acc["dev_ms"] / 1000.0
     tot_steiner = acc["steiner"]
     if world > 1:

@@ -72,6 +72,8 @@ template <class T> static T* dmalloc(size_t n) {
 
 struct gq_ctx {
   DevCache cache;
+  char* pin = nullptr; size_t pin_cap = 0, pin_used = 0;                 // pinned read-back staging
+  std::vector<std::tuple<void*, size_t, size_t>> staged;
   int device = 0;
   cudaStream_t st = nullptr;
   std::string err;
@@ -135,17 +137,37 @@ static const char* g_fine_names[32] = {"i.region", "i.big", "i.filter", "i.scan"
   "r.setup", "r.gridc", "r.kept", "x.fallback", "r.misc2"};
 static thread_local double g_fine_last = 0;
 static void fine(gq_ctx* c, int k);
+// Device -> host reads go through a pinned staging buffer on the context's
+// stream: a pageable destination makes the copy synchronous and serialises it
+// against every other context's stream (C5 runs several at once).  stage()
+// enqueues, sync() waits and delivers.
+static void stage(gq_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (c->pin_used + bytes + 64 > c->pin_cap) {   // too large for the staging buffer: pageable copy
+    stage(c, dst, src, bytes);
+    return;
+  }
+  size_t off = c->pin_used;
+  CK(cudaMemcpyAsync(c->pin + off, src, bytes, cudaMemcpyDeviceToHost, c->st));
+  c->staged.push_back({dst, off, bytes});
+  c->pin_used = (off + bytes + 15) & ~size_t(15);
+}
 static void sync(gq_ctx* c) {
+  // the error word travels with the stream too (cudaMemcpyFromSymbol would use the legacy stream)
+  const size_t eoff = c->pin_cap - 16;
+  CK(cudaMemcpyFromSymbolAsync(c->pin + eoff, g_err, sizeof(unsigned int), 0, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  for (auto& s : c->staged) std::memcpy(std::get<0>(s), c->pin + std::get<1>(s), std::get<2>(s));
+  c->staged.clear();
+  c->pin_used = 0;
   unsigned int e = 0;
-  CK(cudaMemcpyFromSymbol(&e, g_err, sizeof(e)));
+  std::memcpy(&e, c->pin + eoff, sizeof(e));
   if (e) {
     char buf[128];
     std::snprintf(buf, sizeof buf, "device error flags 0x%x", e);
     throw std::runtime_error(buf);
   }
 }
-static void pull(gq_ctx* c) { CK(cudaMemcpyAsync(&c->hc, c->dctr, sizeof(Counters), cudaMemcpyDeviceToHost, c->st)); sync(c); }
+static void pull(gq_ctx* c) { stage(c, &c->hc, c->dctr, sizeof(Counters)); sync(c); }
 // the mesh / record counts only: the instrumentation counters are device-owned
 static void push(gq_ctx* c) { CK(cudaMemcpyAsync(c->dctr, &c->hc, offsetof(Counters, region_calls), cudaMemcpyHostToDevice, c->st)); }
 static int grid_for(long long n, int bs = 128, int cap = 148 * 16) {
@@ -193,8 +215,8 @@ static int select_flagged(gq_ctx* c, const int* flags, int n, int* out) {
   exclusive_scan(c, flags, c->tmpC, n);
   LAUNCH(k_scatter_flagged, n, flags, c->tmpC, n, out);
   int last_f = 0, last_s = 0;
-  CK(cudaMemcpyAsync(&last_f, flags + n - 1, 4, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(&last_s, c->tmpC + n - 1, 4, cudaMemcpyDeviceToHost, c->st));
+  stage(c, &last_f, flags + n - 1, 4);
+  stage(c, &last_s, c->tmpC + n - 1, 4);
   sync(c);
   return last_f + last_s;
 }
@@ -206,10 +228,10 @@ static void exclusive_scan(gq_ctx* c, const int* in, int* out, int n) {
 }
 // device -> host copy ordered on the context's stream, complete on return
 static void d2h(gq_ctx* c, void* dst, const void* src, size_t bytes) {
-  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  stage(c, dst, src, bytes);
+  sync(c);
 }
-static int read_int(gq_ctx* c, const int* d) { int v; CK(cudaMemcpyAsync(&v, d, sizeof v, cudaMemcpyDeviceToHost, c->st)); sync(c); return v; }
+static int read_int(gq_ctx* c, const int* d) { int v; stage(c, &v, d, sizeof v); sync(c); return v; }
 
 static void alloc_scratch(Scr& s, int nthreads, int cap, int tcap, int fcap, cudaStream_t st) {
   s.nthreads = nthreads; s.cap = cap; s.tcap = tcap; s.fcap = fcap;
@@ -583,7 +605,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   // overflow passes: the large warp tier, then one block per cavity
   ensure_tmp(c, n1 + 1);
   std::vector<int> hs(n1 - n0);
-  CK(cudaMemcpyAsync(hs.data(), c->C.status + n0, sizeof(int) * (n1 - n0), cudaMemcpyDeviceToHost, c->st));
+  stage(c, hs.data(), c->C.status + n0, sizeof(int) * (n1 - n0));
   sync(c);
   std::vector<int> ovf;
   for (int k = 0; k < n1 - n0; ++k) if (hs[k] == CS_OVF) ovf.push_back(n0 + k);
@@ -595,7 +617,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
     launch_warp_regions(c, k_region_warp<WT2_MAXT, WT2_HASH, 1>, WR_WARPS * sizeof(WarpShared2), no, 0, no, c->tmpB);
     region_end(c);
     LAUNCH(k_gather_status, no, c->C, c->tmpB, no, c->tmpA);
-    CK(cudaMemcpyAsync(hs.data(), c->tmpA, sizeof(int) * no, cudaMemcpyDeviceToHost, c->st));
+    stage(c, hs.data(), c->tmpA, sizeof(int) * no);
     sync(c);
     for (int k = 0; k < no; ++k) if (hs[k] == CS_OVF) big.push_back(ovf[k]);
   } else {
@@ -629,7 +651,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
 
 // rounds with at most this many candidates run the filter as one block
 #ifndef SMALL_FILTER
-#define SMALL_FILTER 1024
+#define SMALL_FILTER 64
 #endif
 
 // Contexts alive on each device.  A cooperative launch needs all its blocks
@@ -796,7 +818,7 @@ static bool full_verify(gq_ctx* c) {
   CK(cudaMemsetAsync(c->d_int + 4, 0, 16, c->st));
   LAUNCH(k_count_pending, c->hc.nsegrec + c->hc.nfacerec, c->D, c->d_int + 4);
   int h[8];
-  CK(cudaMemcpyAsync(h, c->d_int, 32, cudaMemcpyDeviceToHost, c->st));
+  stage(c, h, c->d_int, 32);
   sync(c);
   return h[0] > 0 || h[6] > 0 || h[7] > 0;
 }
@@ -935,8 +957,8 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
       if (novf > 0) {
         std::vector<int> pl(W), sw(W);
         LAUNCH(k_gather_status, W, C, d_plist, W, d_scan);
-        CK(cudaMemcpyAsync(pl.data(), d_plist, 4 * (size_t)W, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaMemcpyAsync(sw.data(), d_scan, 4 * (size_t)W, cudaMemcpyDeviceToHost, c->st));
+        stage(c, pl.data(), d_plist, 4 * (size_t)W);
+        stage(c, sw.data(), d_scan, 4 * (size_t)W);
         sync(c);
         for (int w = 0; w < W; ++w) if (sw[w] == CS_OVF) bl.push_back(pl[w]);
         if (WT1_MAXT != WT2_MAXT && !getenv("GQ_THREAD_INIT")) {   // the large warp tier first
@@ -949,7 +971,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
           CK(cudaGetLastError());
           LAUNCH(k_gather_status, no, C, d_keep, no, d_scan);
           std::vector<int> s2(no);
-          CK(cudaMemcpyAsync(s2.data(), d_scan, 4 * (size_t)no, cudaMemcpyDeviceToHost, c->st));
+          stage(c, s2.data(), d_scan, 4 * (size_t)no);
           sync(c);
           std::vector<int> rest;
           for (int k = 0; k < no; ++k) if (s2[k] == CS_OVF) rest.push_back(bl[k]);
@@ -970,7 +992,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
         c->launches++;
         CK(cudaGetLastError());
         LAUNCH(k_gather_status, W, C, d_plist, W, d_scan);
-        CK(cudaMemcpyAsync(sw.data(), d_scan, 4 * (size_t)W, cudaMemcpyDeviceToHost, c->st));
+        stage(c, sw.data(), d_scan, 4 * (size_t)W);
         sync(c);
         for (int w = 0; w < W; ++w) if (sw[w] == CS_OVF) { W = w; break; }
         if (W == 0) throw std::runtime_error("init: cavity overflow");
@@ -998,7 +1020,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
       }
       c->launches++;
       int h2[4];
-      CK(cudaMemcpyAsync(h2, tot, 16, cudaMemcpyDeviceToHost, c->st));
+      stage(c, h2, tot, 16);
       sync(c);
       nacc = h2[0]; add_t = h2[1]; novf_last = h2[2];
       if (nt + add_t > c->D.tcap) throw std::runtime_error("tet capacity exceeded in init");
@@ -1011,12 +1033,12 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
       LAUNCH(k_init_nbf, W, C, d_plist, d_acc, W, d_keep);
       exclusive_scan(c, d_keep, d_scan, W);
       int lastn = 0, lasts = 0, lasta = 0;
-      CK(cudaMemcpyAsync(&lastn, d_keep + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
-      CK(cudaMemcpyAsync(&lasts, d_scan + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
+      stage(c, &lastn, d_keep + W - 1, 4);
+      stage(c, &lasts, d_scan + W - 1, 4);
       exclusive_scan(c, d_acc, d_plist2, W);
       int lastacc_scan = 0;
-      CK(cudaMemcpyAsync(&lastacc_scan, d_plist2 + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
-      CK(cudaMemcpyAsync(&lasta, d_acc + W - 1, 4, cudaMemcpyDeviceToHost, c->st));
+      stage(c, &lastacc_scan, d_plist2 + W - 1, 4);
+      stage(c, &lasta, d_acc + W - 1, 4);
       sync(c);
       nacc = lastacc_scan + lasta;
       add_t = lasts + lastn;
@@ -1133,8 +1155,8 @@ static int scan_total(gq_ctx* c, const int* in, int* out, int n) {
   if (n <= 0) return 0;
   exclusive_scan(c, in, out, n);
   int a = 0, b = 0;
-  CK(cudaMemcpyAsync(&a, in + n - 1, 4, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(&b, out + n - 1, 4, cudaMemcpyDeviceToHost, c->st));
+  stage(c, &a, in + n - 1, 4);
+  stage(c, &b, out + n - 1, 4);
   sync(c);
   return a + b;
 }
@@ -1185,9 +1207,10 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
   }
   g_prof[3] += now_s() - t0;
   double t1 = now_s();
-  if (nit > 0 && nit <= 512 && !getenv("GQ_T2_LAUNCHES")) {   // few items: all passes in one block
+  if (nit > 0 && nit <= 4096 && !getenv("GQ_T2_LAUNCHES")) {   // all passes in one launch, polygons split over blocks
     c->T.n = nit;
-    k_t2_fused<<<1, 128, 0, c->st>>>(c->D, C, c->T, c->S, c->d_int + 16);
+    CK(cudaMemsetAsync(c->d_int + 16, 0, 4, c->st));
+    k_t2_fused<<<std::min(std::min(nit, c->npoly), c->S.nthreads / 128), 128, 0, c->st>>>(c->D, C, c->T, c->S, c->d_int + 16);
     c->launches++;
     CK(cudaGetLastError());
   } else if (nit > 0) {
@@ -1347,7 +1370,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     ensure_tmp(c, nbase + 1);
     LAUNCH(k_kept, nbase, c->C, nbase, c->Q.a);
     int redir[2] = {0, 0};
-    CK(cudaMemcpyAsync(redir, c->d_int + 60, 8, cudaMemcpyDeviceToHost, c->st));   // read with the scan below
+    stage(c, redir, c->d_int + 60, 8);   // read with the scan below
     int kept = scan_total(c, c->Q.a, c->Q.b, nbase);
     LAUNCH(k_pool_pos, nbase, c->C, nbase, c->Q.b, c->Q.a);
     fine(c, 29);

@@ -191,8 +191,9 @@ __device__ __noinline__ int t2_seed_of(const Dev& D, const Cand& C, int c, int p
 // The passes of the facet retiling as bodies over items [start, T.n) with a
 // stride: launched grid-wide for many items, or all passes fused in one block
 // (k_t2_fused) when a round has few of them.
-__device__ void t2_compute_body(const Dev& D, const Cand& C, const T2Items& T, Scratch& S, int start, int stride) {
+__device__ void t2_compute_body(const Dev& D, const Cand& C, const T2Items& T, Scratch& S, int start, int stride, int pm = 1, int pb = 0) {
   for (int w = start; w < T.n; w += stride) {
+    if (pm > 1 && T.pid[w] % pm != pb) continue;   // another block's polygons
     if (T.state[w] != 0) continue;
     int c = T.cand[w], pid = T.pid[w];
     Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = C.vid[c]; X.follow3d = D.poly_obl[pid];
@@ -225,15 +226,17 @@ __device__ inline void t2_for_claims(const Dev& D, const T2Items& T, int w, F f)
     (void)pid;
   }
 }
-__device__ void t2_claim_body(const Dev& D, const Cand& C, const T2Items& T, int start, int stride) {
+__device__ void t2_claim_body(const Dev& D, const Cand& C, const T2Items& T, int start, int stride, int pm = 1, int pb = 0) {
   for (int w = start; w < T.n; w += stride) {
+    if (pm > 1 && T.pid[w] % pm != pb) continue;   // another block's polygons
     if (T.state[w] != 0) continue;
     int r = C.rank[T.cand[w]];
     t2_for_claims(D, T, w, [&](int tid) { atomicMin(T.own + tid, r); });
   }
 }
-__device__ void t2_apply_body(const Dev& D, const Cand& C, const T2Items& T, int* applied, int start, int stride) {
+__device__ void t2_apply_body(const Dev& D, const Cand& C, const T2Items& T, int* applied, int start, int stride, int pm = 1, int pb = 0) {
   for (int w = start; w < T.n; w += stride) {
+    if (pm > 1 && T.pid[w] % pm != pb) continue;   // another block's polygons
     if (T.state[w] != 0) continue;
     int c = T.cand[w];
     int r = C.rank[c];
@@ -244,8 +247,9 @@ __device__ void t2_apply_body(const Dev& D, const Cand& C, const T2Items& T, int
     atomicAdd(applied, 1);
   }
 }
-__device__ void t2_commit_body(const Dev& D, const Cand& C, const T2Items& T, Scratch& S, int start, int stride) {
+__device__ void t2_commit_body(const Dev& D, const Cand& C, const T2Items& T, Scratch& S, int start, int stride, int pm = 1, int pb = 0) {
   for (int w = start; w < T.n; w += stride) {
+    if (pm > 1 && T.pid[w] % pm != pb) continue;   // another block's polygons
     if (T.state[w] != 2) continue;
     int c = T.cand[w], pid = T.pid[w];
     Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = C.vid[c]; X.follow3d = D.poly_obl[pid];
@@ -275,16 +279,18 @@ __device__ void t2_commit_body(const Dev& D, const Cand& C, const T2Items& T, Sc
     T.state[w] = 1;
   }
 }
-__device__ void t2_reset_body(const Dev& D, const T2Items& T, int final_pass, int start, int stride) {
+__device__ void t2_reset_body(const Dev& D, const T2Items& T, int final_pass, int start, int stride, int pm = 1, int pb = 0) {
   for (int w = start; w < T.n; w += stride) {
+    if (pm > 1 && T.pid[w] % pm != pb) continue;   // another block's polygons
     if (!final_pass && T.state[w] == 1 && T.ncav[w] < 0) continue;
     t2_for_claims(D, T, w, [&](int tid) { T.own[tid] = INT_MAX; });
   }
 }
 // retire the removed subface records (after every pass, so lookups in later
 // passes still see the pre-round tables only for untouched keys)
-__device__ void t2_retire_body(const Dev& D, const T2Items& T, int start, int stride) {
+__device__ void t2_retire_body(const Dev& D, const T2Items& T, int start, int stride, int pm = 1, int pb = 0) {
   for (int w = start; w < T.n; w += stride) {
+    if (pm > 1 && T.pid[w] % pm != pb) continue;   // another block's polygons
     const int* rem = T.rem + (size_t)w * T.rcap;
     for (int k = 0; k < T.nrem[w]; ++k) D.sf_fl[rem[k]] = 0;
   }
@@ -304,31 +310,41 @@ __global__ void k_t2_commit(Dev D, Cand C, T2Items T, Scr SC) {
 }
 __global__ void k_t2_reset(Dev D, Cand C, T2Items T, int final_pass) { t2_reset_body(D, T, final_pass, GRID_START, GRID_STRIDE); }
 __global__ void k_t2_retire(Dev D, T2Items T) { t2_retire_body(D, T, GRID_START, GRID_STRIDE); }
-// every pass of a round in one block: no launches or host reads between passes
+// every pass of a round without launches or host reads between passes.  The
+// items of different polygons never share a 2D triangle, so block b takes the
+// polygons with pid % gridDim.x == b and runs its own passes.
 __global__ void __launch_bounds__(128) k_t2_fused(Dev D, Cand C, T2Items T, Scr SC, int* applied_total) {
-  Scratch S = scratch_for(SC, threadIdx.x);
-  __shared__ int s_applied;
-  int left = T.n;
+  Scratch S = scratch_for(SC, blockIdx.x * blockDim.x + threadIdx.x);
+  const int pm = gridDim.x, pb = blockIdx.x;
+  __shared__ int s_applied, s_left;
+  if (threadIdx.x == 0) s_left = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int w = threadIdx.x; w < T.n; w += blockDim.x) mine += (T.pid[w] % pm == pb);
+  atomicAdd(&s_left, mine);
+  __syncthreads();
+  int left = s_left;
+  const int total = left;
   for (int pass = 0; left > 0; ++pass) {
     if (threadIdx.x == 0) s_applied = 0;
-    t2_compute_body(D, C, T, S, threadIdx.x, blockDim.x);
+    t2_compute_body(D, C, T, S, threadIdx.x, blockDim.x, pm, pb);
     __syncthreads();
-    t2_claim_body(D, C, T, threadIdx.x, blockDim.x);
+    t2_claim_body(D, C, T, threadIdx.x, blockDim.x, pm, pb);
     __syncthreads();
-    t2_apply_body(D, C, T, &s_applied, threadIdx.x, blockDim.x);
+    t2_apply_body(D, C, T, &s_applied, threadIdx.x, blockDim.x, pm, pb);
     __syncthreads();
-    t2_reset_body(D, T, 1, threadIdx.x, blockDim.x);
+    t2_reset_body(D, T, 1, threadIdx.x, blockDim.x, pm, pb);
     __syncthreads();
-    t2_commit_body(D, C, T, S, threadIdx.x, blockDim.x);
+    t2_commit_body(D, C, T, S, threadIdx.x, blockDim.x, pm, pb);
     __syncthreads();
-    t2_retire_body(D, T, threadIdx.x, blockDim.x);
+    t2_retire_body(D, T, threadIdx.x, blockDim.x, pm, pb);
     __syncthreads();
     const int applied = s_applied;
     __syncthreads();
     if (applied == 0) { if (threadIdx.x == 0) raise_err(GQ_ERR_2D); break; }
     left -= applied;
   }
-  if (threadIdx.x == 0) *applied_total = T.n - left;
+  if (threadIdx.x == 0) atomicAdd(applied_total, total - left);
 }
 
 __global__ void k_kill_cavities(Dev D, Cand C, Ins I) {

@@ -25,6 +25,7 @@ namespace cg = cooperative_groups;
 #include <algorithm>
 #include <atomic>
 #include <thread>
+#include <tuple>
 #include <array>
 #include <chrono>
 #include <cstdio>
@@ -68,6 +69,8 @@ int gq_create(int device, gq_ctx** out) {
     c->device = device;
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    c->pin_cap = size_t(1) << 20;   // read-back staging (counters, scan tails, overflow lists)
+    CK(cudaHostAlloc((void**)&c->pin, c->pin_cap, cudaHostAllocDefault));
     CK(cudaEventCreate(&c->ev0)); CK(cudaEventCreate(&c->ev1));
     CK(cudaEventCreate(&c->er0)); CK(cudaEventCreate(&c->er1));
     CK(cudaDeviceSetLimit(cudaLimitStackSize, 24576));   // k_fallback: ~18 KB (exact predicates on 40-limb integers)
@@ -111,6 +114,7 @@ int gq_destroy(gq_ctx* c) {
     for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
     { DevCache& C = dev_cache(); std::lock_guard<std::mutex> g(C.mu); cache_trim(C); }
     if (c->st) cudaStreamDestroy(c->st);
+    if (c->pin) cudaFreeHost(c->pin);
   } catch (...) {}
   g_ctx_count[c->device & 63].fetch_sub(1);
   delete c;
