@@ -142,9 +142,17 @@ static void fine(gq_ctx* c, int k);
 // against every other context's stream (C5 runs several at once).  stage()
 // enqueues, sync() waits and delivers.
 static void stage(gq_ctx* c, void* dst, const void* src, size_t bytes) {
-  if (c->pin_used + bytes + 64 > c->pin_cap) {   // too large for the staging buffer: pageable copy
-    stage(c, dst, src, bytes);
-    return;
+  if (c->pin_used + bytes + 64 > c->pin_cap) {
+    if (!c->staged.empty()) {                     // no room beside pending reads: pageable copy
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->st));
+      return;
+    }
+    size_t cap = c->pin_cap;                      // nothing pending: grow the staging buffer
+    while (bytes + 64 > cap) cap *= 2;
+    CK(cudaFreeHost(c->pin));
+    c->pin = nullptr;
+    CK(cudaHostAlloc((void**)&c->pin, cap, cudaHostAllocDefault));
+    c->pin_cap = cap;
   }
   size_t off = c->pin_used;
   CK(cudaMemcpyAsync(c->pin + off, src, bytes, cudaMemcpyDeviceToHost, c->st));
