@@ -55,6 +55,7 @@ struct Counters {
                                      // 2 swallows a vertex, 3 pinched ghost boundary, 4 star check,
                                      // 5 sequential-path overflow, 6 membrane
   int first_real;                    // no alive real tet has a lower index (hint_tet; 0 after compaction)
+  unsigned long long t2st[4];        // 2D cavities (diagnostics): computed, walk steps, exhaustive scans, triangles scanned
 };
 
 // A tet is one 32-byte record {tv, tn} (vertices, then packed neighbour
@@ -1073,6 +1074,7 @@ __device__ __noinline__ int tri2_cavity(const Tri2Ctx& C, const int* forced, int
   const Dev& D = *C.D;
   set.clear();
   int n = 0;
+  atomicAdd(&D.ctr->t2st[0], 1ull);
   if (C.follow3d) {
     // Oblique polygon.  Its Steiner points round off the polygon plane, so an
     // in-plane Delaunay cavity and the 3D cavity disagree near cocircular
@@ -1103,7 +1105,8 @@ __device__ __noinline__ int tri2_cavity(const Tri2Ctx& C, const int* forced, int
     // facets.py:107-123: walk toward p
     int tid = start;
     int n_alive = D.t2count[C.pid];
-    for (int s = 0; s < 4 * n_alive + 16; ++s) {
+    int s = 0;
+    for (; s < 4 * n_alive + 16; ++s) {
       int4 t = D.t2v[tid];
       if (t.z == GHOST) break;
       bool moved = false;
@@ -1114,9 +1117,11 @@ __device__ __noinline__ int tri2_cavity(const Tri2Ctx& C, const int* forced, int
       }
       if (!moved) break;
     }
+    atomicAdd(&D.ctr->t2st[1], (unsigned long long)s);
     if (tri_in_region(C, tid)) seed = tid;
     if (seed < 0 && nforced == 0) {   // exhaustive fallback (facets.py:121-123)
       const int nt2 = D.ctr->nt2;
+      atomicAdd(&D.ctr->t2st[2], 1ull); atomicAdd(&D.ctr->t2st[3], (unsigned long long)nt2);
       for (int t = 0; t < nt2 && seed < 0; ++t)
         if (D.t2alive[t] && D.t2v[t].w == C.pid && tri_in_region(C, t)) seed = t;
     }

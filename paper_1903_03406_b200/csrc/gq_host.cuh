@@ -130,11 +130,11 @@ static thread_local double g_prof[8];
 static thread_local bool g_trace = false;
 static thread_local bool g_fine = false;      // GQ_PROFILE=2: host clock after a sync per stage
 static thread_local bool g_fine_ev = false;   // GQ_PROFILE=3: events per stage (device timeline, no syncs)
-static thread_local double g_fine_t[32];
-static const char* g_fine_names[32] = {"i.region", "i.big", "i.filter", "i.scan", "i.kill", "i.stars", "i.compact",
+static thread_local double g_fine_t[40];
+static const char* g_fine_names[40] = {"i.region", "i.big", "i.filter", "i.scan", "i.kill", "i.stars", "i.compact",
   "p.gridsync", "p.newverts", "p.check", "p.compact", "r.sorted", "r.make", "r.redirect", "r.append", "f.states",
   "f.rank", "f.lfmis", "x.acc", "x.ids", "x.star", "x.postins", "i.misc", "r.misc", "g.warp", "g.ovfscan", "g.block",
-  "r.setup", "r.gridc", "r.kept", "x.fallback", "r.misc2"};
+  "r.setup", "r.gridc", "r.kept", "x.fallback", "r.misc2", "x.verts", "x.items", "x.t2"};
 static thread_local double g_fine_last = 0;
 static void fine(gq_ctx* c, int k);
 // Device -> host reads go through a pinned staging buffer on the context's
@@ -185,6 +185,8 @@ static int grid_for(long long n, int bs = 128, int cap = 148 * 16) {
   return (int)g;
 }
 #define LAUNCH(kern, n, ...) do { kern<<<grid_for(n), 128, 0, c->st>>>(__VA_ARGS__); c->launches++; CK(cudaGetLastError()); } while (0)
+// one item per warp (lane 0), scratch slot per warp
+#define LAUNCH_W(kern, n, ...) do { kern<<<std::max(1, (int)((std::min<long long>(n, c->S.nthreads) + 3) / 4)), 128, 0, c->st>>>(__VA_ARGS__); c->launches++; CK(cudaGetLastError()); } while (0)
 #define LAUNCH_S(kern, n, ...) do { kern<<<grid_for(n, 128, c->S.nthreads / 128), 128, 0, c->st>>>(__VA_ARGS__); c->launches++; CK(cudaGetLastError()); } while (0)
 
 static void ensure_cub(gq_ctx* c, size_t need) {
@@ -1203,6 +1205,7 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
   Ins I; I.list = ins; I.n = ni; I.nv0 = nv; I.nt0base = nt;
   fine(c, 18);
   LAUNCH(k_ins_vertices, ni, c->D, C, I);
+  fine(c, 32);
   // facet 2D retiling work items (candidate, polygon) in priority order
   int* item_of = nullptr;
   int nit = 0;
@@ -1214,8 +1217,11 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
     if (nit > 0) LAUNCH(k_item_fill, ni, c->D, C, ins, ni, pos, flags, c->T, item_of);
   }
   g_prof[3] += now_s() - t0;
+  fine(c, 33);
   double t1 = now_s();
-  if (nit > 0 && nit <= 4096 && !getenv("GQ_T2_LAUNCHES")) {   // all passes in one launch, polygons split over blocks
+  static const int t2_fused_max = getenv("GQ_T2_FUSED_MAX") ? atoi(getenv("GQ_T2_FUSED_MAX")) : 256;
+  static const bool t2_thread = getenv("GQ_T2_THREAD") != nullptr;
+  if (nit > 0 && nit <= t2_fused_max) {   // few items: all passes in one launch, polygons split over blocks
     c->T.n = nit;
     CK(cudaMemsetAsync(c->d_int + 16, 0, 4, c->st));
     k_t2_fused<<<std::min(std::min(nit, c->npoly), c->S.nthreads / 128), 128, 0, c->st>>>(c->D, C, c->T, c->S, c->d_int + 16);
@@ -1225,12 +1231,20 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
     c->T.n = nit;
     int left = nit;
     for (int pass = 0; left > 0; ++pass) {
-      LAUNCH_S(k_t2_compute, nit, c->D, C, c->T, c->S);
-      LAUNCH(k_t2_claim, nit, c->D, C, c->T);
       CK(cudaMemsetAsync(c->d_int + 16, 0, 4, c->st));
-      LAUNCH_S(k_t2_apply, nit, c->D, C, c->T, c->S, c->d_int + 16);
-      LAUNCH(k_t2_reset, nit, c->D, C, c->T, 1);
-      LAUNCH_S(k_t2_commit, nit, c->D, C, c->T, c->S);
+      if (t2_thread) {
+        LAUNCH_S(k_t2_compute, nit, c->D, C, c->T, c->S);
+        LAUNCH(k_t2_claim, nit, c->D, C, c->T);
+        LAUNCH_S(k_t2_apply, nit, c->D, C, c->T, c->S, c->d_int + 16);
+        LAUNCH(k_t2_reset, nit, c->D, C, c->T, 1);
+        LAUNCH_S(k_t2_commit, nit, c->D, C, c->T, c->S);
+      } else {
+        LAUNCH_W(k_t2w_compute, nit, c->D, C, c->T, c->S);
+        LAUNCH_W(k_t2w_claim, nit, c->D, C, c->T);
+        LAUNCH_W(k_t2w_apply, nit, c->D, C, c->T, c->d_int + 16);
+        LAUNCH_W(k_t2w_reset, nit, c->D, c->T, 1);
+        LAUNCH_W(k_t2w_commit, nit, c->D, C, c->T, c->S);
+      }
       LAUNCH(k_t2_retire, nit, c->D, c->T);
       int applied = read_int(c, c->d_int + 16);
       if (g_trace) std::fprintf(stderr, "[t2] pass %d applied %d of %d\n", pass, applied, left);
@@ -1241,7 +1255,7 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
   g_prof[4] += now_s() - t1;
   if (g_trace && nit > 0) std::fprintf(stderr, "[t2] round %d items %d inserted %d\n", round_no, nit, ni);
   t1 = now_s();
-  fine(c, 19);
+  fine(c, 34);
   LAUNCH(k_ins_segsplit, ni, c->D, C, I);
   LAUNCH(k_kill_cavities, ni, c->D, C, I);
   {
@@ -1651,13 +1665,16 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   resolve_events(c);
   if (g_fine || g_fine_ev) {
     std::fprintf(stderr, "[gq fine]");
-    for (int k = 0; k < 32; ++k) if (g_fine_t[k] > 0) { std::fprintf(stderr, " %s %.1f;", g_fine_names[k], 1000 * g_fine_t[k]); g_fine_t[k] = 0; }
+    for (int k = 0; k < 40; ++k) if (g_fine_t[k] > 0) { std::fprintf(stderr, " %s %.1f;", g_fine_names[k], 1000 * g_fine_t[k]); g_fine_t[k] = 0; }
     std::fprintf(stderr, "\n");
   }
   if (getenv("GQ_PROFILE")) {
     std::fprintf(stderr, "[gq profile] init %.1f ms (%d rounds);", c->init_ms, c->init_rounds);
     for (int k = 0; k < 8; ++k) { std::fprintf(stderr, " %s %.1f ms;", g_prof_names[k], 1000 * g_prof[k]); g_prof[k] = 0; }
     std::fprintf(stderr, " region kernels %.1f ms; launches %lld\n", c->region_ms, c->launches);
+    pull(c);
+    std::fprintf(stderr, "[gq 2d] cavities %llu walk steps %llu exhaustive scans %llu (%llu triangles)\n", c->hc.t2st[0],
+                 c->hc.t2st[1], c->hc.t2st[2], c->hc.t2st[3]);
   }
   pull(c);
   if (out) {

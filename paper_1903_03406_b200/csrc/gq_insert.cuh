@@ -310,6 +310,28 @@ __global__ void k_t2_commit(Dev D, Cand C, T2Items T, Scr SC) {
 }
 __global__ void k_t2_reset(Dev D, Cand C, T2Items T, int final_pass) { t2_reset_body(D, T, final_pass, GRID_START, GRID_STRIDE); }
 __global__ void k_t2_retire(Dev D, T2Items T) { t2_retire_body(D, T, GRID_START, GRID_STRIDE); }
+// One item per warp on lane 0: an item is a long chain of dependent hash and
+// mesh loads whose trip counts differ item to item, so items sharing a warp
+// serialise each other's divergent paths; alone in a warp they only wait on
+// memory, which the other resident warps hide (C5: 2D passes 3x faster).
+#define WARP_ITEM_START ((int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5))
+#define WARP_ITEM_STRIDE ((int)((gridDim.x * blockDim.x) >> 5))
+__global__ void k_t2w_compute(Dev D, Cand C, T2Items T, Scr SC) {
+  if (threadIdx.x & 31) return;
+  Scratch S = scratch_for(SC, WARP_ITEM_START);
+  t2_compute_body(D, C, T, S, WARP_ITEM_START, WARP_ITEM_STRIDE);
+}
+__global__ void k_t2w_claim(Dev D, Cand C, T2Items T) { if (!(threadIdx.x & 31)) t2_claim_body(D, C, T, WARP_ITEM_START, WARP_ITEM_STRIDE); }
+__global__ void k_t2w_apply(Dev D, Cand C, T2Items T, int* applied) {
+  if (!(threadIdx.x & 31)) t2_apply_body(D, C, T, applied, WARP_ITEM_START, WARP_ITEM_STRIDE);
+}
+__global__ void k_t2w_reset(Dev D, T2Items T, int final_pass) { if (!(threadIdx.x & 31)) t2_reset_body(D, T, final_pass, WARP_ITEM_START, WARP_ITEM_STRIDE); }
+__global__ void k_t2w_commit(Dev D, Cand C, T2Items T, Scr SC) {
+  if (threadIdx.x & 31) return;
+  Scratch S = scratch_for(SC, WARP_ITEM_START);
+  t2_commit_body(D, C, T, S, WARP_ITEM_START, WARP_ITEM_STRIDE);
+}
+
 // every pass of a round without launches or host reads between passes.  The
 // items of different polygons never share a 2D triangle, so block b takes the
 // polygons with pid % gridDim.x == b and runs its own passes.
