@@ -64,7 +64,7 @@ __device__ __noinline__ bool face_check(const Dev& D, int r, Scratch& S) {
   return false;
 }
 // mode 0: records flagged CHECK; mode 1: every live record (full_verify)
-__global__ void k_check(Dev D, Scr SC, int mode, int* found) {
+__global__ void k_check(const __grid_constant__ Dev D, const __grid_constant__ Scr SC, int mode, int* found) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   Scratch S = scratch_for(SC, tid);
   int ns = D.ctr->nsegrec, nf = D.ctr->nfacerec;
@@ -81,14 +81,14 @@ __global__ void k_check(Dev D, Scr SC, int mode, int* found) {
     if (bad) { atomicOr(fl, RF_ENC); atomicAdd(found, 1); }
   }
 }
-__global__ void k_clear_flag(Dev D, unsigned int flag) {
+__global__ void k_clear_flag(const __grid_constant__ Dev D, unsigned int flag) {
   int ns = D.ctr->nsegrec, nf = D.ctr->nfacerec;
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < ns + nf; w += gridDim.x * blockDim.x) {
     if (w < ns) D.sg_fl[w] &= ~flag; else D.sf_fl[w - ns] &= ~flag;
   }
 }
 // counts: [0] pending segs, [1] pending faces, [2] enc segs (live), [3] enc faces
-__global__ void k_count_pending(Dev D, int* out) {
+__global__ void k_count_pending(const __grid_constant__ Dev D, int* out) {
   int ns = D.ctr->nsegrec, nf = D.ctr->nfacerec;
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < ns + nf; w += gridDim.x * blockDim.x) {
     unsigned int f = w < ns ? D.sg_fl[w] : D.sf_fl[w - ns];
@@ -98,7 +98,7 @@ __global__ void k_count_pending(Dev D, int* out) {
     if (!(f & RF_BLOCK) && !(f & RF_SKIP)) atomicAdd(out + base, 1);
   }
 }
-__global__ void k_flag_pending_keys(Dev D, int phase, unsigned int need, unsigned int deny, int* flags,
+__global__ void k_flag_pending_keys(const __grid_constant__ Dev D, int phase, unsigned int need, unsigned int deny, int* flags,
                                     unsigned long long* k1, unsigned int* k2) {
   int ns = D.ctr->nsegrec, nf = D.ctr->nfacerec;
   int n = phase == 0 ? ns : nf;
@@ -110,21 +110,21 @@ __global__ void k_flag_pending_keys(Dev D, int phase, unsigned int need, unsigne
     else { int4 q = D.sf_v[r]; k1[r] = key2(q.y, q.z); k2[r] = (unsigned int)q.x; }
   }
 }
-__global__ void k_face_a(Dev D, const int* recs, int n, unsigned int* out) {
+__global__ void k_face_a(const __grid_constant__ Dev D, const int* recs, int n, unsigned int* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = (unsigned int)D.sf_v[recs[i]].x;
 }
-__global__ void k_flag_bad(Dev D, double B, int* flags) {
+__global__ void k_flag_bad(const __grid_constant__ Dev D, double B, int* flags) {
   int nt = D.ctr->nt;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x)
     flags[t] = D.alive[t] == 1 && D.tv[t].w >= 0 && D.ratio[t] > B && D.skip[t] == 0;
 }
-__global__ void k_set_cands(Cand C, int n0, int n, int kind, const int* tgts, int pool0) {
+__global__ void k_set_cands(const __grid_constant__ Cand C, int n0, int n, int kind, const int* tgts, int pool0) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     C.kind[n0 + k] = kind; C.tgt[n0 + k] = tgts[k]; C.pool[n0 + k] = pool0 + k;
     C.status[n0 + k] = CS_OK; C.bigi[n0 + k] = -1;
   }
 }
-__global__ void k_clear_redir(Dev D, int phase) {
+__global__ void k_clear_redir(const __grid_constant__ Dev D, int phase) {
   int n = phase == 0 ? D.ctr->nsegrec : D.ctr->nfacerec;
   unsigned int* fl = phase == 0 ? D.sg_fl : D.sf_fl;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) fl[r] &= ~RF_REDIR;

@@ -127,7 +127,7 @@ __device__ __noinline__ void insert_one(const Dev& D, const Cand& C, int c, Scra
   }
 }
 
-__global__ void k_fallback(Dev D, Cand C, Scr SCB, FallbackIO F, T2Items T, SkipLog L) {
+__global__ void k_fallback(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Scr SCB, FallbackIO F, T2Items T, SkipLog L) {
   if (blockIdx.x || threadIdx.x) return;
   Scratch S = scratch_for(SCB, 0);
   CandCtx X; X.round_no = F.round_no; X.seed = F.seed; X.with_facets = F.with_facets;
@@ -205,7 +205,7 @@ __global__ void k_fallback(Dev D, Cand C, Scr SCB, FallbackIO F, T2Items T, Skip
 }
 
 // accepted tets whose region has a too-short boundary edge (refine.py:891-894)
-__global__ void k_accept_flags(Dev D, Cand C, const int* acc, int nacc, int* insflag, SkipLog L, int round_no, double lmin2) {
+__global__ void k_accept_flags(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const int* acc, int nacc, int* insflag, SkipLog L, int round_no, double lmin2) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nacc; k += gridDim.x * blockDim.x) {
     int c = acc[k];
     if (C.kind[c] == K_TET && C.mind[c] < lmin2) {
@@ -219,26 +219,26 @@ __global__ void k_accept_flags(Dev D, Cand C, const int* acc, int nacc, int* ins
     } else insflag[k] = 1;
   }
 }
-__global__ void k_assign_ids(Cand C, const int* ins, int n, const int* nbfscan, int nv0, int nt0) {
+__global__ void k_assign_ids(const __grid_constant__ Cand C, const int* ins, int n, const int* nbfscan, int nv0, int nt0) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     int c = ins[k];
     C.vid[c] = nv0 + k;
     C.nt0[c] = nt0 + nbfscan[k];
   }
 }
-__global__ void k_gather_nbf(Cand C, const int* ins, int n, int* out) {
+__global__ void k_gather_nbf(const __grid_constant__ Cand C, const int* ins, int n, int* out) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) out[k] = C.nbf[ins[k]];
 }
-__global__ void k_rank_scatter(Cand C, const int* order, int n) {
+__global__ void k_rank_scatter(const __grid_constant__ Cand C, const int* order, int n) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) C.rank[order[k]] = k;
 }
 
 // compaction of dead tet slots (mesh.py:847-865), stable
-__global__ void k_compact_flags(Dev D, int* flags) {
+__global__ void k_compact_flags(const __grid_constant__ Dev D, int* flags) {
   int nt = D.ctr->nt;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) flags[t] = D.alive[t] == 1;
 }
-__global__ void k_compact_move(Dev D, const int* remap, int nt, TetRow tv2, TetRow tn2, uint8_t* sub2, uint8_t* seg2,
+__global__ void k_compact_move(const __grid_constant__ Dev D, const int* remap, int nt, TetRow tv2, TetRow tn2, uint8_t* sub2, uint8_t* seg2,
                                double* ratio2, uint8_t* skip2) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
     if (D.alive[t] != 1) continue;
@@ -250,7 +250,7 @@ __global__ void k_compact_move(Dev D, const int* remap, int nt, TetRow tv2, TetR
     sub2[r] = D.sub[t]; seg2[r] = D.seg[t]; ratio2[r] = D.ratio[t]; skip2[r] = D.skip[t];
   }
 }
-__global__ void k_compact_vt(Dev D, const int* remap, const int* flags, int nv) {
+__global__ void k_compact_vt(const __grid_constant__ Dev D, const int* remap, const int* flags, int nv) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
     int t = D.vert_tet[v];
     D.vert_tet[v] = t >= 0 ? (flags[t] ? remap[t] : -1) : -1;
@@ -266,7 +266,7 @@ __device__ inline bool bin_edge(double ang) {
   double x = ang / 5.0;
   return fabs(x - rint(x)) < 1e-11 * fmax(1.0, x);
 }
-__global__ void k_quality(Dev D, double B, unsigned long long* bad, unsigned long long* hist, int* edge_list,
+__global__ void k_quality(const __grid_constant__ Dev D, double B, unsigned long long* bad, unsigned long long* hist, int* edge_list,
                           int edge_cap, int* n_edge) {
   int nt = D.ctr->nt;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
@@ -448,8 +448,8 @@ __device__ inline bool star_pairs_ok(const Dev& D, const int* bf, int nbf, const
   __syncwarp();
   return *X.flag == 0;
 }
-__global__ void __launch_bounds__(32 * WS_WARPS) k_star_check(Dev D, Cand C, const int* acc, int nacc, int* insflag,
-                                                            Scr SB, SkipLog L, int round_no) {
+__global__ void __launch_bounds__(32 * WS_WARPS) k_star_check(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const int* acc, int nacc, int* insflag,
+                                                            const __grid_constant__ Scr SB, SkipLog L, int round_no) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   StarShared& X = reinterpret_cast<StarShared*>(smem_raw)[wib];

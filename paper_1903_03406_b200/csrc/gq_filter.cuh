@@ -22,14 +22,14 @@ __device__ inline void for_claims(const Dev& D, const Cand& C, const Owners& W, 
   if (ex >= 0) f((C.kind[c] == K_SEG ? W.soff : W.foff) + ex);
 }
 
-__global__ void k_claim(Dev D, Cand C, Owners W, int n) {
+__global__ void k_claim(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Owners W, int n) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     if (C.state[c] != 0) continue;
     int r = C.rank[c];
     for_claims(D, C, W, c, [&](int k) { atomicMin(W.own + k, r); });
   }
 }
-__global__ void k_decide(Dev D, Cand C, Owners W, int n, int it) {
+__global__ void k_decide(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Owners W, int n, int it) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     if (C.state[c] != 0) continue;
     int r = C.rank[c];
@@ -38,14 +38,14 @@ __global__ void k_decide(Dev D, Cand C, Owners W, int n, int it) {
     if (win) C.state[c] = 10 + it;   // accepted this iteration (marked next)
   }
 }
-__global__ void k_mark(Dev D, Cand C, Owners W, int n, int it) {
+__global__ void k_mark(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Owners W, int n, int it) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     if (C.state[c] != 10 + it) continue;
     for_claims(D, C, W, c, [&](int k) { W.own[k] = -1; });
     C.state[c] = 1;
   }
 }
-__global__ void k_reject(Dev D, Cand C, Owners W, int n, int* undecided) {
+__global__ void k_reject(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Owners W, int n, int* undecided) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     if (C.state[c] != 0) continue;
     bool hit = false;
@@ -85,7 +85,7 @@ __device__ __forceinline__ void gsync() {
   if (ONE) __syncthreads(); else cg::this_grid().sync();
 }
 template <bool ONE>
-__global__ void __launch_bounds__(256) k_filter_coop(Dev D, Cand C, Owners W, int n, int* ctr) {
+__global__ void __launch_bounds__(256) k_filter_coop(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Owners W, int n, int* ctr) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -143,12 +143,12 @@ __global__ void __launch_bounds__(256) k_filter_coop(Dev D, Cand C, Owners W, in
     warp_claims(D, C, W, c, lane, [&](int k) { W.own[k] = INT_MAX; });
   }
 }
-__global__ void k_strict_state(Cand C, int n) {
+__global__ void k_strict_state(const __grid_constant__ Cand C, int n) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
     if (C.state[c] == 10) C.state[c] = 1;
     else if (C.state[c] == 0) C.state[c] = 2;
 }
-__global__ void k_reset_claims(Dev D, Cand C, Owners W, int n, int all) {
+__global__ void k_reset_claims(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Owners W, int n, int all) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     int s = C.state[c];
     if (!all && s != 0 && s != 2) continue;

@@ -48,7 +48,7 @@ __device__ inline bool cons_ball(const Dev& D, int kind, int r, double* c, doubl
 // where it spans at most 3 cells per axis, so a query reads one short run per
 // level and there is no "big ball" list scanned by everyone.
 // pass 0 counts, pass 1 fills.
-__global__ void k_grid_build(Dev D, CGrid g, int nseg, int nface, int pass) {
+__global__ void k_grid_build(const __grid_constant__ Dev D, CGrid g, int nseg, int nface, int pass) {
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nseg + nface; x += gridDim.x * blockDim.x) {
     int kind = x < nseg ? 0 : 1, r = x < nseg ? x : x - nseg;
     unsigned int fl = kind == 0 ? D.sg_fl[r] : D.sf_fl[r];
@@ -96,7 +96,7 @@ __device__ inline void grid_encroached(const Dev& D, const CGrid& g, const doubl
   }
 }
 // post_round part 1 (refine.py:818-828): new vertices against all balls
-__global__ void k_grid_newverts(Dev D, CGrid g, int v0, int v1) {
+__global__ void k_grid_newverts(const __grid_constant__ Dev D, CGrid g, int v0, int v1) {
   for (int v = v0 + blockIdx.x * blockDim.x + threadIdx.x; v < v1; v += gridDim.x * blockDim.x) {
     grid_encroached(D, g, PT(D, v), 3, [&](int kind, int r) {
       unsigned int* fl = kind == 0 ? D.sg_fl + r : D.sf_fl + r;
@@ -105,7 +105,7 @@ __global__ void k_grid_newverts(Dev D, CGrid g, int v0, int v1) {
   }
 }
 // redirect hits of candidate points (refine.py:603-613, 636-654)
-__global__ void k_grid_cands(Dev D, CGrid g, Cand C, int n0, int n1) {
+__global__ void k_grid_cands(const __grid_constant__ Dev D, CGrid g, const __grid_constant__ Cand C, int n0, int n1) {
   for (int c = n0 + blockIdx.x * blockDim.x + threadIdx.x; c < n1; c += gridDim.x * blockDim.x) {
     int kind = C.kind[c];
     C.nrseg[c] = 0; C.nrface[c] = 0;

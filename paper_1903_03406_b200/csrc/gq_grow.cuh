@@ -14,40 +14,40 @@
 __global__ void k_live_flags(const unsigned int* fl, int n, int* flags) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) flags[r] = (fl[r] & RF_LIVE) ? 1 : 0;
 }
-__global__ void k_move_seg_records(Dev D, const int* flags, const int* scan, int n, int2* uv2, int* sid2, unsigned int* fl2) {
+__global__ void k_move_seg_records(const __grid_constant__ Dev D, const int* flags, const int* scan, int n, int2* uv2, int* sid2, unsigned int* fl2) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     if (!flags[r]) continue;
     int q = scan[r];
     uv2[q] = D.sg_uv[r]; sid2[q] = D.sg_sid[r]; fl2[q] = D.sg_fl[r];
   }
 }
-__global__ void k_move_face_records(Dev D, const int* flags, const int* scan, int n, int4* v2, unsigned int* fl2) {
+__global__ void k_move_face_records(const __grid_constant__ Dev D, const int* flags, const int* scan, int n, int4* v2, unsigned int* fl2) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     if (!flags[r]) continue;
     int q = scan[r];
     v2[q] = D.sf_v[r]; fl2[q] = D.sf_fl[r];
   }
 }
-__global__ void k_rehash_segs(Dev D, int n) {
+__global__ void k_rehash_segs(const __grid_constant__ Dev D, int n) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     int2 e = D.sg_uv[r];
     ht_put(D.sg_hk, D.sg_hv, D.sg_hmask, key2(e.x, e.y), r);
   }
 }
-__global__ void k_rehash_faces(Dev D, int n) {
+__global__ void k_rehash_faces(const __grid_constant__ Dev D, int n) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     int4 f = D.sf_v[r];
     ht_put(D.sf_hk, D.sf_hv, D.sf_hmask, key3(f.x, f.y, f.z), r);
   }
 }
-__global__ void k_t2_live(Dev D, int n, int* flags) {
+__global__ void k_t2_live(const __grid_constant__ Dev D, int n, int* flags) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) flags[t] = D.t2alive[t] ? 1 : 0;
 }
-__global__ void k_t2_move(Dev D, const int* flags, const int* scan, int n, int4* v2) {
+__global__ void k_t2_move(const __grid_constant__ Dev D, const int* flags, const int* scan, int n, int4* v2) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
     if (flags[t]) v2[scan[t]] = D.t2v[t];
 }
-__global__ void k_t2_rehash(Dev D, int n) {
+__global__ void k_t2_rehash(const __grid_constant__ Dev D, int n) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     int4 q = D.t2v[t];
     ht_put(D.he_hk, D.he_hv, D.he_hmask, keyhe(q.x, q.y, q.w), t);
@@ -55,7 +55,7 @@ __global__ void k_t2_rehash(Dev D, int n) {
     ht_put(D.he_hk, D.he_hv, D.he_hmask, keyhe(q.z, q.x, q.w), t);
   }
 }
-__global__ void k_t2_last_remap(Dev D, const int* flags, const int* scan) {
+__global__ void k_t2_last_remap(const __grid_constant__ Dev D, const int* flags, const int* scan) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < D.npoly; p += gridDim.x * blockDim.x) {
     int t = D.t2last[p];
     D.t2last[p] = (t >= 0 && flags[t]) ? scan[t] : -1;
@@ -125,15 +125,15 @@ static void ensure_mesh_room(gq_ctx* c, long long nv_need, long long nt_need) {
 
 static int scan_total(gq_ctx* c, const int* in, int* out, int n);
 
-__global__ void k_rehash_live_segs(Dev D, int n) {
+__global__ void k_rehash_live_segs(const __grid_constant__ Dev D, int n) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
     if (D.sg_fl[r] & RF_LIVE) { int2 e = D.sg_uv[r]; ht_put(D.sg_hk, D.sg_hv, D.sg_hmask, key2(e.x, e.y), r); }
 }
-__global__ void k_rehash_live_faces(Dev D, int n) {
+__global__ void k_rehash_live_faces(const __grid_constant__ Dev D, int n) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
     if (D.sf_fl[r] & RF_LIVE) { int4 f = D.sf_v[r]; ht_put(D.sf_hk, D.sf_hv, D.sf_hmask, key3(f.x, f.y, f.z), r); }
 }
-__global__ void k_t2_rehash_live(Dev D, int n) {
+__global__ void k_t2_rehash_live(const __grid_constant__ Dev D, int n) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     if (!D.t2alive[t]) continue;
     int4 q = D.t2v[t];

@@ -539,10 +539,10 @@ static void ensure_huge(gq_ctx* c, int n, int mcap) {
   CK(cudaMemsetAsync(H.fepoch, 0, 4 * nb, c->st));
   c->hlist = dmalloc<int>(k); c->hlist_cap = k;
 }
-__global__ void k_status_of(Cand C, const int* list, int n, int* out) {
+__global__ void k_status_of(const __grid_constant__ Cand C, const int* list, int n, int* out) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) out[k] = C.status[list[k]];
 }
-__global__ void k_set_status(Cand C, const int* list, int n, int from, int to) {
+__global__ void k_set_status(const __grid_constant__ Cand C, const int* list, int n, int from, int to) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
     if (C.status[list[k]] == from) C.status[list[k]] = to;
 }
@@ -679,7 +679,7 @@ static int coop_share(gq_ctx* c, int full) {
 // equal (class, hash) -- a 64-bit splitmix collision -- is then put in
 // canonical-tuple order by the thread at its head (growblast.py:49 compares
 // the whole priority tuple).
-__global__ void k_rank_keys(Cand C, int n, unsigned long long* kh, unsigned int* kk, int* idx) {
+__global__ void k_rank_keys(const __grid_constant__ Cand C, int n, unsigned long long* kh, unsigned int* kk, int* idx) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     bool ok = C.status[c] == CS_OK;
     kh[c] = ok ? C.h[c] : ~0ull;
@@ -693,7 +693,7 @@ __device__ __forceinline__ bool canon_less(int4 a, int4 b) {
   if (a.z != b.z) return a.z < b.z;
   return a.w < b.w;
 }
-__global__ void k_rank_ties(Cand C, int* order, int n) {
+__global__ void k_rank_ties(const __grid_constant__ Cand C, int* order, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += gridDim.x * blockDim.x) {
     int a = order[i];
     if (C.status[a] != CS_OK) continue;
@@ -1098,7 +1098,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
 
 // ------------------------------------------------------------------ round
 
-__global__ void k_states(Dev D, Cand C, int n, int* okf, int* failf) {
+__global__ void k_states(const __grid_constant__ Dev D, const __grid_constant__ Cand C, int n, int* okf, int* failf) {
   unsigned long long claims = 0;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     int st = C.status[c];
@@ -1110,10 +1110,10 @@ __global__ void k_states(Dev D, Cand C, int n, int* okf, int* failf) {
   }
   if (claims) atomicAdd(&D.ctr->claims, claims);
 }
-__global__ void k_kept(Cand C, int n, int* keep) {
+__global__ void k_kept(const __grid_constant__ Cand C, int n, int* keep) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) keep[c] = C.status[c] != CS_DROP;
 }
-__global__ void k_acc_byrank(Cand C, int n, int* byrank) {
+__global__ void k_acc_byrank(const __grid_constant__ Cand C, int n, int* byrank) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
     if (C.state[c] == 1) byrank[C.rank[c]] = c;
 }
@@ -1123,14 +1123,14 @@ __global__ void k_nonneg(const int* a, int n, int* f) {
 __global__ void k_gather_i32(const int* src, const int* idx, int n, int* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[idx[i]];
 }
-__global__ void k_item_count(Dev D, Cand C, const int* ins, int ni, int* cnt) {
+__global__ void k_item_count(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const int* ins, int ni, int* cnt) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ni; k += gridDim.x * blockDim.x) {
     int c = ins[k], kind = C.kind[c];
     if (kind == K_SEG) { int sid = D.sg_sid[C.tgt[c]]; cnt[k] = D.segpoly_off[sid + 1] - D.segpoly_off[sid]; }
     else cnt[k] = kind == K_FACE ? 1 : 0;
   }
 }
-__global__ void k_item_fill(Dev D, Cand C, const int* ins, int ni, const int* off, const int* cnt, T2Items T, int* item_of) {
+__global__ void k_item_fill(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const int* ins, int ni, const int* off, const int* cnt, T2Items T, int* item_of) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ni; k += gridDim.x * blockDim.x) {
     int c = ins[k], kind = C.kind[c], o = off[k];
     item_of[2 * k] = o; item_of[2 * k + 1] = o + cnt[k];
@@ -1142,15 +1142,15 @@ __global__ void k_item_fill(Dev D, Cand C, const int* ins, int ni, const int* of
     }
   }
 }
-__global__ void k_count_seed_dead(Dev D, Cand C, int n, int* out) {
+__global__ void k_count_seed_dead(const __grid_constant__ Dev D, const __grid_constant__ Cand C, int n, int* out) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     if (C.state[c] != 2 || C.kind[c] != K_TET) continue;
     atomicAdd(out, 1);
     if (!D.alive[C.tgt[c]]) atomicAdd(out + 1, 1);
   }
 }
-__global__ void k_bump(Dev D, int dnv, int dnt) { D.ctr->nv += dnv; D.ctr->nt += dnt; }
-__global__ void k_pool_pos(Cand C, int n, const int* keepscan, const int* keep) {
+__global__ void k_bump(const __grid_constant__ Dev D, int dnv, int dnt) { D.ctr->nv += dnv; D.ctr->nt += dnt; }
+__global__ void k_pool_pos(const __grid_constant__ Cand C, int n, const int* keepscan, const int* keep) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
     C.pool[c] = keep[c] ? keepscan[c] : -1;
 }

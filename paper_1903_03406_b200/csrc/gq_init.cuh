@@ -7,7 +7,7 @@
 // pending point in a prefix window of the insertion order computes its
 // cavity; the filter accepts points whose claims avoid every lower-order
 // pending point, which makes the result the sequential one.
-__global__ void k_init_first(Dev D, const int* order, int n, int* first_out) {
+__global__ void k_init_first(const __grid_constant__ Dev D, const int* order, int n, int* first_out) {
   if (blockIdx.x || threadIdx.x) return;
   int first[4]; int nf = 0;
   first[nf++] = order[0];
@@ -69,7 +69,7 @@ __global__ void k_init_first(Dev D, const int* order, int n, int* first_out) {
 // Candidate c == pending point c (its position in the insertion order after
 // the first tet).  A point's cavity stays cached across rounds while all its
 // tets are alive and none of them was rewired since it was computed.
-__global__ void k_init_region(Dev D, Cand C, Scr SC, const int* pend, const int* plist, int W, int* hint,
+__global__ void k_init_region(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const __grid_constant__ Scr SC, const int* pend, const int* plist, int W, int* hint,
                               const int* succ, const int* touched, int round, int big) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   Scratch S = scratch_for(SC, tid);
@@ -108,13 +108,13 @@ __global__ void k_init_region(Dev D, Cand C, Scr SC, const int* pend, const int*
   }
 }
 // window filter: claims of every window point, strict lower-order rule
-__global__ void k_init_claim(Dev D, Cand C, Owners W, const int* plist, int nw) {
+__global__ void k_init_claim(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Owners W, const int* plist, int nw) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
     int c = plist[w];
     for_claims(D, C, W, c, [&](int k) { atomicMin(W.own + k, c); });
   }
 }
-__global__ void k_init_decide(Dev D, Cand C, Owners W, const int* plist, int nw, int* acc) {
+__global__ void k_init_decide(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Owners W, const int* plist, int nw, int* acc) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
     int c = plist[w];
     bool win = true;
@@ -122,7 +122,7 @@ __global__ void k_init_decide(Dev D, Cand C, Owners W, const int* plist, int nw,
     acc[w] = win ? 1 : 0;
   }
 }
-__global__ void k_init_unclaim(Dev D, Cand C, Owners W, const int* plist, int nw) {
+__global__ void k_init_unclaim(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Owners W, const int* plist, int nw) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x)
     for_claims(D, C, W, plist[w], [&](int k) { W.own[k] = INT_MAX; });
 }
@@ -131,7 +131,7 @@ __global__ void k_init_unclaim(Dev D, Cand C, Owners W, const int* plist, int nw
 // lane-parallel; block 0 scans acceptance and boundary-face counts between the
 // barriers; totals go to tot[0] (accepted) and tot[1] (new tets).
 template <bool ONE>
-__global__ void __launch_bounds__(256) k_init_filter_coop(Dev D, Cand C, Owners W, const int* plist, int nw_in, int nt,
+__global__ void __launch_bounds__(256) k_init_filter_coop(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Owners W, const int* plist, int nw_in, int nt,
                                                           int* acc, int* accscan, int* nbfscan, int* tot, int* succ) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
@@ -207,11 +207,11 @@ __global__ void k_init_compact2(const int* plist, const int* acc, const int* acc
   }
 }
 // accepted window points: new tet ids (scan of nbf in insertion order)
-__global__ void k_init_nbf(Cand C, const int* plist, const int* acc, int nw, int* nbfv) {
+__global__ void k_init_nbf(const __grid_constant__ Cand C, const int* plist, const int* acc, int nw, int* nbfv) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x)
     nbfv[w] = acc[w] ? C.nbf[plist[w]] : 0;
 }
-__global__ void k_init_kill(Dev D, Cand C, const int* plist, const int* acc, const int* scan, int nw, int nt,
+__global__ void k_init_kill(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const int* plist, const int* acc, const int* scan, int nw, int nt,
                             int* succ) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
     if (!acc[w]) continue;
@@ -223,7 +223,7 @@ __global__ void k_init_kill(Dev D, Cand C, const int* plist, const int* acc, con
     for (int j = 0; j < C.ntet[c]; ++j) { D.alive[v.tets[j]] = 0; succ[v.tets[j]] = nt0; }
   }
 }
-__global__ void k_init_stars(Dev D, Cand C, const int* pend, const int* plist, const int* acc, int nw,
+__global__ void k_init_stars(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const int* pend, const int* plist, const int* acc, int nw,
                              int* touched, int round) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
     if (!acc[w]) continue;
@@ -237,15 +237,15 @@ __global__ void k_init_stars(Dev D, Cand C, const int* pend, const int* plist, c
     C.status[c] = CS_DROP;
   }
 }
-__global__ void k_count_ovf(const Cand C, const int* plist, int W, int* out) {
+__global__ void k_count_ovf(const const __grid_constant__ Cand C, const int* plist, int W, int* out) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x)
     if (C.status[plist[w]] == CS_OVF) atomicAdd(out, 1);
     else if (C.status[plist[w]] == CS_OK) atomicMax(out + 1, C.ntet[plist[w]]);
 }
-__global__ void k_gather_status(const Cand C, const int* plist, int W, int* out) {
+__global__ void k_gather_status(const const __grid_constant__ Cand C, const int* plist, int W, int* out) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) out[w] = C.status[plist[w]];
 }
-__global__ void k_release_big(Cand C, const int* list, int n) {
+__global__ void k_release_big(const __grid_constant__ Cand C, const int* list, int n) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     int c = list[k];
     if (C.status[c] != CS_DROP) { C.status[c] = CS_OK; C.memb[c] = -2; }   // -2: was big, route to the block kernel
@@ -265,7 +265,7 @@ __global__ void k_init_keep(const int* acc, int nw, int* keep) {
 }
 
 // facet bootstrap: one thread per polygon (facets.py:57-90, 342-372)
-__global__ void k_facets_init(Dev D, const int* poff, const int* pidx, int f, Scr SC, int* t2base) {
+__global__ void k_facets_init(const __grid_constant__ Dev D, const int* poff, const int* pidx, int f, const __grid_constant__ Scr SC, int* t2base) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   Scratch S = scratch_for(SC, tid);
   for (int pid = tid; pid < f; pid += gridDim.x * blockDim.x) {
@@ -308,7 +308,7 @@ __global__ void k_facets_init(Dev D, const int* poff, const int* pidx, int f, Sc
     }
   }
 }
-__global__ void k_facets_records(Dev D, int nt2) {
+__global__ void k_facets_records(const __grid_constant__ Dev D, int nt2) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt2; t += gridDim.x * blockDim.x) {
     if (!D.t2alive[t]) continue;
     int4 q = D.t2v[t];
@@ -317,7 +317,7 @@ __global__ void k_facets_records(Dev D, int nt2) {
     new_face_record(D, q.x, q.y, q.z, q.w, RF_LIVE);
   }
 }
-__global__ void k_segs_init(Dev D, const int* seg, int m) {
+__global__ void k_segs_init(const __grid_constant__ Dev D, const int* seg, int m) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < m; s += gridDim.x * blockDim.x) {
     int u = seg[2 * s], v = seg[2 * s + 1];
     if (u > v) { int t = u; u = v; v = t; }
@@ -326,7 +326,7 @@ __global__ void k_segs_init(Dev D, const int* seg, int m) {
     ht_put(D.sg_hk, D.sg_hv, D.sg_hmask, key2(u, v), s);
   }
 }
-__global__ void k_refresh_all(Dev D) {
+__global__ void k_refresh_all(const __grid_constant__ Dev D) {
   int nt = D.ctr->nt;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x)
     if (D.alive[t]) refresh_masks(D, t);

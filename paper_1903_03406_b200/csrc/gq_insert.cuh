@@ -10,7 +10,7 @@ struct Ins {          // inserted candidates in priority order
 };
 
 // vertex ids / points / subsegment splits (refine.py:688-708 bookkeeping)
-__global__ void k_ins_vertices(Dev D, Cand C, Ins I) {
+__global__ void k_ins_vertices(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Ins I) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < I.n; k += gridDim.x * blockDim.x) {
     int c = I.list[k];
     int vid = C.vid[c];
@@ -102,7 +102,7 @@ __device__ __noinline__ bool tri_in_polygon(const Dev& D, int pid, int a, int b,
   }
   return inside;
 }
-__global__ void k_poly_convex(Dev D, int f) {
+__global__ void k_poly_convex(const __grid_constant__ Dev D, int f) {
   for (int pid = blockIdx.x * blockDim.x + threadIdx.x; pid < f; pid += gridDim.x * blockDim.x) {
     const int o0 = D.poly_off[pid], n = D.poly_off[pid + 1] - o0;
     int2 kp = D.poly_keep[pid];
@@ -117,7 +117,7 @@ __global__ void k_poly_convex(Dev D, int f) {
   }
 }
 
-__global__ void k_ins_segsplit(Dev D, Cand C, Ins I) {
+__global__ void k_ins_segsplit(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Ins I) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < I.n; k += gridDim.x * blockDim.x) {
     int c = I.list[k];
     if (C.kind[c] != K_SEG) continue;
@@ -298,35 +298,35 @@ __device__ void t2_retire_body(const Dev& D, const T2Items& T, int start, int st
 
 #define GRID_START (blockIdx.x * blockDim.x + threadIdx.x)
 #define GRID_STRIDE (gridDim.x * blockDim.x)
-__global__ void k_t2_compute(Dev D, Cand C, T2Items T, Scr SC) {
+__global__ void k_t2_compute(const __grid_constant__ Dev D, const __grid_constant__ Cand C, T2Items T, const __grid_constant__ Scr SC) {
   Scratch S = scratch_for(SC, GRID_START);
   t2_compute_body(D, C, T, S, GRID_START, GRID_STRIDE);
 }
-__global__ void k_t2_claim(Dev D, Cand C, T2Items T) { t2_claim_body(D, C, T, GRID_START, GRID_STRIDE); }
-__global__ void k_t2_apply(Dev D, Cand C, T2Items T, Scr SC, int* applied) { t2_apply_body(D, C, T, applied, GRID_START, GRID_STRIDE); }
-__global__ void k_t2_commit(Dev D, Cand C, T2Items T, Scr SC) {
+__global__ void k_t2_claim(const __grid_constant__ Dev D, const __grid_constant__ Cand C, T2Items T) { t2_claim_body(D, C, T, GRID_START, GRID_STRIDE); }
+__global__ void k_t2_apply(const __grid_constant__ Dev D, const __grid_constant__ Cand C, T2Items T, const __grid_constant__ Scr SC, int* applied) { t2_apply_body(D, C, T, applied, GRID_START, GRID_STRIDE); }
+__global__ void k_t2_commit(const __grid_constant__ Dev D, const __grid_constant__ Cand C, T2Items T, const __grid_constant__ Scr SC) {
   Scratch S = scratch_for(SC, GRID_START);
   t2_commit_body(D, C, T, S, GRID_START, GRID_STRIDE);
 }
-__global__ void k_t2_reset(Dev D, Cand C, T2Items T, int final_pass) { t2_reset_body(D, T, final_pass, GRID_START, GRID_STRIDE); }
-__global__ void k_t2_retire(Dev D, T2Items T) { t2_retire_body(D, T, GRID_START, GRID_STRIDE); }
+__global__ void k_t2_reset(const __grid_constant__ Dev D, const __grid_constant__ Cand C, T2Items T, int final_pass) { t2_reset_body(D, T, final_pass, GRID_START, GRID_STRIDE); }
+__global__ void k_t2_retire(const __grid_constant__ Dev D, T2Items T) { t2_retire_body(D, T, GRID_START, GRID_STRIDE); }
 // One item per warp on lane 0: an item is a long chain of dependent hash and
 // mesh loads whose trip counts differ item to item, so items sharing a warp
 // serialise each other's divergent paths; alone in a warp they only wait on
 // memory, which the other resident warps hide (C5: 2D passes 3x faster).
 #define WARP_ITEM_START ((int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5))
 #define WARP_ITEM_STRIDE ((int)((gridDim.x * blockDim.x) >> 5))
-__global__ void k_t2w_compute(Dev D, Cand C, T2Items T, Scr SC) {
+__global__ void k_t2w_compute(const __grid_constant__ Dev D, const __grid_constant__ Cand C, T2Items T, const __grid_constant__ Scr SC) {
   if (threadIdx.x & 31) return;
   Scratch S = scratch_for(SC, WARP_ITEM_START);
   t2_compute_body(D, C, T, S, WARP_ITEM_START, WARP_ITEM_STRIDE);
 }
-__global__ void k_t2w_claim(Dev D, Cand C, T2Items T) { if (!(threadIdx.x & 31)) t2_claim_body(D, C, T, WARP_ITEM_START, WARP_ITEM_STRIDE); }
-__global__ void k_t2w_apply(Dev D, Cand C, T2Items T, int* applied) {
+__global__ void k_t2w_claim(const __grid_constant__ Dev D, const __grid_constant__ Cand C, T2Items T) { if (!(threadIdx.x & 31)) t2_claim_body(D, C, T, WARP_ITEM_START, WARP_ITEM_STRIDE); }
+__global__ void k_t2w_apply(const __grid_constant__ Dev D, const __grid_constant__ Cand C, T2Items T, int* applied) {
   if (!(threadIdx.x & 31)) t2_apply_body(D, C, T, applied, WARP_ITEM_START, WARP_ITEM_STRIDE);
 }
-__global__ void k_t2w_reset(Dev D, T2Items T, int final_pass) { if (!(threadIdx.x & 31)) t2_reset_body(D, T, final_pass, WARP_ITEM_START, WARP_ITEM_STRIDE); }
-__global__ void k_t2w_commit(Dev D, Cand C, T2Items T, Scr SC) {
+__global__ void k_t2w_reset(const __grid_constant__ Dev D, T2Items T, int final_pass) { if (!(threadIdx.x & 31)) t2_reset_body(D, T, final_pass, WARP_ITEM_START, WARP_ITEM_STRIDE); }
+__global__ void k_t2w_commit(const __grid_constant__ Dev D, const __grid_constant__ Cand C, T2Items T, const __grid_constant__ Scr SC) {
   if (threadIdx.x & 31) return;
   Scratch S = scratch_for(SC, WARP_ITEM_START);
   t2_commit_body(D, C, T, S, WARP_ITEM_START, WARP_ITEM_STRIDE);
@@ -335,7 +335,7 @@ __global__ void k_t2w_commit(Dev D, Cand C, T2Items T, Scr SC) {
 // every pass of a round without launches or host reads between passes.  The
 // items of different polygons never share a 2D triangle, so block b takes the
 // polygons with pid % gridDim.x == b and runs its own passes.
-__global__ void __launch_bounds__(128) k_t2_fused(Dev D, Cand C, T2Items T, Scr SC, int* applied_total) {
+__global__ void __launch_bounds__(128) k_t2_fused(const __grid_constant__ Dev D, const __grid_constant__ Cand C, T2Items T, const __grid_constant__ Scr SC, int* applied_total) {
   Scratch S = scratch_for(SC, blockIdx.x * blockDim.x + threadIdx.x);
   const int pm = gridDim.x, pb = blockIdx.x;
   __shared__ int s_applied, s_left;
@@ -369,14 +369,14 @@ __global__ void __launch_bounds__(128) k_t2_fused(Dev D, Cand C, T2Items T, Scr 
   if (threadIdx.x == 0) atomicAdd(applied_total, total - left);
 }
 
-__global__ void k_kill_cavities(Dev D, Cand C, Ins I) {
+__global__ void k_kill_cavities(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Ins I) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < I.n; k += gridDim.x * blockDim.x) {
     int c = I.list[k];
     SlabView v = slab(C, c);
     for (int j = 0; j < C.ntet[c]; ++j) D.alive[v.tets[j]] = 0;
   }
 }
-__global__ void k_star(Dev D, Cand C, Ins I) {
+__global__ void k_star(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Ins I) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < I.n; k += gridDim.x * blockDim.x) {
     int c = I.list[k];
     SlabView v = slab(C, c);
@@ -402,7 +402,7 @@ __device__ inline StarHash huge_star_hash(const Cand& C, int c, int* flag) {
   X.key = C.hskey + h; X.v0 = C.hsv0 + h; X.v1 = C.hsv1 + h; X.cap = C.hs; X.flag = flag;
   return X;
 }
-__global__ void __launch_bounds__(32 * WS_WARPS) k_star_warp(Dev D, Cand C, Ins I, Scr SB) {
+__global__ void __launch_bounds__(32 * WS_WARPS) k_star_warp(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Ins I, const __grid_constant__ Scr SB) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   StarShared& X = reinterpret_cast<StarShared*>(smem_raw)[wib];
@@ -420,8 +420,8 @@ __global__ void __launch_bounds__(32 * WS_WARPS) k_star_warp(Dev D, Cand C, Ins 
   }
   if (lane == 0 && n_created) { atomicAdd(&D.ctr->created, n_created); atomicAdd(&D.ctr->deleted, n_deleted); }
 }
-__global__ void __launch_bounds__(32 * WS_WARPS) k_init_stars_warp(Dev D, Cand C, const int* pend, const int* plist,
-                                                                   const int* acc, int nw_, int* touched, int round, Scr SB) {
+__global__ void __launch_bounds__(32 * WS_WARPS) k_init_stars_warp(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const int* pend, const int* plist,
+                                                                   const int* acc, int nw_, int* touched, int round, const __grid_constant__ Scr SB) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   StarShared& X = reinterpret_cast<StarShared*>(smem_raw)[wib];
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(32 * WS_WARPS) k_init_stars_warp(Dev D, Cand C
 
 // dirty constraints + survivor mask refresh for subfaces retiled in 2D but
 // not crossed by the 3D cavity (refine.py:720-736)
-__global__ void k_post_insert(Dev D, Cand C, Ins I, T2Items T, Scr SC, const int* item_of) {
+__global__ void k_post_insert(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Ins I, T2Items T, const __grid_constant__ Scr SC, const int* item_of) {
   int tid0 = blockIdx.x * blockDim.x + threadIdx.x;
   Scratch S = scratch_for(SC, tid0);
   for (int k = tid0; k < I.n; k += gridDim.x * blockDim.x) {

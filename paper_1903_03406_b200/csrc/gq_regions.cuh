@@ -6,7 +6,7 @@
 // kernels
 // ===========================================================================
 
-__global__ void k_make_cands(Dev D, Cand C, Scr SC, int n0, int n1, CandCtx X, SkipLog L, double lmin2) {
+__global__ void k_make_cands(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const __grid_constant__ Scr SC, int n0, int n1, CandCtx X, SkipLog L, double lmin2) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   Scratch S = scratch_for(SC, tid);
   unsigned long long n_cands = 0;
@@ -42,7 +42,7 @@ __global__ void k_make_cands(Dev D, Cand C, Scr SC, int n0, int n1, CandCtx X, S
 }
 
 // region of every candidate in [n0,n1) with status OK (or the listed ones)
-__global__ void k_region(Dev D, Cand C, Scr SC, int n0, int n1, const int* list, int probe, int big) {
+__global__ void k_region(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const __grid_constant__ Scr SC, int n0, int n1, const int* list, int probe, int big) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   Scratch S = scratch_for(SC, tid);
   int n = list ? n1 : n1 - n0;
@@ -84,7 +84,7 @@ __device__ __forceinline__ int cell_of(const CellHint& H, const double* p) {
   }
   return (c[0] * H.G + c[1]) * H.G + c[2];
 }
-__global__ void k_init_cellmark(Dev D, CellHint H, const int* pend, const int* plist, const int* acc, int nw) {
+__global__ void k_init_cellmark(const __grid_constant__ Dev D, CellHint H, const int* pend, const int* plist, const int* acc, int nw) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x)
     if (acc[w]) { int v = pend[plist[w]]; H.cellv[cell_of(H, PT(D, v))] = v; }
 }
@@ -117,7 +117,7 @@ typedef WarpSharedT<WT1_MAXT, WT1_HASH> WarpShared1;
 typedef WarpSharedT<WT2_MAXT, WT2_HASH> WarpShared2;
 // candidates [n0,n1) (list == nullptr) or list[n0..n1) (the small tier's overflows)
 template <int MAXT, int HASH, int MINB>
-__global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_region_warp(Dev D, Cand C, Scr SC, int n0, int n1, const int* list) {
+__global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_region_warp(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const __grid_constant__ Scr SC, int n0, int n1, const int* list) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   typedef WarpSharedT<MAXT, HASH> WS;
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_region_warp(Dev D, Cand
 // bulk construction, warp per pending point (cached cavities re-validated);
 // redo_ovf: the large tier, run on the small tier's overflows
 template <int MAXT, int HASH, int MINB>
-__global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_init_region_warp(Dev D, Cand C, Scr SC, const int* pend, const int* plist,
+__global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_init_region_warp(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const __grid_constant__ Scr SC, const int* pend, const int* plist,
                                                                     int Wn, int* hint, const int* succ, const int* touched, int round,
                                                                     CellHint H, int redo_ovf) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -254,7 +254,7 @@ __device__ inline void block_region_cand(const Dev& D, const Cand& C, int c, Blo
     }
     __syncthreads();
 }
-__global__ void __launch_bounds__(BR_THREADS) k_region_block(Dev D, Cand C, Scr SB, const int* list, int nb, int base) {
+__global__ void __launch_bounds__(BR_THREADS) k_region_block(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const __grid_constant__ Scr SB, const int* list, int nb, int base) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ BlockView B;
   if (threadIdx.x == 0) view_of_shared(B, *reinterpret_cast<BlockShared*>(smem_raw));
@@ -274,7 +274,7 @@ struct HugeArena {
   unsigned long long* fkey; unsigned int* fep; unsigned int* fepoch;         // per block constraint-pass set (fcap)
   int hcap, mcap, fcap, nblocks;
 };
-__global__ void __launch_bounds__(BR_THREADS) k_region_huge(Dev D, Cand C, Scr SB, HugeArena H, const int* list, int nb) {
+__global__ void __launch_bounds__(BR_THREADS) k_region_huge(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const __grid_constant__ Scr SB, HugeArena H, const int* list, int nb) {
   __shared__ BlockView B;
   const int b = blockIdx.x;
   if (threadIdx.x == 0) {
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(BR_THREADS) k_region_huge(Dev D, Cand C, Scr S
     block_region_cand(D, C, c, B, S);
   }
 }
-__global__ void __launch_bounds__(BR_THREADS) k_init_region_block(Dev D, Cand C, Scr SB, const int* pend, const int* list, int nb,
+__global__ void __launch_bounds__(BR_THREADS) k_init_region_block(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const __grid_constant__ Scr SB, const int* pend, const int* list, int nb,
                                                                   int* hint, const int* succ, int round) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ BlockView B;
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(BR_THREADS) k_init_region_block(Dev D, Cand C,
 }
 
 // redirect decision (refine.py:595-613, 615-662); marks records RF_REDIR
-__global__ void k_redirect(Dev D, Cand C, int n0, int n1, int* nredir) {
+__global__ void k_redirect(const __grid_constant__ Dev D, const __grid_constant__ Cand C, int n0, int n1, int* nredir) {
   for (int c = n0 + blockIdx.x * blockDim.x + threadIdx.x; c < n1; c += gridDim.x * blockDim.x) {
     int kind = C.kind[c];
     if (kind == K_SEG || C.status[c] == CS_DROP) continue;
