@@ -95,6 +95,69 @@ __device__ inline void grid_encroached(const Dev& D, const CGrid& g, const doubl
     for (int k = g.start[cell]; k < e; ++k) test(g.codes[k]);
   }
 }
+// A query's cell lists can run to hundreds of balls (coarse levels, few and
+// large constraints early on): the warp versions below scan them 32 at a time.
+__device__ inline int grid_hit(const Dev& D, int code, const double* p, int kinds) {   // kind hit, or -1
+  int kind = code & 1, r = code >> 1;
+  if (!((kinds >> kind) & 1)) return -1;
+  if (kind == 0) {
+    if (!(D.sg_fl[r] & RF_LIVE)) return -1;
+    int2 e = D.sg_uv[r];
+    return encroaches_segment(PT(D, e.x), PT(D, e.y), p) ? 0 : -1;
+  }
+  if (!(D.sf_fl[r] & RF_LIVE)) return -1;
+  int4 q = D.sf_v[r];
+  return encroaches_face(PT(D, q.x), PT(D, q.y), PT(D, q.z), p) ? 1 : -1;
+}
+// warp-uniform p; f(kind, rec, hit) is called by every lane once per chunk of
+// 32 list entries (hit false on lanes without one), so callers can ballot
+template <class F>
+__device__ inline void grid_encroached_warp(const Dev& D, const CGrid& g, const double* p, int kinds, F f) {
+  const int lane = threadIdx.x & 31;
+  const int ci = cg_ci(g, p[0], 0), cj = cg_ci(g, p[1], 1), ck = cg_ci(g, p[2], 2);
+  for (int l = 0; l < g.L; ++l) {
+    const int Gl = cg_gl(g.G, l);
+    const int cell = g.off[l] + ((ci >> l) * Gl + (cj >> l)) * Gl + (ck >> l);
+    const int s = g.start[cell], e = g.start[cell + 1];
+    for (int b = s; b < e; b += 32) {
+      int k = b + lane, kind = -1, r = -1;
+      if (k < e) { int code = g.codes[k]; r = code >> 1; kind = grid_hit(D, code, p, kinds); }
+      f(kind, r);
+    }
+  }
+}
+#define GRID_WARP0 ((int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5))
+#define GRID_NWARP ((int)((gridDim.x * blockDim.x) >> 5))
+__global__ void k_grid_newverts_w(const __grid_constant__ Dev D, CGrid g, int v0, int v1) {
+  for (int v = v0 + GRID_WARP0; v < v1; v += GRID_NWARP)
+    grid_encroached_warp(D, g, PT(D, v), 3, [&](int kind, int r) {
+      if (kind < 0) return;
+      unsigned int* fl = kind == 0 ? D.sg_fl + r : D.sf_fl + r;
+      if (!(*fl & RF_SKIP)) atomicOr(fl, RF_ENC);
+    });
+}
+__global__ void k_grid_cands_w(const __grid_constant__ Dev D, CGrid g, const __grid_constant__ Cand C, int n0, int n1) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int c = n0 + GRID_WARP0; c < n1; c += GRID_NWARP) {
+    int kind = C.kind[c];
+    if (kind == K_SEG || C.status[c] == CS_DROP) {
+      if (lane == 0) { C.nrseg[c] = 0; C.nrface[c] = 0; }
+      continue;
+    }
+    int ns = 0, nf = 0;
+    int* rs = C.rseg + (size_t)c * CRD;
+    int* rf = C.rface + (size_t)c * CRD;
+    grid_encroached_warp(D, g, C.p + 3 * (size_t)c, kind == K_TET ? 3 : 1, [&](int k, int r) {
+      bool hs = k == 0 && !(D.sg_fl[r] & RF_SKIP), hf = k == 1 && !(D.sf_fl[r] & RF_SKIP);
+      unsigned ms = __ballot_sync(0xffffffffu, hs), mf = __ballot_sync(0xffffffffu, hf);
+      if (hs) { int q = ns + __popc(ms & lt); if (q < CRD) rs[q] = r; else raise_err(GQ_ERR_CAP); }
+      if (hf) { int q = nf + __popc(mf & lt); if (q < CRD) rf[q] = r; else raise_err(GQ_ERR_CAP); }
+      ns += __popc(ms); nf += __popc(mf);
+    });
+    if (lane == 0) { C.nrseg[c] = ns < CRD ? ns : CRD; C.nrface[c] = nf < CRD ? nf : CRD; }
+  }
+}
 // post_round part 1 (refine.py:818-828): new vertices against all balls
 __global__ void k_grid_newverts(const __grid_constant__ Dev D, CGrid g, int v0, int v1) {
   for (int v = v0 + blockIdx.x * blockDim.x + threadIdx.x; v < v1; v += gridDim.x * blockDim.x) {

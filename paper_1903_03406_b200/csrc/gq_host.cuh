@@ -128,6 +128,7 @@ static double now_s() { return std::chrono::duration<double>(std::chrono::steady
 static thread_local double g_prof[8];
 // fine stage timers (GQ_PROFILE=2): synchronise and charge the elapsed time
 static thread_local bool g_trace = false;
+static const bool g_grid_thread = getenv("GQ_GRID_THREAD") != nullptr;   // experiments: thread-per-query grid kernels
 static thread_local bool g_fine = false;      // GQ_PROFILE=2: host clock after a sync per stage
 static thread_local bool g_fine_ev = false;   // GQ_PROFILE=3: events per stage (device timeline, no syncs)
 static thread_local double g_fine_t[40];
@@ -1224,7 +1225,8 @@ static void insert_accepted(gq_ctx* c, int n, long long* nacc_out, long long* in
   if (nit > 0 && nit <= t2_fused_max) {   // few items: all passes in one launch, polygons split over blocks
     c->T.n = nit;
     CK(cudaMemsetAsync(c->d_int + 16, 0, 4, c->st));
-    k_t2_fused<<<std::min(std::min(nit, c->npoly), c->S.nthreads / 128), 128, 0, c->st>>>(c->D, C, c->T, c->S, c->d_int + 16);
+    if (t2_thread) k_t2_fused<false><<<std::min(std::min(nit, c->npoly), c->S.nthreads / 128), 128, 0, c->st>>>(c->D, C, c->T, c->S, c->d_int + 16);
+    else k_t2_fused<true><<<std::min(std::min(nit, c->npoly), c->S.nthreads / 8), 256, 0, c->st>>>(c->D, C, c->T, c->S, c->d_int + 16);
     c->launches++;
     CK(cudaGetLastError());
   } else if (nit > 0) {
@@ -1384,7 +1386,8 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     double t1 = now_s();
     // redirects first (refine.py:603-662): dropped candidates need no region
     grid_sync(c);
-    LAUNCH(k_grid_cands, nbase, c->D, c->G, c->C, 0, nbase);
+    if (g_grid_thread) LAUNCH(k_grid_cands, nbase, c->D, c->G, c->C, 0, nbase);
+    else LAUNCH_W(k_grid_cands_w, nbase, c->D, c->G, c->C, 0, nbase);
     fine(c, 28);
     CK(cudaMemsetAsync(c->d_int + 60, 0, 8, c->st));
     LAUNCH(k_redirect, nbase, c->D, c->C, 0, nbase, c->d_int + 60);
@@ -1454,7 +1457,10 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   fine(c, -1);
   grid_sync(c);
   fine(c, 7);
-  if (c->hc.nv > c->reg_nv) LAUNCH(k_grid_newverts, c->hc.nv - c->reg_nv, c->D, c->G, c->reg_nv, c->hc.nv);
+  if (c->hc.nv > c->reg_nv) {
+    if (g_grid_thread) LAUNCH(k_grid_newverts, c->hc.nv - c->reg_nv, c->D, c->G, c->reg_nv, c->hc.nv);
+    else LAUNCH_W(k_grid_newverts_w, c->hc.nv - c->reg_nv, c->D, c->G, c->reg_nv, c->hc.nv);
+  }
   c->reg_nv = c->hc.nv;
   fine(c, 8);
   CK(cudaMemsetAsync(c->d_int, 0, 16, c->st));

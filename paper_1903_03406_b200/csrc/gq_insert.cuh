@@ -335,9 +335,13 @@ __global__ void k_t2w_commit(const __grid_constant__ Dev D, const __grid_constan
 // every pass of a round without launches or host reads between passes.  The
 // items of different polygons never share a 2D triangle, so block b takes the
 // polygons with pid % gridDim.x == b and runs its own passes.
-__global__ void __launch_bounds__(128) k_t2_fused(const __grid_constant__ Dev D, const __grid_constant__ Cand C, T2Items T, const __grid_constant__ Scr SC, int* applied_total) {
-  Scratch S = scratch_for(SC, blockIdx.x * blockDim.x + threadIdx.x);
+// WARP: one item per warp (lane 0) as in the multi-launch passes
+template <bool WARP>
+__global__ void __launch_bounds__(256) k_t2_fused(const __grid_constant__ Dev D, const __grid_constant__ Cand C, T2Items T, const __grid_constant__ Scr SC, int* applied_total) {
+  const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5;
+  Scratch S = scratch_for(SC, WARP ? blockIdx.x * nw + wid : blockIdx.x * blockDim.x + threadIdx.x);
   const int pm = gridDim.x, pb = blockIdx.x;
+  const int i0 = WARP ? ((threadIdx.x & 31) ? T.n : wid) : threadIdx.x, di = WARP ? nw : blockDim.x;
   __shared__ int s_applied, s_left;
   if (threadIdx.x == 0) s_left = 0;
   __syncthreads();
@@ -349,15 +353,15 @@ __global__ void __launch_bounds__(128) k_t2_fused(const __grid_constant__ Dev D,
   const int total = left;
   for (int pass = 0; left > 0; ++pass) {
     if (threadIdx.x == 0) s_applied = 0;
-    t2_compute_body(D, C, T, S, threadIdx.x, blockDim.x, pm, pb);
+    t2_compute_body(D, C, T, S, i0, di, pm, pb);
     __syncthreads();
-    t2_claim_body(D, C, T, threadIdx.x, blockDim.x, pm, pb);
+    t2_claim_body(D, C, T, i0, di, pm, pb);
     __syncthreads();
-    t2_apply_body(D, C, T, &s_applied, threadIdx.x, blockDim.x, pm, pb);
+    t2_apply_body(D, C, T, &s_applied, i0, di, pm, pb);
     __syncthreads();
-    t2_reset_body(D, T, 1, threadIdx.x, blockDim.x, pm, pb);
+    t2_reset_body(D, T, 1, i0, di, pm, pb);
     __syncthreads();
-    t2_commit_body(D, C, T, S, threadIdx.x, blockDim.x, pm, pb);
+    t2_commit_body(D, C, T, S, i0, di, pm, pb);
     __syncthreads();
     t2_retire_body(D, T, threadIdx.x, blockDim.x, pm, pb);
     __syncthreads();
