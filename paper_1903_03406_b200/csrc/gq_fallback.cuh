@@ -268,6 +268,10 @@ __device__ inline bool bin_edge(double ang) {
 }
 __global__ void k_quality(const __grid_constant__ Dev D, double B, unsigned long long* bad, unsigned long long* hist, int* edge_list,
                           int edge_cap, int* n_edge) {
+  // per-block counts in shared memory, one global add per bin per block
+  __shared__ unsigned int s_cnt[37];   // [0] bad, [1 + b] histogram bin b
+  for (int i = threadIdx.x; i < 37; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
   int nt = D.ctr->nt;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
     if (!D.alive[t] || D.tv[t].w == GHOST) continue;
@@ -293,7 +297,7 @@ __global__ void k_quality(const __grid_constant__ Dev D, double B, unsigned long
     }
     double ratio = sqrt(r2 / sh);
     if (!isfinite(ratio)) ratio = INFINITY;
-    if (ratio > B) atomicAdd(bad, 1ull);
+    if (ratio > B) atomicAdd(&s_cnt[0], 1u);
     int bins[6];
     bool edge = false;
     for (int e = 0; e < 6; ++e) {
@@ -319,8 +323,11 @@ __global__ void k_quality(const __grid_constant__ Dev D, double B, unsigned long
       int k = atomicAdd(n_edge, 1);
       if (k < edge_cap) { edge_list[k] = t; continue; }
     }
-    for (int e = 0; e < 6; ++e) atomicAdd(hist + bins[e], 1ull);
+    for (int e = 0; e < 6; ++e) atomicAdd(&s_cnt[1 + bins[e]], 1u);
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 37; i += blockDim.x)
+    if (s_cnt[i]) atomicAdd(i == 0 ? bad : hist + (i - 1), (unsigned long long)s_cnt[i]);
 }
 
 // batched predicates / constructions for parity tests (gq_batch)

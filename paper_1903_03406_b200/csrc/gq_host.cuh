@@ -128,6 +128,13 @@ static double now_s() { return std::chrono::duration<double>(std::chrono::steady
 static thread_local double g_prof[8];
 // fine stage timers (GQ_PROFILE=2): synchronise and charge the elapsed time
 static thread_local bool g_trace = false;
+// Experiment / debug switches, read once when the library loads (never on the
+// per-round path)
+static const bool o_thread_regions = getenv("GQ_THREAD_REGIONS") != nullptr;
+static const bool o_filter_launches = getenv("GQ_FILTER_LAUNCHES") != nullptr;
+static const bool o_thread_init = getenv("GQ_THREAD_INIT") != nullptr;
+static const bool o_init_launches = getenv("GQ_INIT_LAUNCHES") != nullptr;
+static const int o_trace_from = getenv("GQ_TRACE_FROM") ? atoi(getenv("GQ_TRACE_FROM")) : -1;
 static const bool g_grid_thread = getenv("GQ_GRID_THREAD") != nullptr;   // experiments: thread-per-query grid kernels
 static thread_local bool g_fine = false;      // GQ_PROFILE=2: host clock after a sync per stage
 static thread_local bool g_fine_ev = false;   // GQ_PROFILE=3: events per stage (device timeline, no syncs)
@@ -594,7 +601,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   if (n1 <= n0) return;
   fine(c, 31);
   region_begin(c);
-  if (!getenv("GQ_THREAD_REGIONS")) {   // debug switch: per-thread kernel
+  if (!o_thread_regions) {   // debug switch: per-thread kernel
     launch_warp_regions(c, k_region_warp<WT1_MAXT, WT1_HASH, WT1_MINB>, WR_WARPS * sizeof(WarpShared1), n1 - n0, n0, n1,
                         (const int*)nullptr);
   } else {
@@ -621,7 +628,7 @@ static void run_regions(gq_ctx* c, int n0, int n1, int probe) {
   std::vector<int> ovf;
   for (int k = 0; k < n1 - n0; ++k) if (hs[k] == CS_OVF) ovf.push_back(n0 + k);
   std::vector<int> big;
-  if (!ovf.empty() && WT1_MAXT != WT2_MAXT && !getenv("GQ_THREAD_REGIONS")) {
+  if (!ovf.empty() && WT1_MAXT != WT2_MAXT && !o_thread_regions) {
     int no = (int)ovf.size();
     CK(cudaMemcpyAsync(c->tmpB, ovf.data(), sizeof(int) * no, cudaMemcpyHostToDevice, c->st));
     region_begin(c);
@@ -730,7 +737,7 @@ static void rank_candidates(gq_ctx* c, int n) {
 // LFMIS filter over candidates [0,n): state 0 for ok ones, 3 for the rest.
 static void run_filter(gq_ctx* c, int n, int* nacc_out) {
   if (n <= 0) return;
-  if (!getenv("GQ_FILTER_LAUNCHES")) {
+  if (!o_filter_launches) {
     static int blocks_per_sm = 0, nsm = 0;
     if (!blocks_per_sm) {
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_filter_coop<false>, 256, 0));
@@ -922,7 +929,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     int W = (int)std::min<double>(left, std::max(64.0, wf * inserted));
     fine(c, 22);
     region_begin(c);
-    if (!getenv("GQ_THREAD_INIT")) {
+    if (!o_thread_init) {
       int blocks = std::min((W + WR_WARPS - 1) / WR_WARPS, c->S.nthreads / WR_WARPS);
       static int* h_wdbg = nullptr;
       if (getenv("GQ_WATCHDOG") && !h_wdbg) {
@@ -961,7 +968,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     // cooperative filter below cuts the window at the first new one on the device, and
     // the block kernel picks it up next round -- no read-back here in the common case.
     std::vector<int> bl;
-    if (novf_last > 0 || g_trace || getenv("GQ_INIT_LAUNCHES")) {
+    if (novf_last > 0 || g_trace || o_init_launches) {
       CK(cudaMemsetAsync(c->d_int + 40, 0, 8, c->st));
       LAUNCH(k_count_ovf, W, C, d_plist, W, c->d_int + 40);
       int novf = read_int(c, c->d_int + 40);
@@ -972,7 +979,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
         stage(c, sw.data(), d_scan, 4 * (size_t)W);
         sync(c);
         for (int w = 0; w < W; ++w) if (sw[w] == CS_OVF) bl.push_back(pl[w]);
-        if (WT1_MAXT != WT2_MAXT && !getenv("GQ_THREAD_INIT")) {   // the large warp tier first
+        if (WT1_MAXT != WT2_MAXT && !o_thread_init) {   // the large warp tier first
           int no = (int)bl.size();
           CK(cudaMemcpyAsync(d_keep, bl.data(), 4 * (size_t)no, cudaMemcpyHostToDevice, c->st));
           int blocks = std::min((no + WR_WARPS - 1) / WR_WARPS, c->S.nthreads / WR_WARPS);
@@ -1013,7 +1020,7 @@ static void init_delaunay(gq_ctx* c, const int* order, int n) {
     }
     fine(c, 1);
     int nacc = 0, add_t = 0;
-    if (!getenv("GQ_INIT_LAUNCHES")) {
+    if (!o_init_launches) {
       static int bps = 0, nsm = 0;
       if (!bps) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_init_filter_coop<false>, 256, 0));
@@ -1338,7 +1345,7 @@ static void fine(gq_ctx* c, int k) {
 static RoundOut run_round(gq_ctx* c, int round_no) {
   RoundOut R;
   c->big_used = 0;
-  if (getenv("GQ_TRACE_FROM")) g_trace = round_no >= atoi(getenv("GQ_TRACE_FROM"));   // stage trace from a round on
+  if (o_trace_from >= 0) g_trace = round_no >= o_trace_from;   // stage trace from a round on
   g_wd_round.store(round_no);
   pull(c);
   maintain_capacity(c);
