@@ -127,81 +127,170 @@ __device__ __noinline__ void insert_one(const Dev& D, const Cand& C, int c, Scra
   }
 }
 
-__global__ void k_fallback(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Scr SCB, FallbackIO F, T2Items T, SkipLog L) {
-  if (blockIdx.x || threadIdx.x) return;
-  Scratch S = scratch_for(SCB, 0);
+// ---------------------------------------------------------------------------
+// Sequential fallback (refine.py:748-806 _fallback, called in failed-list order
+// at refine.py:897-902).  Each failed candidate is re-evaluated on the mesh left
+// by the accepted insertions and by every earlier fallback.  Almost all of them
+// fail again (C4 face rounds: ~1% insert), and a failing evaluation writes only
+// flags, so the list runs in waves: k_fb_scan evaluates every remaining
+// candidate in parallel on the current mesh, without side effects; k_fb_apply
+// then applies, in list order, the outcomes of the candidates before the first
+// one that inserts (or that exceeds the scan's arenas) -- they saw exactly the
+// mesh the sequential loop would show them -- and runs that first candidate
+// through the full sequential body.  The next wave starts after it.  Results,
+// vertex ids and tet ids equal the one-candidate-at-a-time loop.
+#define FB_NONE 0      // target gone
+#define FB_TOOCLOSE 1  // skip, reason too_close
+#define FB_HULL 2      // tet: a hull subface obstructs it (arg = face record, -1 none)
+#define FB_SHORT 3     // tet: short boundary edge
+#define FB_MEMB 4      // membrane (arg = 4t+i)
+#define FB_CNSS 5      // skip, reason cavity_not_star_shaped
+#define FB_BREAK 6     // inserts (or needs the sequential arenas): run the full body
+
+// evaluation of failed candidate k; commit=false: no writes except the
+// candidate's own arrays (returns the outcome), commit=true: the sequential body
+__device__ __noinline__ int fallback_eval(const Dev& D, const Cand& C, Scratch& S, const FallbackIO& F, T2Items& T,
+                                          const SkipLog& L, int k, bool commit, int* arg) {
   CandCtx X; X.round_no = F.round_no; X.seed = F.seed; X.with_facets = F.with_facets;
-  for (int k = 0; k < F.n; ++k) {
-    int c = F.list[k];
-    int kind = C.kind[c], tgt = C.tgt[c];
-    if (C.status[c] == CS_TOOCLOSE) { skip_cand(D, C, c, 2, F.round_no, L, skip_order(2, k)); continue; }
-    if (kind == K_TET && !(tgt >= 0 && tgt < D.ctr->nt && D.alive[tgt])) continue;
-    if (kind == K_SEG && !(D.sg_fl[tgt] & RF_LIVE)) continue;
-    if (kind == K_FACE && !(D.sf_fl[tgt] & RF_LIVE)) continue;
-    if (!make_cand(D, C, c, X, S)) { raise_err(GQ_ERR_DEGEN); continue; }
-    const double* p = C.p + 3 * (size_t)c;
-    if (kind == K_TET) {
-      int cur = tgt, prev = -1, hull = -2;
-      int max_steps = walk_cap(D, 64);
-      bool done = false;
-      for (int step = 0; step < max_steps && !done; ++step) {
-        int4 q = D.tv[cur];
-        if (q.w == GHOST) { int a = q.x, b = q.y, cc = q.z; sort3(a, b, cc); hull = face_lookup(D, a, b, cc); if (hull < 0) hull = -1; done = true; break; }
-        bool moved = false;
-        for (int kk = 0; kk < 4; ++kk) {
-          int i = (kk + step) & 3;
-          int u = tnk(D, cur, i) >> 2;
-          if (u == prev) continue;
-          int f[3]; face_verts(q, i, f);
-          if (orient3d(PT(D, f[0]), PT(D, f[1]), PT(D, f[2]), p) > 0) {
-            if (D.tv[u].w == GHOST) { sort3(f[0], f[1], f[2]); hull = face_lookup(D, f[0], f[1], f[2]); if (hull < 0) hull = -1; done = true; break; }
-            prev = cur; cur = u; moved = true; break;
-          }
+  int c = F.list[k];
+  int kind = C.kind[c], tgt = C.tgt[c];
+  if (C.status[c] == CS_TOOCLOSE) { if (commit) skip_cand(D, C, c, 2, F.round_no, L, skip_order(2, k)); return FB_TOOCLOSE; }
+  if (kind == K_TET && !(tgt >= 0 && tgt < D.ctr->nt && D.alive[tgt])) return FB_NONE;
+  if (kind == K_SEG && !(D.sg_fl[tgt] & RF_LIVE)) return FB_NONE;
+  if (kind == K_FACE && !(D.sf_fl[tgt] & RF_LIVE)) return FB_NONE;
+  if (!make_cand(D, C, c, X, S)) { if (commit) raise_err(GQ_ERR_DEGEN); return commit ? FB_NONE : FB_BREAK; }
+  const double* p = C.p + 3 * (size_t)c;
+  if (kind == K_TET) {
+    int cur = tgt, prev = -1, hull = -2;
+    int max_steps = walk_cap(D, 64);
+    bool done = false;
+    for (int step = 0; step < max_steps && !done; ++step) {
+      int4 q = D.tv[cur];
+      if (q.w == GHOST) { int a = q.x, b = q.y, cc = q.z; sort3(a, b, cc); hull = face_lookup(D, a, b, cc); if (hull < 0) hull = -1; done = true; break; }
+      bool moved = false;
+      for (int kk = 0; kk < 4; ++kk) {
+        int i = (kk + step) & 3;
+        int u = tnk(D, cur, i) >> 2;
+        if (u == prev) continue;
+        int f[3]; face_verts(q, i, f);
+        if (orient3d(PT(D, f[0]), PT(D, f[1]), PT(D, f[2]), p) > 0) {
+          if (D.tv[u].w == GHOST) { sort3(f[0], f[1], f[2]); hull = face_lookup(D, f[0], f[1], f[2]); if (hull < 0) hull = -1; done = true; break; }
+          prev = cur; cur = u; moved = true; break;
         }
-        if (done) break;
-        if (!moved) { done = true; break; }
       }
-      if (!done) {
-        int end = walk(D, p, tgt);
-        if (end >= 0 && D.tv[end].w == GHOST) { int4 q = D.tv[end]; int a = q.x, b = q.y, cc = q.z; sort3(a, b, cc); hull = face_lookup(D, a, b, cc); if (hull < 0) hull = -1; }
-      }
-      if (hull >= 0) {   // redirect the subface to the next round
-        if (!(D.sf_fl[hull] & RF_SKIP)) D.sf_fl[hull] |= RF_ENC;
-        continue;
-      }
+      if (done) break;
+      if (!moved) { done = true; break; }
     }
-    C.bigi[c] = 0;
-    SlabView sv = slab(C, c);
-    RegionOut O = region_view(C, c, sv, 0);
-    int seeds[32];
-    int ns = cand_seeds(D, C, c, seeds, S);
-    atomicAdd(&D.ctr->region_calls, 1ull);
-    int st = ns == 0 ? RS_CNSS : region_compute(D, p, seeds, ns, allow_of(C, c), S, O);
-    store_region(C, c, O);
-    if (st == RS_OK) {
-      if (O.mind <= D.too_close_sq) { skip_cand(D, C, c, 2, F.round_no, L, skip_order(2, k)); continue; }
-      if (kind == K_TET && O.mind < F.lmin2) {
+    if (!done) {
+      int end = walk(D, p, tgt);
+      if (end >= 0 && D.tv[end].w == GHOST) { int4 q = D.tv[end]; int a = q.x, b = q.y, cc = q.z; sort3(a, b, cc); hull = face_lookup(D, a, b, cc); if (hull < 0) hull = -1; }
+    }
+    if (hull >= 0) {   // redirect the subface to the next round
+      if (commit) { if (!(D.sf_fl[hull] & RF_SKIP)) D.sf_fl[hull] |= RF_ENC; }
+      *arg = hull;
+      return FB_HULL;
+    }
+  }
+  C.bigi[c] = commit ? 0 : -1;     // sequential: big slab 0; scan: the candidate's own slab
+  SlabView sv = slab(C, c);
+  RegionOut O = region_view(C, c, sv, 0);
+  int seeds[32];
+  int ns = cand_seeds(D, C, c, seeds, S);
+  atomicAdd(&D.ctr->region_calls, 1ull);
+  int st = ns == 0 ? RS_CNSS : region_compute(D, p, seeds, ns, allow_of(C, c), S, O);
+  store_region(C, c, O);
+  if (st == RS_OK) {
+    if (O.mind <= D.too_close_sq) { if (commit) skip_cand(D, C, c, 2, F.round_no, L, skip_order(2, k)); return FB_TOOCLOSE; }
+    if (kind == K_TET && O.mind < F.lmin2) {
+      if (commit) {
         D.skip[tgt] = 1;
         int cv[4]; tet_canon(D, tgt, cv);
         log_skip(D, L, F.round_no, K_TET, 1, cv, 4, skip_order(2, k));
-        continue;
       }
-      if (D.ctr->nv >= D.vcap) { raise_err(GQ_ERR_CAP); return; }
-      insert_one(D, C, c, S, T, 0);
-      atomicAdd(F.inserted, 1);
-    } else if (st == RS_MEMBRANE) {
+      return FB_SHORT;
+    }
+    if (!commit) return FB_BREAK;
+    if (D.ctr->nv >= D.vcap) { raise_err(GQ_ERR_CAP); return FB_BREAK; }
+    insert_one(D, C, c, S, T, 0);
+    atomicAdd(F.inserted, 1);
+    return FB_BREAK;
+  } else if (st == RS_MEMBRANE) {
+    if (commit) {
       int t = O.memb >> 2, i = O.memb & 3;
       int f[3]; face_verts(D.tv[t], i, f);
       mark_enc_face_key(D, f[0], f[1], f[2]);
       if (kind == K_SEG) D.sg_fl[tgt] |= RF_BLOCK;
       else if (kind == K_FACE) D.sf_fl[tgt] |= RF_BLOCK;
-    } else {
-      if (st == RS_OVERFLOW) atomicAdd(&D.ctr->fail[5], 1u);
-      // not star-shaped, or a cavity beyond the sequential path's arena
-      // (8192 tets): skipped like the reference's CavityNotStarShaped
-      skip_cand(D, C, c, 3, F.round_no, L, skip_order(2, k));
+    }
+    *arg = O.memb;
+    return FB_MEMB;
+  }
+  if (st == RS_OVERFLOW && !commit) return FB_BREAK;   // the sequential arenas may hold it
+  if (commit) {
+    if (st == RS_OVERFLOW) atomicAdd(&D.ctr->fail[5], 1u);
+    // not star-shaped, or a cavity beyond the sequential path's arena
+    // (8192 tets): skipped like the reference's CavityNotStarShaped
+    skip_cand(D, C, c, 3, F.round_no, L, skip_order(2, k));
+  }
+  return FB_CNSS;
+}
+
+// the sequential loop (one thread), kept for GQ_FALLBACK_SERIAL comparisons
+__global__ void k_fallback(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Scr SCB, FallbackIO F, T2Items T, SkipLog L) {
+  if (blockIdx.x || threadIdx.x) return;
+  Scratch S = scratch_for(SCB, 0);
+  int arg = 0;
+  for (int k = 0; k < F.n; ++k) fallback_eval(D, C, S, F, T, L, k, true, &arg);
+}
+
+// wave step 1: outcomes of candidates [start, n) on the current mesh, and the
+// first one that breaks the wave (atomicMin into *first, preset to n)
+__global__ void k_fb_scan(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const __grid_constant__ Scr SC,
+                          FallbackIO F, T2Items T, SkipLog L, const int* startp, int* out, int* first) {
+  int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  Scratch S = scratch_for(SC, tid);
+  const int start = *startp;
+  for (int k = start + tid; k < F.n; k += gridDim.x * blockDim.x) {
+    int arg = -1;
+    int o = fallback_eval(D, C, S, F, T, L, k, false, &arg);
+    out[2 * k] = o; out[2 * k + 1] = arg;
+    if (o == FB_BREAK) atomicMin(first, k);
+  }
+}
+
+// wave step 2 (one thread): apply the outcomes of [start, first) in list order,
+// then the full sequential body for candidate first; *startp = first + 1
+__global__ void k_fb_apply(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Scr SCB, FallbackIO F, T2Items T,
+                           SkipLog L, int* startp, const int* out, int* first) {
+  if (blockIdx.x || threadIdx.x) return;
+  const int start = *startp, f = *first;
+  for (int k = start; k < f; ++k) {
+    int c = F.list[k];
+    int kind = C.kind[c], tgt = C.tgt[c];
+    int o = out[2 * k], arg = out[2 * k + 1];
+    if (o == FB_TOOCLOSE || o == FB_CNSS) {
+      skip_cand(D, C, c, o == FB_TOOCLOSE ? 2 : 3, F.round_no, L, skip_order(2, k));
+    } else if (o == FB_HULL) {
+      if (!(D.sf_fl[arg] & RF_SKIP)) D.sf_fl[arg] |= RF_ENC;
+    } else if (o == FB_SHORT) {
+      D.skip[tgt] = 1;
+      int cv[4]; tet_canon(D, tgt, cv);
+      log_skip(D, L, F.round_no, K_TET, 1, cv, 4, skip_order(2, k));
+    } else if (o == FB_MEMB) {
+      int t = arg >> 2, i = arg & 3;
+      int fv[3]; face_verts(D.tv[t], i, fv);
+      mark_enc_face_key(D, fv[0], fv[1], fv[2]);
+      if (kind == K_SEG) D.sg_fl[tgt] |= RF_BLOCK;
+      else if (kind == K_FACE) D.sf_fl[tgt] |= RF_BLOCK;
     }
   }
+  if (f < F.n) {
+    Scratch S = scratch_for(SCB, 0);
+    int arg = 0;
+    fallback_eval(D, C, S, F, T, L, f, true, &arg);
+  }
+  *startp = f + 1;
+  *first = F.n;
 }
 
 // accepted tets whose region has a too-short boundary edge (refine.py:891-894)

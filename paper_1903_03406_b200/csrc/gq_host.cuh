@@ -134,6 +134,7 @@ static const bool o_thread_regions = getenv("GQ_THREAD_REGIONS") != nullptr;
 static const bool o_filter_launches = getenv("GQ_FILTER_LAUNCHES") != nullptr;
 static const bool o_thread_init = getenv("GQ_THREAD_INIT") != nullptr;
 static const bool o_init_launches = getenv("GQ_INIT_LAUNCHES") != nullptr;
+static const bool o_fallback_serial = getenv("GQ_FALLBACK_SERIAL") != nullptr;   // one-thread fallback loop (comparisons)
 static const int o_trace_from = getenv("GQ_TRACE_FROM") ? atoi(getenv("GQ_TRACE_FROM")) : -1;
 static const bool g_grid_thread = getenv("GQ_GRID_THREAD") != nullptr;   // experiments: thread-per-query grid kernels
 static thread_local bool g_fine = false;      // GQ_PROFILE=2: host clock after a sync per stage
@@ -1163,7 +1164,18 @@ __global__ void k_pool_pos(const __grid_constant__ Cand C, int n, const int* kee
     C.pool[c] = keep[c] ? keepscan[c] : -1;
 }
 
-struct RoundOut { int phase = -1; long long ncand = 0, acc = 0, rej = 0, failed = 0, inserted = 0; };
+struct RoundOut {
+  int phase = -1; long long ncand = 0, acc = 0, rej = 0, failed = 0, inserted = 0;
+  double vt[6] = {0, 0, 0, 0, 0, 0};   // verbose only: pool+regions, filter, insert, fallback, post (synchronised)
+  int st_hist[6] = {0, 0, 0, 0, 0, 0}; // verbose only: candidate status histogram (CS_*)
+};
+// verbose diagnostics: stage boundary with a stream sync (never on the timed path)
+static double vmark(gq_ctx* c, double& last) {
+  CK(cudaStreamSynchronize(c->st));
+  double t = now_s(), d = t - last;
+  last = t;
+  return d;
+}
 
 
 static const char* g_prof_names[8] = {"pool", "regions", "filter", "insert", "2d", "fallback", "post", "other"};
@@ -1344,6 +1356,7 @@ static void fine(gq_ctx* c, int k) {
 
 static RoundOut run_round(gq_ctx* c, int round_no) {
   RoundOut R;
+  double vlast = c->verbose ? now_s() : 0;
   c->big_used = 0;
   if (o_trace_from >= 0) g_trace = round_no >= o_trace_from;   // stage trace from a round on
   g_wd_round.store(round_no);
@@ -1420,6 +1433,13 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   }
   int n = nbase;
   fine(c, 23);
+  if (c->verbose) {
+    R.vt[0] = vmark(c, vlast);
+    std::vector<int> st(n);
+    if (n) d2h(c, st.data(), c->C.status, 4 * (size_t)n);
+    for (int v : st) if (v >= 0 && v < 6) R.st_hist[v]++;
+    vlast = now_s();
+  }
   double t1 = now_s();
   ensure_tmp(c, n + 1);
   LAUNCH(k_states, n, c->D, c->C, n, c->Q.a, c->Q.b);
@@ -1433,7 +1453,9 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   g_prof[2] += now_s() - t1;
   R.failed = nfail;
   R.phase = phase;
+  if (c->verbose) R.vt[1] = vmark(c, vlast);
   insert_accepted(c, n, &R.acc, &R.inserted, round_no);
+  if (c->verbose) R.vt[2] = vmark(c, vlast);
   R.rej = nok - R.acc;
   t1 = now_s();
   fine(c, -1);
@@ -1444,12 +1466,31 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     FallbackIO F; F.list = c->Q.h; F.n = nfail; F.round_no = round_no; F.seed = c->seed;
     F.with_facets = c->npoly > 0; F.lmin2 = lmin2; F.inserted = c->d_int + 20;
     CK(cudaMemsetAsync(c->d_int + 20, 0, 4, c->st));
-    k_fallback<<<1, 1, 0, c->st>>>(c->D, c->C, c->SB, F, c->T, c->L);
-    c->launches++;
-    CK(cudaGetLastError());
+    if (o_fallback_serial) {
+      k_fallback<<<1, 1, 0, c->st>>>(c->D, c->C, c->SB, F, c->T, c->L);
+      c->launches++;
+      CK(cudaGetLastError());
+    } else {
+      // waves (gq_fallback.cuh): parallel evaluation, in-order application
+      int* out = dmalloc<int>(2 * (size_t)nfail);
+      int h0[2] = {0, nfail};
+      CK(cudaMemcpyAsync(c->d_int + 24, h0, 8, cudaMemcpyHostToDevice, c->st));
+      int start = 0, waves = 0;
+      while (start < nfail) {
+        LAUNCH_S(k_fb_scan, nfail - start, c->D, c->C, c->S, F, c->T, c->L, c->d_int + 24, out, c->d_int + 25);
+        k_fb_apply<<<1, 1, 0, c->st>>>(c->D, c->C, c->SB, F, c->T, c->L, c->d_int + 24, out, c->d_int + 25);
+        c->launches++;
+        CK(cudaGetLastError());
+        start = read_int(c, c->d_int + 24);
+        ++waves;
+      }
+      dfree(out);
+      if (g_trace) std::fprintf(stderr, "[fallback] round %d: %d candidates in %d waves\n", round_no, nfail, waves);
+    }
     R.inserted += read_int(c, c->d_int + 20);
   }
   fine(c, 30);
+  if (c->verbose) R.vt[3] = vmark(c, vlast);
   if (g_trace && phase == 2) {   // how many blasted tet candidates had their own tet taken by an accepted cavity
     CK(cudaMemsetAsync(c->d_int + 56, 0, 8, c->st));
     LAUNCH(k_count_seed_dead, n, c->D, c->C, n, c->d_int + 56);
@@ -1487,6 +1528,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
   }
   fine(c, 10);
   g_prof[6] += now_s() - t1;
+  if (c->verbose) R.vt[4] = vmark(c, vlast);
   return R;
 }
 
@@ -1669,6 +1711,10 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
                    c->hc.skipr[2], c->hc.skipr[3], c->hc.skipr[4], c->hc.skipr[5], c->hc.skipr[6], c->hc.skipr[7],
                    c->hc.skipr[8], c->hc.skipr[9], c->hc.skipr[10], c->hc.skipr[11], c->hc.fail[0], c->hc.fail[1],
                    c->hc.fail[2], c->hc.fail[3], c->hc.fail[4], c->hc.fail[5], c->hc.fail[6]);
+      std::fprintf(stderr, "  stages ms: pool+regions %.1f filter %.1f insert %.1f fallback %.1f post %.1f"
+                   " | status ok %d cnss %d tooclose %d memb %d ovf %d drop %d\n",
+                   1e3 * R.vt[0], 1e3 * R.vt[1], 1e3 * R.vt[2], 1e3 * R.vt[3], 1e3 * R.vt[4], R.st_hist[0],
+                   R.st_hist[1], R.st_hist[2], R.st_hist[3], R.st_hist[4], R.st_hist[5]);
     }
     round_no += 1;
   }
