@@ -281,7 +281,7 @@ __device__ inline int region_block(const Dev& D, const double* p, const int* see
   }
   __syncthreads();
   if (__syncthreads_or(bf_has_ghost_part(D, O.bf, nbf, tid, BR_THREADS)) &&
-      __syncthreads_or(bf_open_part(D, O.bf, nbf, tid, BR_THREADS)))
+      bf_open_block(D, O.bf, nbf, S.fset, BR_THREADS))
     return RS_BADSTAR;
   // swallow check + min distance over boundary vertices: reuse the hash as a
   // vertex set (cavity membership is no longer needed)

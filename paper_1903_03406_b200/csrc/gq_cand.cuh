@@ -14,6 +14,7 @@
 #define CS_MEMB 3
 #define CS_OVF 4
 #define CS_DROP 5      // redirected / skipped before the pool
+#define MEMB_HUGE_OVF (-3)   // C.memb of a failed candidate whose cavity overflowed every region tier
 
 // slab capacities (normal pass); overflowing candidates rerun with big slabs
 #define CT 256

@@ -591,6 +591,80 @@ __device__ inline bool bf_open_part(const Dev& D, const int* bf, int nbf, int r,
   return false;
 }
 
+// Linear-time forms of bf_open_part (same answer): every boundary-face edge is
+// counted in a hash instead of against every other face.
+//  - one thread: two tagged keys per edge in the thread's 64-bit set (the set
+//    keeps its other keys; a full set falls back to the quadratic count);
+//  - a block: the count packed into the key of a raw table on the block's
+//    64-bit arena (cleared first; the set's epoch is bumped afterwards so its
+//    own users see it empty).  Call with every thread of the block.
+__device__ __forceinline__ unsigned long long bf_edge_key(int a, int b) {
+  int x = a + 1, y = b + 1;   // ghost (-1) -> 0
+  if (x > y) { int t = x; x = y; y = t; }
+  return ((unsigned long long)(unsigned)x << 30) | (unsigned long long)(unsigned)y;
+}
+__device__ inline bool bf_open_seq(const Dev& D, const int* bf, int nbf, LSet& F) {
+  const unsigned long long T1 = 8ull << 60, T2 = 9ull << 60;
+  for (int k = 0; k < nbf; ++k) {
+    int f[3]; face_verts(D.tv[bf[k] >> 2], bf[k] & 3, f);
+    for (int e = 0; e < 3; ++e) {
+      unsigned long long E = bf_edge_key(f[e], f[(e + 1) % 3]);
+      int a = F.add(T1 | E);
+      if (a < 0) return bf_open_part(D, bf, nbf, 0, 1);
+      if (a == 1) continue;
+      a = F.add(T2 | E);
+      if (a < 0) return bf_open_part(D, bf, nbf, 0, 1);
+      if (a == 0) return true;            // a third face on this edge
+    }
+  }
+  for (int k = 0; k < nbf; ++k) {
+    int f[3]; face_verts(D.tv[bf[k] >> 2], bf[k] & 3, f);
+    for (int e = 0; e < 3; ++e)
+      if (!F.has(T2 | bf_edge_key(f[e], f[(e + 1) % 3]))) return true;   // a single face on this edge
+  }
+  return false;
+}
+__device__ inline bool bf_open_block(const Dev& D, const int* bf, int nbf, LSet& F, int nthreads) {
+  const int tid = threadIdx.x;
+  if ((long long)F.cap < 4LL * nbf) return __syncthreads_or(bf_open_part(D, bf, nbf, tid, nthreads));
+  volatile unsigned long long* K = F.key;
+  for (int i = tid; i < F.cap; i += nthreads) K[i] = 0ull;
+  __syncthreads();
+  for (int k = tid; k < nbf; k += nthreads) {
+    int f[3]; face_verts(D.tv[bf[k] >> 2], bf[k] & 3, f);
+    for (int e = 0; e < 3; ++e) {
+      unsigned long long E = bf_edge_key(f[e], f[(e + 1) % 3]) << 2;   // low 2 bits: count (saturating at 3)
+      unsigned int i = (unsigned int)mix64(E) & (unsigned int)(F.cap - 1);
+      while (true) {
+        unsigned long long cur = K[i];
+        if (cur == 0ull) {
+          cur = atomicCAS(&F.key[i], 0ull, E | 1ull);
+          if (cur == 0ull) break;
+        }
+        if ((cur >> 2) == (E >> 2)) {
+          while ((cur & 3ull) != 3ull) {
+            unsigned long long old = atomicCAS(&F.key[i], cur, cur + 1ull);
+            if (old == cur) break;
+            cur = old;
+          }
+          break;
+        }
+        i = (i + 1) & (unsigned int)(F.cap - 1);
+      }
+    }
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int i = tid; i < F.cap && !bad; i += nthreads) {
+    unsigned long long v = K[i];
+    bad = v != 0ull && (v & 3ull) != 2ull;
+  }
+  bad = __syncthreads_or(bad);
+  if (tid == 0) F.clear();
+  __syncthreads();
+  return bad;
+}
+
 struct Scratch {     // per-thread scratch views
   ISet tset;         // tet -> list index
   LSet fset;         // tagged keys: vertices, edges, faces
@@ -847,7 +921,7 @@ __device__ __noinline__ int region_compute(const Dev& D, const double* p, const 
     }
   }
   // (sequential path: every cavity is checked, see k_star_check for why the peel is not enough)
-  if (bf_open_part(D, O.bf, O.nbf, 0, 1)) return RS_BADSTAR;
+  if (bf_open_seq(D, O.bf, O.nbf, S.fset)) return RS_BADSTAR;
   double mind = __longlong_as_double(0x7ff0000000000000ll);
   for (int a = 0; a < O.nbf; ++a) {
     int t = O.bf[a] >> 2, i = O.bf[a] & 3;

@@ -146,6 +146,8 @@ __device__ __noinline__ void insert_one(const Dev& D, const Cand& C, int c, Scra
 #define FB_MEMB 4      // membrane (arg = 4t+i)
 #define FB_CNSS 5      // skip, reason cavity_not_star_shaped
 #define FB_BREAK 6     // inserts (or needs the sequential arenas): run the full body
+#define FB_OVF 7       // the concurrent cavity overflowed every tier (> 64k tets): beyond the
+                       // sequential arena (8192 tets) too, skipped without re-growing it
 
 // evaluation of failed candidate k; commit=false: no writes except the
 // candidate's own arrays (returns the outcome), commit=true: the sequential body
@@ -158,6 +160,10 @@ __device__ __noinline__ int fallback_eval(const Dev& D, const Cand& C, Scratch& 
   if (kind == K_TET && !(tgt >= 0 && tgt < D.ctr->nt && D.alive[tgt])) return FB_NONE;
   if (kind == K_SEG && !(D.sg_fl[tgt] & RF_LIVE)) return FB_NONE;
   if (kind == K_FACE && !(D.sf_fl[tgt] & RF_LIVE)) return FB_NONE;
+  if (C.status[c] == CS_CNSS && C.memb[c] == MEMB_HUGE_OVF) {
+    if (commit) { atomicAdd(&D.ctr->fail[5], 1u); skip_cand(D, C, c, 3, F.round_no, L, skip_order(2, k)); }
+    return FB_OVF;
+  }
   if (!make_cand(D, C, c, X, S)) { if (commit) raise_err(GQ_ERR_DEGEN); return commit ? FB_NONE : FB_BREAK; }
   const double* p = C.p + 3 * (size_t)c;
   if (kind == K_TET) {
@@ -268,7 +274,8 @@ __global__ void k_fb_apply(const __grid_constant__ Dev D, const __grid_constant_
     int c = F.list[k];
     int kind = C.kind[c], tgt = C.tgt[c];
     int o = out[2 * k], arg = out[2 * k + 1];
-    if (o == FB_TOOCLOSE || o == FB_CNSS) {
+    if (o == FB_OVF) atomicAdd(&D.ctr->fail[5], 1u);
+    if (o == FB_TOOCLOSE || o == FB_CNSS || o == FB_OVF) {
       skip_cand(D, C, c, o == FB_TOOCLOSE ? 2 : 3, F.round_no, L, skip_order(2, k));
     } else if (o == FB_HULL) {
       if (!(D.sf_fl[arg] & RF_SKIP)) D.sf_fl[arg] |= RF_ENC;

@@ -555,6 +555,10 @@ __global__ void k_set_status(const __grid_constant__ Cand C, const int* list, in
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
     if (C.status[list[k]] == from) C.status[list[k]] = to;
 }
+__global__ void k_mark_memb(const __grid_constant__ Cand C, const int* list, int n, int status, int memb) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    if (C.status[list[k]] == status) C.memb[list[k]] = memb;
+}
 // block-tier overflows of this round: the huge tier, capacities doubled until
 // every cavity fits (64k tets at most: beyond, the candidate fails).  Cavities
 // that large come from the far circumcentres of nearly flat tets lying on a
@@ -585,6 +589,7 @@ static void run_huge_regions(gq_ctx* c, const std::vector<int>& big) {
     if (g_trace || c->verbose) std::fprintf(stderr, "[huge] %d cavities, capacity %d tets, %d overflow\n", nh, mcap, still);
     if (still == 0) return;
     if (mcap >= (1 << 16)) {   // beyond 64k tets: failed candidates (the sequential fallback skips them)
+      LAUNCH(k_mark_memb, nh, c->C, c->hlist, nh, CS_OVF, MEMB_HUGE_OVF);   // the fallback skips them outright
       LAUNCH(k_set_status, nh, c->C, c->hlist, nh, CS_OVF, CS_CNSS);
       return;
     }
@@ -1168,6 +1173,7 @@ struct RoundOut {
   int phase = -1; long long ncand = 0, acc = 0, rej = 0, failed = 0, inserted = 0;
   double vt[6] = {0, 0, 0, 0, 0, 0};   // verbose only: pool+regions, filter, insert, fallback, post (synchronised)
   int st_hist[6] = {0, 0, 0, 0, 0, 0}; // verbose only: candidate status histogram (CS_*)
+  int waves = 0;                       // fallback waves
 };
 // verbose diagnostics: stage boundary with a stream sync (never on the timed path)
 static double vmark(gq_ctx* c, double& last) {
@@ -1485,6 +1491,7 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
         ++waves;
       }
       dfree(out);
+      R.waves = waves;
       if (g_trace) std::fprintf(stderr, "[fallback] round %d: %d candidates in %d waves\n", round_no, nfail, waves);
     }
     R.inserted += read_int(c, c->d_int + 20);
@@ -1712,9 +1719,9 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
                    c->hc.skipr[8], c->hc.skipr[9], c->hc.skipr[10], c->hc.skipr[11], c->hc.fail[0], c->hc.fail[1],
                    c->hc.fail[2], c->hc.fail[3], c->hc.fail[4], c->hc.fail[5], c->hc.fail[6]);
       std::fprintf(stderr, "  stages ms: pool+regions %.1f filter %.1f insert %.1f fallback %.1f post %.1f"
-                   " | status ok %d cnss %d tooclose %d memb %d ovf %d drop %d\n",
+                   " | status ok %d cnss %d tooclose %d memb %d ovf %d drop %d | fallback waves %d\n",
                    1e3 * R.vt[0], 1e3 * R.vt[1], 1e3 * R.vt[2], 1e3 * R.vt[3], 1e3 * R.vt[4], R.st_hist[0],
-                   R.st_hist[1], R.st_hist[2], R.st_hist[3], R.st_hist[4], R.st_hist[5]);
+                   R.st_hist[1], R.st_hist[2], R.st_hist[3], R.st_hist[4], R.st_hist[5], R.waves);
     }
     round_no += 1;
   }
