@@ -242,8 +242,10 @@ def north_star(ctx, rounds: int, eq_rounds: int):
                              "value": int(eq.steiner_points) / (eq.device_ms / 1000.0),
                              "reference_port": "34,960 Steiner in 190.8 s over the same 2 rounds on one core of the "
                                                "build container (183 Steiner/s; profiles/r02_summary.md)"},
-            "note": "one device-timed refine per bench run; the full refine does not reach a fixed point within "
-                    "the reference's default 500 rounds (DESIGN.md section 7)"}
+            "skipped": int(cnt.n_skipped),
+            "note": "one device-timed refine per bench run at the reference's default max_rounds (500): the "
+                    "refine returns there like the reference's; it has not reached a fixed point yet "
+                    "(faces still encroached, tet phase not started; DESIGN.md section 7)"}
 
 
 def main():
@@ -253,8 +255,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gqm3d", choices=["gqm3d", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
-    ap.add_argument("--north-star-rounds", type=int, default=60,
-                    help="C2/C5 runs: also refine C4 once with this round cap (0: skip)")
+    ap.add_argument("--north-star-rounds", type=int, default=500,
+                    help="C2/C5 runs: also refine C4 once with this round cap (0: skip); "
+                         "500 = the reference's default RefineConfig.max_rounds")
     ap.add_argument("--scale", type=float, default=1.0, help="workload scale (1.0 = the BASELINE config)")
     ap.add_argument("--max-rounds", type=int, default=500)
     ap.add_argument("--e2e-steps", type=int, default=3, help="end-to-end refines timed (<= --steps)")

@@ -53,9 +53,10 @@ struct Counters {
   unsigned int skipr[12];            // skipped elements by kind * 4 + reason (diagnostics)
   unsigned int fail[8];              // failed-region causes (diagnostics): 0 no seed, 1 seed peeled,
                                      // 2 swallows a vertex, 3 pinched ghost boundary, 4 star check,
-                                     // 5 sequential-path overflow, 6 membrane
+                                     // 5 sequential-path overflow, 6 membrane, 7 exhaustive walk scans
   int first_real;                    // no alive real tet has a lower index (hint_tet; 0 after compaction)
   unsigned long long t2st[4];        // 2D cavities (diagnostics): computed, walk steps, exhaustive scans, triangles scanned
+  unsigned long long fb_slow;        // slowest fallback evaluation (diagnostics): cycles << 8 | outcome << 4 | kind
 };
 
 // A tet is one 32-byte record {tv, tn} (vertices, then packed neighbour
@@ -493,6 +494,7 @@ __device__ __noinline__ int walk(const Dev& D, const double* p, int hint) {
     }
   }
   int nt = D.ctr->nt;
+  atomicAdd(&D.ctr->fail[7], 1u);
   for (int s = 0; s < nt; ++s) {
     if (!D.alive[s] || D.tv[s].w == GHOST) continue;
     int4 q = D.tv[s];

@@ -258,7 +258,10 @@ __global__ void k_fb_scan(const __grid_constant__ Dev D, const __grid_constant__
   const int start = *startp;
   for (int k = start + tid; k < F.n; k += gridDim.x * blockDim.x) {
     int arg = -1;
+    long long t0 = clock64();
     int o = fallback_eval(D, C, S, F, T, L, k, false, &arg);
+    unsigned long long dt = (unsigned long long)(clock64() - t0);
+    atomicMax(&D.ctr->fb_slow, (dt << 8) | (unsigned long long)(o << 4) | (unsigned long long)C.kind[F.list[k]]);
     out[2 * k] = o; out[2 * k + 1] = arg;
     if (o == FB_BREAK) atomicMin(first, k);
   }

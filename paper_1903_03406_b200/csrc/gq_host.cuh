@@ -1712,16 +1712,19 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
       const unsigned int* k = c->hc.chk;
       std::fprintf(stderr, "round %d phase=%d candidates=%lld accepted=%lld blasted=%lld failed=%lld inserted=%lld time=%.4f"
                    " | nv %d nt %d segs %d faces %d skipped %d | check: seg miss %u enc %u (collinear %u) face miss %u enc %u (coplanar %u)"
-                   " | skips seg %u/%u/%u/%u face %u/%u/%u/%u tet %u/%u/%u/%u | fails %u/%u/%u/%u/%u/%u/%u\n",
+                   " | skips seg %u/%u/%u/%u face %u/%u/%u/%u tet %u/%u/%u/%u | fails %u/%u/%u/%u/%u/%u/%u/%u\n",
                    round_no, R.phase, R.ncand, R.acc, R.rej, R.failed, R.inserted, dt, c->hc.nv, c->hc.nt, c->hc.nsegrec,
                    c->hc.nfacerec, c->hc.nskip, k[0], k[1], k[2], k[3], k[4], k[5], c->hc.skipr[0], c->hc.skipr[1],
                    c->hc.skipr[2], c->hc.skipr[3], c->hc.skipr[4], c->hc.skipr[5], c->hc.skipr[6], c->hc.skipr[7],
                    c->hc.skipr[8], c->hc.skipr[9], c->hc.skipr[10], c->hc.skipr[11], c->hc.fail[0], c->hc.fail[1],
-                   c->hc.fail[2], c->hc.fail[3], c->hc.fail[4], c->hc.fail[5], c->hc.fail[6]);
+                   c->hc.fail[2], c->hc.fail[3], c->hc.fail[4], c->hc.fail[5], c->hc.fail[6], c->hc.fail[7]);
       std::fprintf(stderr, "  stages ms: pool+regions %.1f filter %.1f insert %.1f fallback %.1f post %.1f"
-                   " | status ok %d cnss %d tooclose %d memb %d ovf %d drop %d | fallback waves %d\n",
+                   " | status ok %d cnss %d tooclose %d memb %d ovf %d drop %d | fallback waves %d, slowest eval %.2f ms (outcome %d kind %d)\n",
                    1e3 * R.vt[0], 1e3 * R.vt[1], 1e3 * R.vt[2], 1e3 * R.vt[3], 1e3 * R.vt[4], R.st_hist[0],
-                   R.st_hist[1], R.st_hist[2], R.st_hist[3], R.st_hist[4], R.st_hist[5], R.waves);
+                   R.st_hist[1], R.st_hist[2], R.st_hist[3], R.st_hist[4], R.st_hist[5], R.waves,
+                   (double)(c->hc.fb_slow >> 8) / 1.965e6, (int)((c->hc.fb_slow >> 4) & 15), (int)(c->hc.fb_slow & 15));
+      c->hc.fb_slow = 0;
+      CK(cudaMemsetAsync(&c->dctr->fb_slow, 0, 8, c->st));
     }
     round_no += 1;
   }

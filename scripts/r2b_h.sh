@@ -1,0 +1,3 @@
+mkdir -p gpurun_out/r2h
+timeout 600 python scripts/run_cfg.py C4 --max-rounds 250 --verbose > gpurun_out/r2h/c4.log 2>&1; echo "exit $?" >> gpurun_out/r2h/c4.log
+GQM3D_LIB=$PWD/paper_1903_03406_b200/libgqm3d_dbg.so timeout 600 python scripts/run_cfg.py C4 --max-rounds 165 --verbose > gpurun_out/r2h/c4dbg.log 2>&1; echo "exit $?" >> gpurun_out/r2h/c4dbg.log
