@@ -315,11 +315,9 @@ __device__ __noinline__ int cand_seeds(const Dev& D, const Cand& C, int c, int* 
   if (kind == K_SEG) {
     int2 e = D.sg_uv[tgt];
     int n = 0;
-    around_vertex(D, e.x, S.tset, S.stack, 2 * S.cap, [&](int t) {
-      if (has_v(D.tv[t], e.y)) {
-        if (n < 32) out[n++] = t;
-        else { int mx = 0; for (int k = 1; k < 32; ++k) if (out[k] > out[mx]) mx = k; if (t < out[mx]) out[mx] = t; }
-      }
+    around_edge(D, e.x, e.y, S.tset, S.stack, 2 * S.cap, [&](int t) {
+      if (n < 32) out[n++] = t;
+      else { int mx = 0; for (int k = 1; k < 32; ++k) if (out[k] > out[mx]) mx = k; if (t < out[mx]) out[mx] = t; }
       return false;
     }, [&] { n = 0; });
     for (int a = 1; a < n; ++a) { int x = out[a], b = a - 1; while (b >= 0 && out[b] > x) { out[b + 1] = out[b]; --b; } out[b + 1] = x; }

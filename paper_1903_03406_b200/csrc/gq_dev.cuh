@@ -57,6 +57,7 @@ struct Counters {
   int first_real;                    // no alive real tet has a lower index (hint_tet; 0 after compaction)
   unsigned long long t2st[4];        // 2D cavities (diagnostics): computed, walk steps, exhaustive scans, triangles scanned
   unsigned long long fb_slow;        // slowest fallback evaluation (diagnostics): cycles << 8 | outcome << 4 | kind
+  unsigned long long vq[4];          // vertex-star queries (diagnostics): stale-start scans, tets scanned, large-arena reruns, lock spins
 };
 
 // A tet is one 32-byte record {tv, tn} (vertices, then packed neighbour
@@ -291,6 +292,7 @@ __device__ __noinline__ int around_vertex_try(const Dev& D, int v, ISet& seen, i
   int start = D.vert_tet[v];
   if (start < 0 || start >= D.ctr->nt || !D.alive[start] || !has_v(D.tv[start], v)) {
     start = first_alive_with(D, v);
+    atomicAdd(&D.ctr->vq[0], 1ull); atomicAdd(&D.ctr->vq[1], (unsigned long long)(start < 0 ? D.ctr->nt : start + 1));
     if (start < 0) return 0;
     D.vert_tet[v] = start;   // same side effect as the reference
   }
@@ -325,6 +327,7 @@ __device__ inline int vpool_acquire(const Dev& D) {
       int s = (int)((s0 + k) % (unsigned int)D.vp_n);
       if (atomicCAS(D.vp_lock + s, 0, 1) == 0) { __threadfence(); return s; }
     }
+    atomicAdd(&D.ctr->vq[3], 1ull);
     __nanosleep(256);
   }
 }
@@ -338,6 +341,7 @@ __device__ inline bool around_vertex(const Dev& D, int v, ISet& seen, int* stack
   int r = around_vertex_try(D, v, seen, stack, cap, f);
   if (r >= 0) return r > 0;
   reset();
+  atomicAdd(&D.ctr->vq[2], 1ull);
   int s = vpool_acquire(D);
   ISet big;
   size_t o = (size_t)s * D.vp_cap;
@@ -351,9 +355,27 @@ template <class F>
 __device__ inline bool around_vertex(const Dev& D, int v, ISet& seen, int* stack, int cap, F f) {
   return around_vertex(D, v, seen, stack, cap, f, [] {});
 }
+// Visit the tets of edge (u,v) (f(t) may stop early): the DFS around u on the
+// per-thread arena; when u's star outgrows it (a box corner is joined to
+// thousands of hull vertices), the star of v, which holds the same edge tets,
+// on the per-thread arena; only when both overflow, u on a large arena.  The
+// visited set is the same either way; u's stale vert_tet entry is repaired by
+// the first attempt exactly as before.
+template <class F, class R>
+__device__ inline bool around_edge(const Dev& D, int u, int v, ISet& seen, int* stack, int cap, F f, R reset) {
+  auto fu = [&](int t) { return has_v(D.tv[t], v) ? f(t) : false; };
+  int r = around_vertex_try(D, u, seen, stack, cap, fu);
+  if (r >= 0) return r > 0;
+  reset();
+  auto fv = [&](int t) { return has_v(D.tv[t], u) ? f(t) : false; };
+  r = around_vertex_try(D, v, seen, stack, cap, fv);
+  if (r >= 0) return r > 0;
+  reset();
+  return around_vertex(D, u, seen, stack, cap, fu, reset);
+}
 __device__ inline bool edge_exists(const Dev& D, int u, int v, ISet& seen, int* stack, int cap) {
   bool found = false;
-  around_vertex(D, u, seen, stack, cap, [&](int t) { if (has_v(D.tv[t], v)) { found = true; return true; } return false; });
+  around_edge(D, u, v, seen, stack, cap, [&](int) { found = true; return true; }, [] {});
   return found;
 }
 // (t,i) of an alive tet with face {a,b,c} (sorted), or t=-1

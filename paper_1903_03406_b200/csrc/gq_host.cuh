@@ -1723,6 +1723,8 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
                    1e3 * R.vt[0], 1e3 * R.vt[1], 1e3 * R.vt[2], 1e3 * R.vt[3], 1e3 * R.vt[4], R.st_hist[0],
                    R.st_hist[1], R.st_hist[2], R.st_hist[3], R.st_hist[4], R.st_hist[5], R.waves,
                    (double)(c->hc.fb_slow >> 8) / 1.965e6, (int)((c->hc.fb_slow >> 4) & 15), (int)(c->hc.fb_slow & 15));
+      std::fprintf(stderr, "  star queries: stale starts %llu (tets scanned %llu), large-arena reruns %llu, lock spins %llu\n",
+                   c->hc.vq[0], c->hc.vq[1], c->hc.vq[2], c->hc.vq[3]);
       c->hc.fb_slow = 0;
       CK(cudaMemsetAsync(&c->dctr->fb_slow, 0, 8, c->st));
     }

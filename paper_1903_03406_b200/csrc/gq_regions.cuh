@@ -149,6 +149,16 @@ __global__ void __launch_bounds__(32 * WR_WARPS, MINB) k_region_warp(const __gri
       } else if (st == RS_OVERFLOW) C.status[c] = CS_OVF;
       else if (st == RS_MEMBRANE) { C.status[c] = CS_MEMB; C.memb[c] = O.memb; }
       else C.status[c] = CS_CNSS;
+#ifdef GQ_DEBUG2D
+      if (st == RS_CNSS && O.seed < 0 && C.kind[c] == K_SEG) {
+        __shared__ unsigned int dummy; (void)dummy;
+        unsigned int kk = atomicAdd(&D.ctr->fail[4], 0u);
+        int r = C.tgt[c]; int2 e = D.sg_uv[r];
+        if (kk < 1) printf("[noseedseg] cand %d seg rec %d (%d,%d) sid %d fl %x vsid %d %d origin %d %d p %.17g %.17g %.17g\n", c, r, e.x, e.y,
+                           D.sg_sid[r], D.sg_fl[r], D.vsid[e.x], D.vsid[e.y], (int)D.vorigin[e.x], (int)D.vorigin[e.y],
+                           C.p[3 * (size_t)c], C.p[3 * (size_t)c + 1], C.p[3 * (size_t)c + 2]);
+      }
+#endif
     }
     __syncwarp();
   }

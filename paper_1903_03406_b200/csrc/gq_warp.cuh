@@ -123,6 +123,13 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
           printf("[noseed] k %u nseeds %d p %.17g %.17g %.17g seed0 %d alive %d tv %d %d %d %d walk %d insph %d\n", k, nseeds,
                  p[0], p[1], p[2], t0s, (int)D.alive[t0s], q.x, q.y, q.z, q.w, W.seed,
                  q.w == GHOST ? -9 : insphere(PT(D, q.x), PT(D, q.y), PT(D, q.z), PT(D, q.w), p));
+          for (int j = 0; j < 4; ++j) {
+            int v = tvk(q, j);
+            if (v == GHOST) continue;
+            const double* a = PT(D, v);
+            double d2 = (a[0] - p[0]) * (a[0] - p[0]) + (a[1] - p[1]) * (a[1] - p[1]) + (a[2] - p[2]) * (a[2] - p[2]);
+            if (d2 == 0.0) printf("[noseed]   k %u coincides with vertex %d origin %d vsid %d\n", k, v, (int)D.vorigin[v], D.vsid[v]);
+          }
         }
 #else
         (void)k;
