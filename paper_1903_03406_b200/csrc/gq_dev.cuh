@@ -57,7 +57,8 @@ struct Counters {
   int first_real;                    // no alive real tet has a lower index (hint_tet; 0 after compaction)
   unsigned long long t2st[4];        // 2D cavities (diagnostics): computed, walk steps, exhaustive scans, triangles scanned
   unsigned long long fb_slow;        // slowest fallback evaluation (diagnostics): cycles << 8 | outcome << 4 | kind
-  unsigned long long vq[4];          // vertex-star queries (diagnostics): stale-start scans, tets scanned, large-arena reruns, lock spins
+  unsigned long long vq[6];          // vertex-star queries (diagnostics): stale-start scans, tets scanned, large-arena reruns, lock spins;
+                                     // walks past the deterministic cap, their randomised steps
 };
 
 // A tet is one 32-byte record {tv, tn} (vertices, then packed neighbour
@@ -486,9 +487,12 @@ __device__ __noinline__ int walk(const Dev& D, const double* p, int hint) {
     // scan's tie rule locally (lowest_equivalent): same tet, no O(nt) pass.
     unsigned long long r = 0x9E3779B97F4A7C15ull ^ (unsigned long long)t;
     prev = -1;
-    for (int s2 = 0; s2 < 16 * max_steps; ++s2) {
+    atomicAdd(&D.ctr->vq[4], 1ull);
+    int s2 = 0;
+    for (; s2 < 16 * max_steps; ++s2) {
       int4 q = D.tv[t];
       if (q.w == GHOST) break;
+      if ((s2 & 255) == 255) atomicAdd(&D.ctr->vq[5], 256ull);
       r = r * 6364136223846793005ull + 1442695040888963407ull;
       int off = (int)(r >> 62);
       bool moved = false;

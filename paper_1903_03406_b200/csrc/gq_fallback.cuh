@@ -5,7 +5,9 @@
 // ---------------------------------------------------------------------------
 // sequential fallback for failed candidates (refine.py:748-799): one thread,
 // in pool order, on the updated mesh.  Uses the big scratch / slab 0.
-struct FallbackIO { const int* list; int n; int round_no; unsigned long long seed; int with_facets; double lmin2; int* inserted; };
+struct FallbackIO { const int* list; int n; int round_no; unsigned long long seed; int with_facets; double lmin2; int* inserted;
+                   int window;   // candidates evaluated per wave (waves)
+};
 
 __device__ inline void mark_enc_face_key(const Dev& D, int a, int b, int c) {
   sort3(a, b, c);
@@ -249,14 +251,17 @@ __global__ void k_fallback(const __grid_constant__ Dev D, const __grid_constant_
   for (int k = 0; k < F.n; ++k) fallback_eval(D, C, S, F, T, L, k, true, &arg);
 }
 
-// wave step 1: outcomes of candidates [start, n) on the current mesh, and the
-// first one that breaks the wave (atomicMin into *first, preset to n)
+// wave step 1: outcomes of the window [start, start + F.window) on the current
+// mesh, and the first one that breaks the wave (atomicMin into *first, preset
+// to the window's end).  The window keeps a slow evaluation late in the list
+// (a subsegment whose midpoint walk crosses the box gap: ~25 ms on one thread)
+// from being repeated in every wave.
 __global__ void k_fb_scan(const __grid_constant__ Dev D, const __grid_constant__ Cand C, const __grid_constant__ Scr SC,
                           FallbackIO F, T2Items T, SkipLog L, const int* startp, int* out, int* first) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   Scratch S = scratch_for(SC, tid);
-  const int start = *startp;
-  for (int k = start + tid; k < F.n; k += gridDim.x * blockDim.x) {
+  const int start = *startp, wend = min(F.n, start + F.window);
+  for (int k = start + tid; k < wend; k += gridDim.x * blockDim.x) {
     int arg = -1;
     long long t0 = clock64();
     int o = fallback_eval(D, C, S, F, T, L, k, false, &arg);
@@ -268,11 +273,12 @@ __global__ void k_fb_scan(const __grid_constant__ Dev D, const __grid_constant__
 }
 
 // wave step 2 (one thread): apply the outcomes of [start, first) in list order,
-// then the full sequential body for candidate first; *startp = first + 1
+// then the full sequential body for candidate first when it broke the window;
+// the next wave starts after it (or at the window's end)
 __global__ void k_fb_apply(const __grid_constant__ Dev D, const __grid_constant__ Cand C, Scr SCB, FallbackIO F, T2Items T,
                            SkipLog L, int* startp, const int* out, int* first) {
   if (blockIdx.x || threadIdx.x) return;
-  const int start = *startp, f = *first;
+  const int start = *startp, f = *first, wend = min(F.n, start + F.window);
   for (int k = start; k < f; ++k) {
     int c = F.list[k];
     int kind = C.kind[c], tgt = C.tgt[c];
@@ -294,13 +300,15 @@ __global__ void k_fb_apply(const __grid_constant__ Dev D, const __grid_constant_
       else if (kind == K_FACE) D.sf_fl[tgt] |= RF_BLOCK;
     }
   }
-  if (f < F.n) {
+  int next = wend;
+  if (f < wend) {
     Scratch S = scratch_for(SCB, 0);
     int arg = 0;
     fallback_eval(D, C, S, F, T, L, f, true, &arg);
+    next = f + 1;
   }
-  *startp = f + 1;
-  *first = F.n;
+  *startp = next;
+  *first = min(F.n, next + F.window);
 }
 
 // accepted tets whose region has a too-short boundary edge (refine.py:891-894)

@@ -135,6 +135,7 @@ static const bool o_filter_launches = getenv("GQ_FILTER_LAUNCHES") != nullptr;
 static const bool o_thread_init = getenv("GQ_THREAD_INIT") != nullptr;
 static const bool o_init_launches = getenv("GQ_INIT_LAUNCHES") != nullptr;
 static const bool o_fallback_serial = getenv("GQ_FALLBACK_SERIAL") != nullptr;   // one-thread fallback loop (comparisons)
+static const int o_fb_window = getenv("GQ_FB_WINDOW") ? std::max(1, atoi(getenv("GQ_FB_WINDOW"))) : 1024;   // fallback wave window
 static const int o_trace_from = getenv("GQ_TRACE_FROM") ? atoi(getenv("GQ_TRACE_FROM")) : -1;
 static const bool g_grid_thread = getenv("GQ_GRID_THREAD") != nullptr;   // experiments: thread-per-query grid kernels
 static thread_local bool g_fine = false;      // GQ_PROFILE=2: host clock after a sync per stage
@@ -1479,11 +1480,12 @@ static RoundOut run_round(gq_ctx* c, int round_no) {
     } else {
       // waves (gq_fallback.cuh): parallel evaluation, in-order application
       int* out = dmalloc<int>(2 * (size_t)nfail);
-      int h0[2] = {0, nfail};
+      F.window = o_fb_window;
+      int h0[2] = {0, std::min(nfail, F.window)};
       CK(cudaMemcpyAsync(c->d_int + 24, h0, 8, cudaMemcpyHostToDevice, c->st));
       int start = 0, waves = 0;
       while (start < nfail) {
-        LAUNCH_S(k_fb_scan, nfail - start, c->D, c->C, c->S, F, c->T, c->L, c->d_int + 24, out, c->d_int + 25);
+        LAUNCH_S(k_fb_scan, std::min(nfail - start, F.window), c->D, c->C, c->S, F, c->T, c->L, c->d_int + 24, out, c->d_int + 25);
         k_fb_apply<<<1, 1, 0, c->st>>>(c->D, c->C, c->SB, F, c->T, c->L, c->d_int + 24, out, c->d_int + 25);
         c->launches++;
         CK(cudaGetLastError());
@@ -1723,8 +1725,9 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
                    1e3 * R.vt[0], 1e3 * R.vt[1], 1e3 * R.vt[2], 1e3 * R.vt[3], 1e3 * R.vt[4], R.st_hist[0],
                    R.st_hist[1], R.st_hist[2], R.st_hist[3], R.st_hist[4], R.st_hist[5], R.waves,
                    (double)(c->hc.fb_slow >> 8) / 1.965e6, (int)((c->hc.fb_slow >> 4) & 15), (int)(c->hc.fb_slow & 15));
-      std::fprintf(stderr, "  star queries: stale starts %llu (tets scanned %llu), large-arena reruns %llu, lock spins %llu\n",
-                   c->hc.vq[0], c->hc.vq[1], c->hc.vq[2], c->hc.vq[3]);
+      std::fprintf(stderr, "  star queries: stale starts %llu (tets scanned %llu), large-arena reruns %llu, lock spins %llu;"
+                   " walks past the cap %llu (randomised steps ~%llu)\n",
+                   c->hc.vq[0], c->hc.vq[1], c->hc.vq[2], c->hc.vq[3], c->hc.vq[4], c->hc.vq[5]);
       c->hc.fb_slow = 0;
       CK(cudaMemsetAsync(&c->dctr->fb_slow, 0, 8, c->st));
     }

@@ -1,7 +1,8 @@
 """The sequential fallback (refine.py:748-806, called in failed-list order at
 refine.py:897-902) runs on the device in waves: a side-effect-free parallel
 evaluation of every remaining failed candidate, then an in-order application
-up to the first candidate that inserts (gq_fallback.cuh).  These tests run the
+up to the first candidate that inserts, a window of candidates per wave
+(gq_fallback.cuh).  These tests run the
 same refinements with the one-thread loop (GQ_FALLBACK_SERIAL=1, read when the
 library loads, hence a subprocess per mode) and require identical meshes:
 points, tets, constraint sets, per-round rows and the skip list."""
@@ -43,11 +44,14 @@ print(json.dumps({"hash": h.hexdigest(), "steiner": rep.steiner_points, "rows": 
 """
 
 
-def _run(case: str, serial: bool) -> dict:
+def _run(case: str, serial: bool, window: int = 0) -> dict:
     env = dict(os.environ)
     env.pop("GQ_FALLBACK_SERIAL", None)
+    env.pop("GQ_FB_WINDOW", None)
     if serial:
         env["GQ_FALLBACK_SERIAL"] = "1"
+    if window:
+        env["GQ_FB_WINDOW"] = str(window)
     out = subprocess.run([sys.executable, "-c", _WORKER, ROOT, case], env=env, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
@@ -58,6 +62,9 @@ def _run(case: str, serial: bool) -> dict:
 def test_fallback_waves_equal_serial_loop(case):
     waves = _run(case, serial=False)
     serial = _run(case, serial=True)
+    narrow = _run(case, serial=False, window=3)    # many windows without a break
+    assert narrow["hash"] == serial["hash"] and narrow["rows"] == serial["rows"]
+    assert narrow["skipped"] == serial["skipped"]
     if case != "c2":
         assert sum(r[4] for r in waves["rows"]) > 0, "no failed candidate: the fallback was not exercised"
     assert waves["rows"] == serial["rows"]
