@@ -57,12 +57,11 @@ __device__ __noinline__ void insert_one(const Dev& D, const Cand& C, int c, Scra
       int pid = fpid >= 0 ? fpid : D.segpoly[o0 + k];
       Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = vid; X.follow3d = D.poly_obl[pid];
       proj2(D, pid, p, X.p);
-      int forced[CC + 2]; int nf;
-      t2_forced(D, C, c, pid, forced, nf, CC + 2);
-      int seeds[CC + 3]; int ns = 0;
-      for (int j = 0; j < nf; ++j) seeds[ns++] = forced[j];
+      int forced[T2_FCAP + 1]; int nf;    // the crossed triangles, then (seeds) the target's own
+      t2_forced(D, C, c, pid, forced, nf, T2_FCAP);
+      const int* seeds = forced; int ns = nf;
       int ts = t2_seed_of(D, C, c, pid);
-      if (ts >= 0) seeds[ns++] = ts;
+      if (ts >= 0) forced[ns++] = ts;
       int* cav = T.cav + (size_t)w * T.cap;
       int n = tri2_cavity(X, forced, nf, seeds, ns, S.tset, cav, S.stack, T.cap);
       if (n < 0) {

@@ -428,7 +428,8 @@ static void alloc_mesh(gq_ctx* c, int n, int m, int f, int npidx) {
   c->W.own = dmalloc<int>(5 * tcap + sgcap);
   CK(cudaMemsetAsync(c->W.own, 0x7f, (5 * tcap + sgcap) * 4, c->st));
   // 2D items
-  c->T.cap = 256; c->T.rcap = 128;
+  c->T.cap = T2_CAP; c->T.rcap = T2_CAP;
+  static_assert(T2_CAP <= CT * 2, "tri2_cavity: DFS stack + component marks (2 * T2_CAP) must fit the 2 * Scratch.cap stack");
   c->T.icap = 0;
   c->T.cand = c->T.pid = c->T.state = c->T.ncav = c->T.nrem = c->T.cav = c->T.rem = nullptr;   // freed by free_all
   ensure_items(c, 1 << 16);

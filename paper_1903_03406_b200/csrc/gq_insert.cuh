@@ -150,6 +150,11 @@ __device__ __noinline__ bool collinear_sliver(const Dev& D, int a, int b, int c)
 }
 
 // 2D retiling work items: (candidate, polygon)
+// per-item capacities of the facet retiling: crossed triangles of one polygon
+// (local array), and 2D cavity triangles (T.cap; tri2_cavity's DFS stack and
+// component marks take 2 * T.cap of the thread's 2 * Scratch.cap stack)
+#define T2_FCAP 256
+#define T2_CAP 512
 struct T2Items {
   int* cand; int* pid; int* state; int n;   // state 0 pending, 1 done
   int* cav; int* ncav; int cap;             // per item cavity tids
@@ -170,12 +175,13 @@ __device__ __noinline__ void t2_forced(const Dev& D, const Cand& C, int c, int p
     // triangle with directed edge a->b or b->a holding c
     int t = he_lookup(D, f.x, f.y, pid);
     if (t < 0 || !(D.t2v[t].x == f.z || D.t2v[t].y == f.z || D.t2v[t].z == f.z)) t = he_lookup(D, f.y, f.x, pid);
-    if (t >= 0 && nf < cap) forced[nf++] = t;
+    if (t < 0) continue;
+    if (nf < cap) forced[nf++] = t; else raise_err(GQ_ERR_CAP);   // never drop a crossed triangle silently
   }
   if (C.kind[c] == K_SEG) {   // split edge triangles (facets.py:310-315)
     int2 e = D.sg_uv[C.tgt[c]];
-    int t1 = he_lookup(D, e.x, e.y, pid); if (t1 >= 0 && nf < cap) forced[nf++] = t1;
-    int t2 = he_lookup(D, e.y, e.x, pid); if (t2 >= 0 && nf < cap) forced[nf++] = t2;
+    int t1 = he_lookup(D, e.x, e.y, pid); if (t1 >= 0) { if (nf < cap) forced[nf++] = t1; else raise_err(GQ_ERR_CAP); }
+    int t2 = he_lookup(D, e.y, e.x, pid); if (t2 >= 0) { if (nf < cap) forced[nf++] = t2; else raise_err(GQ_ERR_CAP); }
   }
 }
 __device__ __noinline__ int t2_seed_of(const Dev& D, const Cand& C, int c, int pid) {
@@ -198,12 +204,11 @@ __device__ void t2_compute_body(const Dev& D, const Cand& C, const T2Items& T, S
     int c = T.cand[w], pid = T.pid[w];
     Tri2Ctx X; X.D = &D; X.pid = pid; X.vid = C.vid[c]; X.follow3d = D.poly_obl[pid];
     proj2(D, pid, C.p + 3 * (size_t)c, X.p);
-    int forced[CC + 2]; int nf;
-    t2_forced(D, C, c, pid, forced, nf, CC + 2);
-    int seeds[CC + 3]; int ns = 0;
-    for (int k = 0; k < nf; ++k) seeds[ns++] = forced[k];
+    int forced[T2_FCAP + 1]; int nf;      // the crossed triangles, then (seeds) the target's own
+    t2_forced(D, C, c, pid, forced, nf, T2_FCAP);
+    const int* seeds = forced; int ns = nf;
     int ts = t2_seed_of(D, C, c, pid);
-    if (ts >= 0) seeds[ns++] = ts;
+    if (ts >= 0) forced[ns++] = ts;
     int n = tri2_cavity(X, forced, nf, seeds, ns, S.tset, T.cav + (size_t)w * T.cap, S.stack, T.cap);
     if (n < 0) {
 #ifdef GQ_DEBUG2D
