@@ -40,6 +40,7 @@ __device__ inline Scratch scratch_for(const Scr& s, int tid) {
   S.fset.cur = s.epoch + 2 * tid + 1; S.fset.cap = s.fcap;
   S.list = s.list + (size_t)tid * s.cap; S.stack = s.stack + (size_t)tid * 2 * s.cap;
   S.in = s.in + (size_t)tid * s.cap; S.comp = s.comp + (size_t)tid * s.cap; S.cap = s.cap;
+  S.cancel = nullptr; S.me = 0;
   return S;
 }
 

@@ -701,6 +701,10 @@ struct Scratch {     // per-thread scratch views
   uint8_t* in;
   uint8_t* comp;
   int cap;           // max tets
+  // fallback scan (k_fb_scan): the evaluation of list entry `me` is abandoned
+  // once an earlier entry has broken the wave (*cancel < me); null elsewhere
+  const int* cancel;
+  int me;
 };
 
 struct RegionOut {   // output slab views (capacities given)
@@ -748,6 +752,7 @@ __device__ __noinline__ int region_compute(const Dev& D, const double* p, const 
   int sp = 0;
   S.stack[sp++] = seed;
   while (sp > 0) {
+    if (S.cancel && (sp & 15) == 0 && *(const volatile int*)S.cancel < S.me) return RS_CNSS;   // result unused
     int t = S.stack[--sp];
     for (int i = 0; i < 4; ++i) {
       int u = tnk(D, t, i) >> 2;

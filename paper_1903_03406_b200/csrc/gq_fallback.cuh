@@ -262,6 +262,8 @@ __global__ void k_fb_scan(const __grid_constant__ Dev D, const __grid_constant__
   const int start = *startp, wend = min(F.n, start + F.window);
   for (int k = start + tid; k < wend; k += gridDim.x * blockDim.x) {
     int arg = -1;
+    S.cancel = first; S.me = k;
+    if (*(const volatile int*)first < k) { out[2 * k] = FB_CNSS; out[2 * k + 1] = -1; continue; }   // unused
     long long t0 = clock64();
     int o = fallback_eval(D, C, S, F, T, L, k, false, &arg);
     unsigned long long dt = (unsigned long long)(clock64() - t0);
