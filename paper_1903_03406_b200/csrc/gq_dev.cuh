@@ -57,8 +57,9 @@ struct Counters {
   int first_real;                    // no alive real tet has a lower index (hint_tet; 0 after compaction)
   unsigned long long t2st[4];        // 2D cavities (diagnostics): computed, walk steps, exhaustive scans, triangles scanned
   unsigned long long fb_slow;        // slowest fallback evaluation (diagnostics): cycles << 8 | outcome << 4 | kind
-  unsigned long long vq[6];          // vertex-star queries (diagnostics): stale-start scans, tets scanned, large-arena reruns, lock spins;
-                                     // walks past the deterministic cap, their randomised steps
+  unsigned long long vq[11];          // vertex-star queries (diagnostics): stale-start scans, tets scanned, large-arena reruns, lock spins;
+                                     // walks past the deterministic cap, their randomised steps;
+                                     // fallback evaluations over 10 ms: kcycles in make_cand / hull walk / seeds / region, count
 };
 
 // A tet is one 32-byte record {tv, tn} (vertices, then packed neighbour

@@ -165,7 +165,9 @@ __device__ __noinline__ int fallback_eval(const Dev& D, const Cand& C, Scratch& 
     if (commit) { atomicAdd(&D.ctr->fail[5], 1u); skip_cand(D, C, c, 3, F.round_no, L, skip_order(2, k)); }
     return FB_OVF;
   }
+  long long tc0 = clock64();
   if (!make_cand(D, C, c, X, S)) { if (commit) raise_err(GQ_ERR_DEGEN); return commit ? FB_NONE : FB_BREAK; }
+  long long tc1 = clock64(), tc2 = tc1;
   const double* p = C.p + 3 * (size_t)c;
   if (kind == K_TET) {
     int cur = tgt, prev = -1, hull = -2;
@@ -198,13 +200,21 @@ __device__ __noinline__ int fallback_eval(const Dev& D, const Cand& C, Scratch& 
       return FB_HULL;
     }
   }
+  tc2 = clock64();
   C.bigi[c] = commit ? 0 : -1;     // sequential: big slab 0; scan: the candidate's own slab
   SlabView sv = slab(C, c);
   RegionOut O = region_view(C, c, sv, 0);
   int seeds[32];
   int ns = cand_seeds(D, C, c, seeds, S);
   atomicAdd(&D.ctr->region_calls, 1ull);
+  long long tc3 = clock64();
   int st = ns == 0 ? RS_CNSS : region_compute(D, p, seeds, ns, allow_of(C, c), S, O);
+  long long tc4 = clock64();
+  if (!commit && tc4 - tc0 > 19650000ll) {   // diagnostics: where a slow evaluation spends its time
+    atomicAdd(&D.ctr->vq[6], (unsigned long long)((tc1 - tc0) >> 10)); atomicAdd(&D.ctr->vq[7], (unsigned long long)((tc2 - tc1) >> 10));
+    atomicAdd(&D.ctr->vq[8], (unsigned long long)((tc3 - tc2) >> 10)); atomicAdd(&D.ctr->vq[9], (unsigned long long)((tc4 - tc3) >> 10));
+    atomicAdd(&D.ctr->vq[10], 1ull);
+  }
   store_region(C, c, O);
   if (st == RS_OK) {
     if (O.mind <= D.too_close_sq) { if (commit) skip_cand(D, C, c, 2, F.round_no, L, skip_order(2, k)); return FB_TOOCLOSE; }

@@ -1729,6 +1729,8 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
       std::fprintf(stderr, "  star queries: stale starts %llu (tets scanned %llu), large-arena reruns %llu, lock spins %llu;"
                    " walks past the cap %llu (randomised steps ~%llu)\n",
                    c->hc.vq[0], c->hc.vq[1], c->hc.vq[2], c->hc.vq[3], c->hc.vq[4], c->hc.vq[5]);
+      std::fprintf(stderr, "  slow fallback evaluations: %llu, Mcycles make %.1f hull walk %.1f seeds %.1f region %.1f\n",
+                   c->hc.vq[10], c->hc.vq[6] / 1024.0, c->hc.vq[7] / 1024.0, c->hc.vq[8] / 1024.0, c->hc.vq[9] / 1024.0);
       c->hc.fb_slow = 0;
       CK(cudaMemsetAsync(&c->dctr->fb_slow, 0, 8, c->st));
     }
