@@ -22,8 +22,13 @@
 
 namespace gq {
 
-// device-wide sticky error word (bit flags, see gq_main.cu ERR_*)
+// device-wide error record: the bits ever raised (for the message) and a count
+// of raises that is never reset.  A context takes the count at the start of a
+// call and fails when it has grown: concurrent contexts (C5) never wipe or lose
+// each other's errors (an error raised by one is also reported by the others
+// running at that time; every error is fatal).
 __device__ unsigned int g_err;
+__device__ unsigned long long g_errn;
 #define GQ_ERR_BIGINT 1u
 #define GQ_ERR_DEGEN 2u
 #define GQ_ERR_CAP 4u
@@ -31,7 +36,7 @@ __device__ unsigned int g_err;
 #define GQ_ERR_STAR 16u
 #define GQ_ERR_WALK 32u
 #define GQ_ERR_2D 64u
-__device__ __forceinline__ void raise_err_(unsigned int e) { atomicOr(&g_err, e); }
+__device__ __forceinline__ void raise_err_(unsigned int e) { atomicOr(&g_err, e); atomicAdd(&g_errn, 1ull); }
 #ifdef GQ_DEBUG2D
 #define raise_err(e) do { printf("[err] %u at %s:%d\n", (unsigned)(e), __FILE__, __LINE__); raise_err_(e); } while (0)
 #else

@@ -73,6 +73,7 @@ template <class T> static T* dmalloc(size_t n) {
 struct gq_ctx {
   DevCache cache;
   char* pin = nullptr; size_t pin_cap = 0, pin_used = 0;                 // pinned read-back staging
+  unsigned long long errn0 = 0;                                           // device error count at the call's start
   std::vector<std::tuple<void*, size_t, size_t>> staged;
   int device = 0;
   cudaStream_t st = nullptr;
@@ -172,18 +173,27 @@ static void stage(gq_ctx* c, void* dst, const void* src, size_t bytes) {
 static void sync(gq_ctx* c) {
   // the error word travels with the stream too (cudaMemcpyFromSymbol would use the legacy stream)
   const size_t eoff = c->pin_cap - 16;
-  CK(cudaMemcpyFromSymbolAsync(c->pin + eoff, g_err, sizeof(unsigned int), 0, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyFromSymbolAsync(c->pin + eoff, g_errn, sizeof(unsigned long long), 0, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyFromSymbolAsync(c->pin + eoff + 8, g_err, sizeof(unsigned int), 0, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   for (auto& s : c->staged) std::memcpy(std::get<0>(s), c->pin + std::get<1>(s), std::get<2>(s));
   c->staged.clear();
   c->pin_used = 0;
+  unsigned long long n = 0;
   unsigned int e = 0;
-  std::memcpy(&e, c->pin + eoff, sizeof(e));
-  if (e) {
+  std::memcpy(&n, c->pin + eoff, sizeof(n));
+  std::memcpy(&e, c->pin + eoff + 8, sizeof(e));
+  if (n != c->errn0) {
+    c->errn0 = n;   // reported once; the next call starts from here
     char buf[128];
     std::snprintf(buf, sizeof buf, "device error flags 0x%x", e);
     throw std::runtime_error(buf);
   }
+}
+// error baseline of a call (after the stream's earlier work)
+static void err_baseline(gq_ctx* c) {
+  CK(cudaMemcpyFromSymbolAsync(&c->errn0, g_errn, sizeof(unsigned long long), 0, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
 }
 static void pull(gq_ctx* c) { stage(c, &c->hc, c->dctr, sizeof(Counters)); sync(c); }
 // the mesh / record counts only: the instrumentation counters are device-owned
@@ -1556,8 +1566,7 @@ static void refine_impl(gq_ctx* c, const double* xyz, int n, int n_input, const 
   c->n_input = n_input; c->npoly = f;
   c->rounds.clear(); c->rtimes.clear(); c->launches = 0; c->region_ms = 0;
   free_all(c);
-  unsigned int zero = 0;
-  CK(cudaMemcpyToSymbolAsync(g_err, &zero, 4, 0, cudaMemcpyHostToDevice, c->st));
+  err_baseline(c);   // (g_err / g_errn are never reset: other contexts may be running)
   unsigned long long z4[4] = {0, 0, 0, 0};
   CK(cudaMemcpyToSymbolAsync(g_exact_calls, z4, 32, 0, cudaMemcpyHostToDevice, c->st));
   int npidx = f > 0 ? poff[f] : 0;

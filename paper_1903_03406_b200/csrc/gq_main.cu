@@ -71,6 +71,7 @@ int gq_create(int device, gq_ctx** out) {
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     c->pin_cap = size_t(1) << 20;   // read-back staging (counters, scan tails, overflow lists)
     CK(cudaHostAlloc((void**)&c->pin, c->pin_cap, cudaHostAllocDefault));
+    err_baseline(c);   // errors raised before this context existed are not its own
     CK(cudaEventCreate(&c->ev0)); CK(cudaEventCreate(&c->ev1));
     CK(cudaEventCreate(&c->er0)); CK(cudaEventCreate(&c->er1));
     CK(cudaDeviceSetLimit(cudaLimitStackSize, 24576));   // k_fallback: ~18 KB (exact predicates on 40-limb integers)
@@ -255,6 +256,8 @@ int gq_certify_pairs(int device, const double* xyz, int32_t n, const int32_t* se
     *status = 0; *n_pairs = 0;
     int nf = m + f;
     if (nf < 2) return GQ_OK;
+    unsigned long long errn0 = 0, errn1 = 0;   // error count baseline (g_err is never reset, gq_host.cuh sync)
+    CK(cudaMemcpyFromSymbol(&errn0, g_errn, 8));
     double* dP = dmalloc<double>(3 * (size_t)n);
     int* dseg = dmalloc<int>(2 * (size_t)std::max(m, 1));
     int* dtri = dmalloc<int>(3 * (size_t)std::max(f, 1));
@@ -305,8 +308,8 @@ int gq_certify_pairs(int device, const double* xyz, int32_t n, const int32_t* se
     if (nbig) k_cert_big<<<grid_for((long long)nbig * nf, 128, 148 * 32), 128>>>(I, big, nbig, O);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
-    unsigned int e = 0;
-    CK(cudaMemcpyFromSymbol(&e, g_err, 4));
+    CK(cudaMemcpyFromSymbol(&errn1, g_errn, 8));
+    const bool e = errn1 != errn0;
     CK(cudaMemcpy(h, scal + 1, 8, cudaMemcpyDeviceToHost));
     int np = std::min(h[1], cap);
     if (np && pairs) CK(cudaMemcpy(pairs, dpairs, 8 * (size_t)np, cudaMemcpyDeviceToHost));
