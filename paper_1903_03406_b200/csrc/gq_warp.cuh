@@ -83,6 +83,34 @@ __device__ inline int wh_find(const WS& W, int k) {
   return -1;
 }
 
+// bf_open_part for a warp with the boundary faces' vertex triples staged in
+// shared memory first (the cavity hash is free at this point and is cleared
+// again right after): the pairing count reads shared memory instead of
+// gathering every face's vertices from the mesh nbf times.  Same answer.
+__device__ inline bool bf_open_warp(const Dev& D, const int* bf, int nbf, int* sh, int shcap, int lane) {
+  if (3 * nbf > shcap) return __any_sync(0xffffffffu, bf_open_part(D, bf, nbf, lane, 32));
+  for (int k = lane; k < nbf; k += 32) {
+    int f[3]; face_verts(D.tv[bf[k] >> 2], bf[k] & 3, f);
+    sh[3 * k] = f[0]; sh[3 * k + 1] = f[1]; sh[3 * k + 2] = f[2];
+  }
+  __syncwarp();
+  bool open = false;
+  for (int k = lane; k < nbf && !open; k += 32) {
+    for (int e = 0; e < 3 && !open; ++e) {
+      const int x = sh[3 * k + e], y = sh[3 * k + (e + 1) % 3];
+      int cnt = 0;
+      for (int j = 0; j < nbf && cnt <= 2; ++j) {
+        const int a = sh[3 * j], b = sh[3 * j + 1], c = sh[3 * j + 2];
+        cnt += (a == x || b == x || c == x) && (a == y || b == y || c == y);
+      }
+      open = cnt != 2;
+    }
+  }
+  const bool r = __any_sync(0xffffffffu, open);
+  __syncwarp();
+  return r;
+}
+
 // All 32 lanes of the warp call this with the same arguments.  S is the
 // warp's global scratch (lane 0 only: walks and the constraint pass).
 template <int MAXT, int HASH>
@@ -340,7 +368,7 @@ __device__ inline int region_warp(const Dev& D, const double* p, const int* seed
   __syncwarp();
 #ifndef GQ_NO_GHOSTCHECK
   // (bulk construction skips it: its hull is the convex hull of exact input points)
-  if (check_ghost && W.ghost && __any_sync(FULL, bf_open_part(D, O.bf, nbf, lane, 32))) {
+  if (check_ghost && W.ghost && bf_open_warp(D, O.bf, nbf, W.hkey, WR_HASH, lane)) {
     if (lane == 0) atomicAdd(&D.ctr->fail[3], 1u);
     return RS_BADSTAR;
   }
